@@ -1,0 +1,154 @@
+"""Structured hexahedral mesh, deformation map, Jacobians and DoF numbering.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+* Cells are images of [-1,1]^3.  The configs use the box [0,1]^3
+  split into n[0] x n[1] x n[2] cells, optionally deformed by
+  x_d = xhat_d + eps * s(xhat),  s = prod_e sin(pi t_e),  t_e = (xhat_e-lo_e)/(hi_e-lo_e)
+  (BASELINE.json configs[1], configs[4]; SURVEY §8c reading R2: s is evaluated at
+  the undeformed point, same map on every multigrid level).
+* J = dx/dxi is the analytic derivative of that composed map (chain rule);
+  the oracle inverts it with numpy.linalg (no closed form shared with the GPU).
+* CG numbering: node (k*cx+i, k*cy+j, k*cz+l), x fastest.
+  DG numbering: cell*(k+1)^3 + (i + n*j + n^2*l), cells lexicographic, x fastest.
+* Boundary sides are ordered -x,+x,-y,+y,-z,+z; 0 = Dirichlet, 1 = Neumann.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .basis import lagrange, lagrange_deriv
+
+CG, SIPG = 0, 1
+DIRICHLET, NEUMANN = 0, 1
+
+
+class Mesh:
+    def __init__(self, n, k, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0), eps=0.0,
+                 bc=(DIRICHLET,) * 6):
+        self.n = tuple(int(v) for v in n)
+        self.k = int(k)
+        self.lo = np.asarray(lo, dtype=np.float64)
+        self.hi = np.asarray(hi, dtype=np.float64)
+        self.eps = float(eps)
+        self.bc = tuple(int(b) for b in bc)
+        self.h = (self.hi - self.lo) / np.asarray(self.n, dtype=np.float64)
+        self.n_cells = self.n[0] * self.n[1] * self.n[2]
+        self.nn = tuple(self.k * m + 1 for m in self.n)       # CG nodes per direction
+
+    # ---- cells -------------------------------------------------------------
+    def cell_coords(self, cells=None):
+        """(cx, cy, cz) of lexicographic cell ids (x fastest)."""
+        if cells is None:
+            cells = np.arange(self.n_cells)
+        cells = np.asarray(cells)
+        cx = cells % self.n[0]
+        cy = (cells // self.n[0]) % self.n[1]
+        cz = cells // (self.n[0] * self.n[1])
+        return np.stack([cx, cy, cz], axis=-1)
+
+    def cell_id(self, c):
+        c = np.asarray(c)
+        return c[..., 0] + self.n[0] * (c[..., 1] + self.n[1] * c[..., 2])
+
+    # ---- geometry ----------------------------------------------------------
+    def xhat(self, cc, xi):
+        """Undeformed point of reference point xi [P,3] in cells cc [C,3] -> [C,P,3]."""
+        return self.lo + self.h * (cc[:, None, :] + 0.5 * (xi[None, :, :] + 1.0))
+
+    def _t(self, xh):
+        return (xh - self.lo) / (self.hi - self.lo)
+
+    def phys(self, xh):
+        """x = xhat + eps * s(xhat) * (1,1,1)."""
+        s = np.prod(np.sin(np.pi * self._t(xh)), axis=-1)
+        return xh + self.eps * s[..., None]
+
+    def jacobian(self, cc, xi):
+        """J[c, p, d, e] = d x_d / d xi_e  at reference points xi [P,3] of cells cc."""
+        xh = self.xhat(cc, xi)
+        t = self._t(xh)
+        sn = np.sin(np.pi * t)
+        cs = np.cos(np.pi * t)
+        # ds/dxhat_e = pi/(hi_e-lo_e) cos(pi t_e) prod_{f != e} sin(pi t_f)
+        grad_s = np.empty_like(xh)
+        for e in range(3):
+            others = [f for f in range(3) if f != e]
+            grad_s[..., e] = (np.pi / (self.hi[e] - self.lo[e])) * cs[..., e] \
+                * sn[..., others[0]] * sn[..., others[1]]
+        dxdxh = np.eye(3)[None, None] + self.eps * grad_s[..., None, :]  # [.., d, e]
+        return dxdxh * (0.5 * self.h)[None, None, None, :]
+
+    # ---- numbering ---------------------------------------------------------
+    def cg_n_dofs(self):
+        return self.nn[0] * self.nn[1] * self.nn[2]
+
+    def dg_n_dofs(self):
+        return self.n_cells * (self.k + 1) ** 3
+
+    def cg_dofmap(self, cells=None):
+        """[C, n^3] global CG indices of the local nodes (i + n j + n^2 l)."""
+        cc = self.cell_coords(cells)
+        n, k = self.k + 1, self.k
+        l0 = np.arange(n)
+        gx = k * cc[:, 0, None] + l0[None, :]
+        gy = k * cc[:, 1, None] + l0[None, :]
+        gz = k * cc[:, 2, None] + l0[None, :]
+        idx = (gx[:, None, None, :] + self.nn[0] * (gy[:, None, :, None]
+               + self.nn[1] * gz[:, :, None, None]))
+        return idx.reshape(len(cc), n ** 3)
+
+    def dg_dofmap(self, cells=None):
+        if cells is None:
+            cells = np.arange(self.n_cells)
+        cells = np.asarray(cells)
+        m = (self.k + 1) ** 3
+        return cells[:, None] * m + np.arange(m)[None, :]
+
+    def cg_node_coords(self):
+        """Integer node coordinates (gx, gy, gz) of all CG nodes."""
+        i = np.arange(self.cg_n_dofs())
+        gx = i % self.nn[0]
+        gy = (i // self.nn[0]) % self.nn[1]
+        gz = i // (self.nn[0] * self.nn[1])
+        return np.stack([gx, gy, gz], axis=-1)
+
+    def cg_dirichlet_mask(self):
+        """True on CG nodes lying on a Dirichlet side."""
+        g = self.cg_node_coords()
+        mask = np.zeros(len(g), dtype=bool)
+        for d in range(3):
+            if self.bc[2 * d] == DIRICHLET:
+                mask |= g[:, d] == 0
+            if self.bc[2 * d + 1] == DIRICHLET:
+                mask |= g[:, d] == self.nn[d] - 1
+        return mask
+
+
+def tensor_points(p1d):
+    """3-D tensor grid of a 1-D point set, x fastest: [n^3, 3]."""
+    n = len(p1d)
+    q = np.arange(n ** 3)
+    return np.stack([p1d[q % n], p1d[(q // n) % n], p1d[q // (n * n)]], axis=-1)
+
+
+def tensor_weights(w1d):
+    n = len(w1d)
+    q = np.arange(n ** 3)
+    return w1d[q % n] * w1d[(q // n) % n] * w1d[q // (n * n)]
+
+
+def eval_basis_3d(nodes, pts):
+    """Tensor Lagrange basis phi_i(xi) = phi_i0(a) phi_i1(b) phi_i2(c) and its
+    reference gradient, evaluated POINTWISE at arbitrary points pts [P,3].
+    Returns val [P, n^3] and grad [P, 3, n^3]; local index i = i0 + n i1 + n^2 i2."""
+    n = len(nodes)
+    v = [lagrange(nodes, pts[:, d]) for d in range(3)]          # [P, n]
+    g = [lagrange_deriv(nodes, pts[:, d]) for d in range(3)]
+    i = np.arange(n ** 3)
+    i0, i1, i2 = i % n, (i // n) % n, i // (n * n)
+    val = v[0][:, i0] * v[1][:, i1] * v[2][:, i2]
+    grad = np.stack([g[0][:, i0] * v[1][:, i1] * v[2][:, i2],
+                     v[0][:, i0] * g[1][:, i1] * v[2][:, i2],
+                     v[0][:, i0] * v[1][:, i1] * g[2][:, i2]], axis=1)
+    return val, grad

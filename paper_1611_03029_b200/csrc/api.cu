@@ -1,0 +1,868 @@
+// libfem C ABI (include/fem.h): setup, operator entry points, V-cycle, PCG.
+//
+// Host orchestration only: every arithmetic step on vectors runs in the kernels
+// of kernels_cg.cu / kernels_dg.cu / kernels_mg.cu.  The host does the O(1)
+// scalar work of the paper's algorithms: Chebyshev coefficients,
+// the 15x15 Lanczos eigenvalue problem, the PCG stopping test
+// (P:L1146-1148), and the tiny dense Cholesky factorisation of the coarse
+// matrix (R9), which is assembled on the device by the level-0 operator.
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace fem {
+
+void launch_cg_apply(fem_ctx* h, const Level& L, const double* x, double* y);
+void launch_cg_diagonal(fem_ctx* h, Level& L);
+void launch_dg_apply(fem_ctx* h, const Level& L, const double* x, double* y);
+void launch_dg_diagonal(fem_ctx* h, Level& L);
+void launch_dg_face_geometry(fem_ctx* h, Level& L);
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int n) { g_launches += n; }
+void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error{FEM_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+namespace {
+
+double* dalloc(int64_t n) {
+  void* p = nullptr;
+  FEM_CUDA_TRY(cudaMalloc(&p, sizeof(double) * std::max<int64_t>(n, 1)));
+  return (double*)p;
+}
+
+void dfree(double*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// ---------------------------------------------------------------- profiling
+void prof_begin(fem_ctx* h, bool finest) {
+  if (!h->prof.on || !finest) return;
+  if (h->prof.used + 2 > h->prof.ev.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      FEM_CUDA_TRY(cudaEventCreate(&e));
+      h->prof.ev.push_back(e);
+    }
+  }
+  FEM_CUDA_TRY(cudaEventRecord(h->prof.ev[h->prof.used], h->stream));
+}
+
+void prof_end(fem_ctx* h, bool finest) {
+  if (!h->prof.on || !finest) return;
+  FEM_CUDA_TRY(cudaEventRecord(h->prof.ev[h->prof.used + 1], h->stream));
+  h->prof.used += 2;
+  h->prof.launches += 1;
+}
+
+void prof_collect(fem_ctx* h) {
+  if (!h->prof.on || h->prof.used == 0) return;
+  FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  for (size_t i = 0; i < h->prof.used; i += 2) {
+    float ms = 0;
+    FEM_CUDA_TRY(cudaEventElapsedTime(&ms, h->prof.ev[i], h->prof.ev[i + 1]));
+    h->prof.ms += ms;
+  }
+  h->prof.used = 0;
+}
+
+// ---------------------------------------------------------------- operator
+// y = A x on level L.  y is overwritten.  CG: constrained rows y_c = x_c.
+void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool set_constrained = true) {
+  const bool finest = (&L == &h->levels.back());
+  if (h->prof.on && finest && h->prof.used + 2 > 4096) prof_collect(h);
+  if (is_cg(h)) {
+    launch_zero(h, y, L.n_dofs);
+    prof_begin(h, finest);
+    launch_cg_apply(h, L, x, y);
+    prof_end(h, finest);
+    if (set_constrained) launch_set_constrained(h, L, x, y);
+  } else {
+    prof_begin(h, finest);
+    launch_dg_apply(h, L, x, y);
+    prof_end(h, finest);
+  }
+}
+
+// ---------------------------------------------------------------- Chebyshev
+// x_out = S(x_in, b) on level l (x_in == nullptr: zero start), reading R9/O5:
+// x_1 = x_0 + D^-1 (b - A x_0) / theta;  x_{i+1} = x_i + rho_i rho_{i-1} (x_i - x_{i-1})
+//        + (2 rho_i / delta) D^-1 (b - A x_i),  rho_i = 1/(2 sigma - rho_{i-1}), rho_0 = 1/sigma.
+// Work buffers w[0..2] must differ from x_in/x_out/b.
+void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double* x_out,
+               double* w0, double* w1, double* w2) {
+  const int p = h->opt.cheb_degree;
+  const double a = h->opt.cheb_hi * L.lam, c = h->opt.cheb_lo * L.lam;
+  const double theta = 0.5 * (a + c), delta = 0.5 * (a - c);
+  const double sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  double* bufs[3] = {w0, w1, w2};
+  int nb = 0;
+  auto next = [&](const double* avoid1, const double* avoid2) {
+    for (int i = 0; i < 3; ++i) {
+      double* cand = bufs[(nb + i) % 3];
+      if (cand != avoid1 && cand != avoid2) {
+        nb = (nb + i + 1) % 3;
+        return cand;
+      }
+    }
+    return (double*)nullptr;
+  };
+  const double* xo = nullptr;
+  const double* x = nullptr;
+  // step 1
+  double* xn = (p == 1) ? x_out : next(x_in, nullptr);
+  if (x_in == nullptr) {
+    launch_cheb_step(h, L, xn, nullptr, nullptr, b, nullptr, 0.0, 1.0 / theta, false);
+  } else {
+    apply_level(h, L, x_in, L.t, false);
+    launch_cheb_step(h, L, xn, x_in, nullptr, b, L.t, 0.0, 1.0 / theta, false);
+  }
+  xo = x_in;
+  x = xn;
+  for (int i = 2; i <= p; ++i) {
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    const double c1 = rho_new * rho, c2 = 2.0 * rho_new / delta;
+    rho = rho_new;
+    apply_level(h, L, x, L.t, false);
+    xn = (i == p) ? x_out : next(x, xo);
+    launch_cheb_step(h, L, xn, x, xo, b, L.t, c1, c2, xo != nullptr);
+    xo = x;
+    x = xn;
+  }
+}
+
+void setup_coarse(fem_ctx* h);
+
+// ---------------------------------------------------------------- V-cycle
+// x_out = V(l, b).
+void vcycle(fem_ctx* h, int l, const double* b, double* x_out) {
+  if (l == 0) {
+    setup_coarse(h);
+    launch_coarse_solve(h, b, x_out);
+    return;
+  }
+  Level& L = h->levels[l];
+  Level& C = h->levels[l - 1];
+  // pre-smoothing from zero into L.x (x_out may be L.x for coarse levels)
+  double* xs = (x_out == L.x) ? L.x2 : L.x;
+  double* wa = (x_out == L.x) ? L.x : L.x2;
+  // buffers for the smoother: three distinct from b, xs
+  // work buffers: x3, b2 and wa (wa may be x_out on coarse levels, which is not live
+  // yet; the elementwise Chebyshev update is safe in place)
+  chebyshev(h, L, b, nullptr, xs, L.x3, L.b2, wa);
+  // residual, restriction: C.b = P^T (b - A xs)
+  apply_level(h, L, xs, L.t, false);
+  launch_restrict(h, C, L, b, L.t, C.b);
+  vcycle(h, l - 1, C.b, C.x);
+  launch_prolongate_add(h, C, L, C.x, xs);
+  chebyshev(h, L, b, xs, x_out, L.x3, L.b2, wa);
+}
+
+// ---------------------------------------------------------------- lambda_max
+// Largest eigenvalue of a symmetric tridiagonal matrix (bisection, Sturm counts).
+double tridiag_max_eig(const std::vector<double>& d, const std::vector<double>& e) {
+  const int m = (int)d.size();
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < m; ++i) {
+    double r = (i > 0 ? std::fabs(e[i - 1]) : 0.0) + (i + 1 < m ? std::fabs(e[i]) : 0.0);
+    lo = std::min(lo, d[i] - r);
+    hi = std::max(hi, d[i] + r);
+  }
+  auto count_below = [&](double x) {  // number of eigenvalues < x
+    int cnt = 0;
+    double q = 1.0;
+    for (int i = 0; i < m; ++i) {
+      q = d[i] - x - (i > 0 ? e[i - 1] * e[i - 1] / q : 0.0);
+      if (q == 0.0) q = -1e-300;
+      if (q < 0) ++cnt;
+    }
+    return cnt;
+  };
+  for (int it = 0; it < 200; ++it) {
+    double mid = 0.5 * (lo + hi);
+    if (count_below(mid) < m) lo = mid; else hi = mid;
+    if (hi - lo <= 1e-15 * std::max(1.0, std::fabs(hi))) break;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// 15 Jacobi-PCG iterations on A s-problem (reading O6).
+double estimate_lambda(fem_ctx* h, Level& L) {
+  double *s = L.b, *r = L.x, *z = L.x2, *p = L.x3, *q = L.t;
+  launch_splitmix(h, L, h->opt.eig_seed, s);
+  if (is_cg(h)) launch_set_constrained_value(h, L, 0.0, s);   // Dirichlet entries of s are 0
+  launch_copy(h, r, s, L.n_dofs);
+  launch_cheb_step(h, L, z, nullptr, nullptr, r, nullptr, 0.0, 1.0, false);  // z = D^-1 r
+  launch_copy(h, p, z, L.n_dofs);
+  launch_dot(h, r, z, L.n_dofs, 4);
+  FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal + 4, h->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  double rz = h->hscal[4];
+  std::vector<double> alpha, beta;
+  for (int it = 0; it < h->opt.eig_iters; ++it) {
+    apply_level(h, L, p, q, false);
+    launch_dot(h, p, q, L.n_dofs, 5);
+    FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal + 5, h->scal + 5, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    const double pq = h->hscal[5];
+    if (!(pq > 0) || !(rz > 0)) break;
+    const double a = rz / pq;
+    launch_axpby(h, r, q, -a, 1.0, L.n_dofs);                                   // r -= a q
+    launch_cheb_step(h, L, z, nullptr, nullptr, r, nullptr, 0.0, 1.0, false);  // z = D^-1 r
+    launch_dot(h, r, z, L.n_dofs, 4);
+    FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal + 4, h->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    const double rz_new = h->hscal[4];
+    alpha.push_back(a);
+    beta.push_back(rz_new / rz);
+    rz = rz_new;
+    if (rz_new == 0.0) break;
+    launch_axpby(h, p, z, 1.0, beta.back(), L.n_dofs);                          // p = z + b p
+  }
+  const int m = (int)alpha.size();
+  if (m == 0) throw Error{FEM_E_BREAKDOWN, "Lanczos breakdown on level " + std::to_string(L.idx)};
+  std::vector<double> d(m), e(std::max(m - 1, 0));
+  for (int j = 0; j < m; ++j) {
+    d[j] = 1.0 / alpha[j] + (j > 0 ? beta[j - 1] / alpha[j - 1] : 0.0);
+    if (j + 1 < m) e[j] = std::sqrt(beta[j]) / alpha[j];
+  }
+  return tridiag_max_eig(d, e);
+}
+
+// ---------------------------------------------------------------- coarse solve
+constexpr int kMaxCoarseFree = 4096;
+
+void setup_coarse(fem_ctx* h) {
+  if (h->coarse_inv) return;
+  Level& L0 = h->levels[0];
+  const int64_t n = L0.n_dofs;
+  std::vector<double> diag(n);
+  FEM_CUDA_TRY(cudaMemcpyAsync(diag.data(), L0.diag, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+  // free DoFs: CG rows whose dinv is nonzero; all DG DoFs
+  std::vector<double> dinv(n);
+  FEM_CUDA_TRY(cudaMemcpyAsync(dinv.data(), L0.dinv, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+  FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  std::vector<int> fr;
+  for (int64_t i = 0; i < n; ++i)
+    if (dinv[i] != 0.0) fr.push_back((int)i);
+  const int nf = (int)fr.size();
+  if (nf > kMaxCoarseFree)
+    throw Error{FEM_E_ARG, "coarsest level has " + std::to_string(nf) +
+                               " free DoFs (limit " + std::to_string(kMaxCoarseFree) +
+                               "); use cell counts divisible by a power of two"};
+  std::vector<double> A((size_t)nf * nf), col(n), e(n, 0.0);
+  double *de = L0.x, *dy = L0.t;
+  for (int j = 0; j < nf; ++j) {
+    launch_zero(h, de, n);
+    const double one = 1.0;
+    FEM_CUDA_TRY(cudaMemcpyAsync(de + fr[j], &one, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    apply_level(h, L0, de, dy, false);
+    FEM_CUDA_TRY(cudaMemcpyAsync(col.data(), dy, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (int i = 0; i < nf; ++i) A[(size_t)i * nf + j] = col[fr[i]];
+  }
+  // symmetrise (rounding) and Cholesky A = L L^T
+  for (int i = 0; i < nf; ++i)
+    for (int j = 0; j < i; ++j) A[(size_t)i * nf + j] = A[(size_t)j * nf + i] =
+        0.5 * (A[(size_t)i * nf + j] + A[(size_t)j * nf + i]);
+  std::vector<double> Lc((size_t)nf * nf, 0.0);
+  for (int j = 0; j < nf; ++j) {
+    double s = A[(size_t)j * nf + j];
+    for (int k = 0; k < j; ++k) s -= Lc[(size_t)j * nf + k] * Lc[(size_t)j * nf + k];
+    if (!(s > 0)) throw Error{FEM_E_BREAKDOWN, "coarse matrix not positive definite"};
+    Lc[(size_t)j * nf + j] = std::sqrt(s);
+    for (int i = j + 1; i < nf; ++i) {
+      double t = A[(size_t)i * nf + j];
+      for (int k = 0; k < j; ++k) t -= Lc[(size_t)i * nf + k] * Lc[(size_t)j * nf + k];
+      Lc[(size_t)i * nf + j] = t / Lc[(size_t)j * nf + j];
+    }
+  }
+  // A^-1 columns by forward/backward substitution
+  std::vector<double> inv((size_t)nf * nf), y(nf);
+  for (int c = 0; c < nf; ++c) {
+    for (int i = 0; i < nf; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= Lc[(size_t)i * nf + k] * y[k];
+      y[i] = s / Lc[(size_t)i * nf + i];
+    }
+    for (int i = nf - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < nf; ++k) s -= Lc[(size_t)k * nf + i] * inv[(size_t)k * nf + c];
+      inv[(size_t)i * nf + c] = s / Lc[(size_t)i * nf + i];
+    }
+  }
+  h->n_coarse_free = nf;
+  FEM_CUDA_TRY(cudaMalloc(&h->coarse_free, sizeof(int) * std::max(nf, 1)));
+  h->coarse_inv = dalloc((int64_t)nf * nf);
+  FEM_CUDA_TRY(cudaMemcpy(h->coarse_free, fr.data(), sizeof(int) * nf, cudaMemcpyHostToDevice));
+  FEM_CUDA_TRY(cudaMemcpy(h->coarse_inv, inv.data(), sizeof(double) * nf * nf, cudaMemcpyHostToDevice));
+}
+
+// ---------------------------------------------------------------- setup
+void build_levels(fem_ctx* h) {
+  std::vector<std::array<int, 3>> ns;
+  std::array<int, 3> n = {h->mesh.n[0], h->mesh.n[1], h->mesh.n[2]};
+  ns.push_back(n);
+  while (n[0] % 2 == 0 && n[1] % 2 == 0 && n[2] % 2 == 0 &&
+         std::max(n[0], std::max(n[1], n[2])) > h->opt.coarse_cells) {
+    n = {n[0] / 2, n[1] / 2, n[2] / 2};
+    ns.push_back(n);
+  }
+  const int nl = (int)ns.size();
+  h->levels.resize(nl);
+  for (int l = 0; l < nl; ++l) {
+    Level& L = h->levels[l];
+    const auto& c = ns[nl - 1 - l];
+    L.idx = l;
+    double det = 1.0;
+    for (int d = 0; d < 3; ++d) {
+      L.n[d] = c[d];
+      L.nn[d] = h->k * c[d] + 1;
+      L.h[d] = (h->mesh.hi[d] - h->mesh.lo[d]) / c[d];
+      det *= 0.5 * L.h[d];
+    }
+    for (int d = 0; d < 3; ++d) L.cart[d] = det * (2.0 / L.h[d]) * (2.0 / L.h[d]);
+    L.n_cells = (int64_t)c[0] * c[1] * c[2];
+    L.n_dofs = is_cg(h) ? (int64_t)L.nn[0] * L.nn[1] * L.nn[2]
+                        : L.n_cells * (h->k + 1) * (h->k + 1) * (h->k + 1);
+    L.cartesian = (h->mesh.deform_eps == 0.0);
+    L.diag = dalloc(L.n_dofs);
+    L.dinv = dalloc(L.n_dofs);
+    L.b = dalloc(L.n_dofs);
+    L.x = dalloc(L.n_dofs);
+    L.t = dalloc(L.n_dofs);
+    L.x2 = dalloc(L.n_dofs);
+    L.x3 = dalloc(L.n_dofs);
+    L.b2 = dalloc(L.n_dofs);
+  }
+}
+
+void level_geometry_and_diagonal(fem_ctx* h, Level& L) {
+  const int N = h->k + 1;
+  if (!L.cartesian) {
+    L.G = dalloc(L.n_cells * 6 * N * N * N);
+    const unsigned long long init = std::numeric_limits<unsigned long long>::max();
+    FEM_CUDA_TRY(cudaMemcpyAsync(h->geom_err, &init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
+    launch_geometry(h, L);
+    unsigned long long bad = 0;
+    FEM_CUDA_TRY(cudaMemcpyAsync(&bad, h->geom_err, sizeof(bad), cudaMemcpyDeviceToHost, h->stream));
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (bad != init)
+      throw Error{FEM_E_GEOMETRY, "det J <= 0 on level " + std::to_string(L.idx) + " in cell " +
+                                      std::to_string(bad)};
+    if (!is_cg(h)) launch_dg_face_geometry(h, L);
+  }
+  if (is_cg(h)) {
+    launch_zero(h, L.diag, L.n_dofs);
+    launch_cg_diagonal(h, L);
+    launch_set_constrained(h, L, nullptr, L.diag);     // diag = 1 on constrained rows
+    launch_dinv(h, L);
+    launch_set_constrained_value(h, L, 0.0, L.dinv);   // D^-1 = 0 on constrained rows
+  } else {
+    launch_dg_diagonal(h, L);
+    launch_dinv(h, L);
+  }
+}
+
+struct Staged {
+  fem_ctx* h;
+  double* dev;
+  const double* host_in;
+  double* host_out;
+  int64_t n;
+};
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+void ensure_stage(fem_ctx* h, int64_t n) {
+  if (h->stage_len >= n) return;
+  for (auto& s : h->stage) dfree(s);
+  for (auto& s : h->stage) s = dalloc(n);
+  h->stage_len = n;
+}
+
+// Resolve a caller vector to a device pointer (copy-in for host inputs).
+const double* in_vec(fem_ctx* h, const double* p, int64_t n, int slot) {
+  if (is_device_ptr(p)) return p;
+  ensure_stage(h, n);
+  FEM_CUDA_TRY(cudaMemcpyAsync(h->stage[slot], p, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+  return h->stage[slot];
+}
+
+double* out_vec(fem_ctx* h, double* p, int64_t n, int slot, bool copy_in, bool* staged) {
+  if (is_device_ptr(p)) {
+    *staged = false;
+    return p;
+  }
+  ensure_stage(h, n);
+  *staged = true;
+  if (copy_in)
+    FEM_CUDA_TRY(cudaMemcpyAsync(h->stage[slot], p, sizeof(double) * n, cudaMemcpyHostToDevice, h->stream));
+  return h->stage[slot];
+}
+
+void finish_out(fem_ctx* h, double* host, const double* dev, int64_t n, bool staged) {
+  if (!staged) return;
+  FEM_CUDA_TRY(cudaMemcpyAsync(host, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+  FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+}
+
+void check_handle(fem_handle h) {
+  if (!h) throw Error{FEM_E_ARG, "null handle"};
+  FEM_CUDA_TRY(cudaSetDevice(h->device));
+}
+
+void check_size(int64_t got, int64_t want, const char* what) {
+  if (got != want)
+    throw Error{FEM_E_SIZE, std::string(what) + ": length " + std::to_string(got) + ", expected " +
+                                std::to_string(want)};
+}
+
+Level& level_at(fem_handle h, int32_t level) {
+  if (level < 0 || level >= (int)h->levels.size())
+    throw Error{FEM_E_ARG, "level " + std::to_string(level) + " out of range"};
+  return h->levels[level];
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FEM_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return FEM_E_OOM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return FEM_E_ARG;
+  }
+}
+
+void destroy(fem_ctx* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (auto& L : h->levels) {
+    for (double** p : {&L.G, &L.face, &L.diag, &L.dinv, &L.b, &L.x, &L.x2, &L.x3, &L.t, &L.b2,
+                       &L.pcg_r, &L.pcg_p, &L.pcg_q, &L.pcg_z})
+      dfree(*p);
+  }
+  if (h->coarse_free) cudaFree(h->coarse_free);
+  dfree(h->coarse_inv);
+  dfree(h->red);
+  dfree(h->scal);
+  if (h->hscal) cudaFreeHost(h->hscal);
+  for (auto& s : h->stage) dfree(s);
+  if (h->geom_err) cudaFree(h->geom_err);
+  for (auto e : h->prof.ev) cudaEventDestroy(e);
+  delete h;
+}
+
+}  // namespace
+}  // namespace fem
+
+using namespace fem;
+
+extern "C" {
+
+const char* fem_last_error(void) { return g_last_error.c_str(); }
+
+int64_t fem_kernel_launches(void) { return g_launches.load(); }
+
+int fem_default_options(fem_options* o) {
+  if (!o) {
+    set_error("null options");
+    return FEM_E_ARG;
+  }
+  std::memset(o, 0, sizeof(*o));
+  o->penalty_factor = 2.0;
+  o->cheb_degree = 5;
+  o->cheb_lo = 0.06;
+  o->cheb_hi = 1.2;
+  o->eig_iters = 15;
+  o->coarse_cells = 1;
+  o->eig_seed = 0x5eed;
+  o->lambda_override = nullptr;
+  o->stream = nullptr;
+  o->device = -1;
+  o->profile = 0;
+  return FEM_OK;
+}
+
+int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_options* opt,
+              fem_handle* out) {
+  fem_ctx* h = nullptr;
+  int rc = guarded([&] {
+    if (!mesh || !out) throw Error{FEM_E_ARG, "null mesh or output handle"};
+    if (degree < 1 || degree > kMaxDeg) throw Error{FEM_E_ARG, "degree must be in [1, 8]"};
+    if (method != FEM_CG && method != FEM_SIPG) throw Error{FEM_E_ARG, "method must be FEM_CG or FEM_SIPG"};
+    for (int d = 0; d < 3; ++d) {
+      if (mesh->n[d] < 1) throw Error{FEM_E_ARG, "cells per direction must be >= 1"};
+      if (!(mesh->hi[d] > mesh->lo[d])) throw Error{FEM_E_ARG, "box must have hi > lo"};
+    }
+    for (int s = 0; s < 6; ++s)
+      if (mesh->bc[s] != FEM_BC_DIRICHLET && mesh->bc[s] != FEM_BC_NEUMANN)
+        throw Error{FEM_E_ARG, "bc must be FEM_BC_DIRICHLET or FEM_BC_NEUMANN"};
+    if (mesh->nranks != 1 || mesh->rank != 0)
+      throw Error{FEM_E_ARG, "multi-rank slabs are not available in this build (nranks must be 1)"};
+    h = new fem_ctx();
+    h->k = degree;
+    h->method = method;
+    h->mesh = *mesh;
+    fem_default_options(&h->opt);
+    if (opt) h->opt = *opt;
+    if (h->opt.cheb_degree < 1 || h->opt.eig_iters < 1 || h->opt.coarse_cells < 1 ||
+        !(h->opt.cheb_hi > h->opt.cheb_lo) || !(h->opt.cheb_lo > 0) || !(h->opt.penalty_factor > 0))
+      throw Error{FEM_E_ARG, "invalid solver options"};
+    if (h->opt.device >= 0) FEM_CUDA_TRY(cudaSetDevice(h->opt.device));
+    FEM_CUDA_TRY(cudaGetDevice(&h->device));
+    h->stream = (cudaStream_t)h->opt.stream;
+    h->prof.on = h->opt.profile != 0;
+    build_tables(degree, h->tab);
+    h->red = dalloc(16 * kRedBlocks);
+    h->scal = dalloc(16);
+    FEM_CUDA_TRY(cudaMemset(h->scal, 0, sizeof(double) * 16));
+    FEM_CUDA_TRY(cudaMallocHost(&h->hscal, sizeof(double) * 16));
+    FEM_CUDA_TRY(cudaMalloc(&h->geom_err, sizeof(unsigned long long)));
+    build_levels(h);
+    for (auto& L : h->levels) level_geometry_and_diagonal(h, L);
+    for (size_t l = 1; l < h->levels.size(); ++l) {
+      Level& L = h->levels[l];
+      L.lam = h->opt.lambda_override ? h->opt.lambda_override[l] : estimate_lambda(h, L);
+    }
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    // (the coarse Cholesky factor is built on first use: setup_coarse)
+    // profiling counts only what happens after setup
+    h->prof.used = 0;
+    h->prof.ms = 0;
+    h->prof.launches = 0;
+    *out = h;
+  });
+  if (rc != FEM_OK) destroy(h);
+  return rc;
+}
+
+int fem_info(fem_handle h, int64_t* n_local, int64_t* n_global, int64_t* first_global,
+             int32_t* n_levels) {
+  return guarded([&] {
+    check_handle(h);
+    const Level& L = h->levels.back();
+    if (n_local) *n_local = L.n_dofs;
+    if (n_global) *n_global = L.n_dofs;
+    if (first_global) *first_global = 0;
+    if (n_levels) *n_levels = (int32_t)h->levels.size();
+  });
+}
+
+int fem_level_info(fem_handle h, int32_t level, int64_t* n_dofs, int32_t cells[3]) {
+  return guarded([&] {
+    check_handle(h);
+    const Level& L = level_at(h, level);
+    if (n_dofs) *n_dofs = L.n_dofs;
+    if (cells)
+      for (int d = 0; d < 3; ++d) cells[d] = L.n[d];
+  });
+}
+
+int fem_level_apply(fem_handle h, int32_t level, const double* x, int64_t nx, double* y, int64_t ny) {
+  return guarded([&] {
+    check_handle(h);
+    Level& L = level_at(h, level);
+    if (!x || !y) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nx, L.n_dofs, "x");
+    check_size(ny, L.n_dofs, "y");
+    const double* dx = in_vec(h, x, nx, 0);
+    bool st;
+    double* dy = out_vec(h, y, ny, 1, false, &st);
+    apply_level(h, L, dx, dy, true);
+    finish_out(h, y, dy, ny, st);
+  });
+}
+
+int fem_apply(fem_handle h, const double* x, int64_t nx, double* y, int64_t ny) {
+  if (!h) {
+    set_error("null handle");
+    return FEM_E_ARG;
+  }
+  return fem_level_apply(h, (int32_t)h->levels.size() - 1, x, nx, y, ny);
+}
+
+int fem_level_diagonal(fem_handle h, int32_t level, double* d, int64_t nd) {
+  return guarded([&] {
+    check_handle(h);
+    Level& L = level_at(h, level);
+    if (!d) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nd, L.n_dofs, "d");
+    bool st;
+    double* dd = out_vec(h, d, nd, 0, false, &st);
+    launch_copy(h, dd, L.diag, L.n_dofs);
+    finish_out(h, d, dd, nd, st);
+  });
+}
+
+int fem_diagonal(fem_handle h, double* d, int64_t nd) {
+  if (!h) {
+    set_error("null handle");
+    return FEM_E_ARG;
+  }
+  return fem_level_diagonal(h, (int32_t)h->levels.size() - 1, d, nd);
+}
+
+int fem_level_lambda(fem_handle h, int32_t level, double* lam) {
+  return guarded([&] {
+    check_handle(h);
+    Level& L = level_at(h, level);
+    if (level < 1) throw Error{FEM_E_ARG, "the coarsest level has no smoother"};
+    if (!lam) throw Error{FEM_E_ARG, "null output"};
+    *lam = L.lam;
+  });
+}
+
+int fem_level_geometry(fem_handle h, int32_t level, double* G, int64_t nG) {
+  return guarded([&] {
+    check_handle(h);
+    Level& L = level_at(h, level);
+    const int N = h->k + 1;
+    const int64_t nq = (int64_t)N * N * N;
+    check_size(nG, L.n_cells * 6 * nq, "G");
+    if (!G) throw Error{FEM_E_ARG, "null vector"};
+    if (!L.cartesian) {
+      bool st;
+      double* dG = out_vec(h, G, nG, 0, false, &st);
+      launch_copy(h, dG, L.G, nG);
+      finish_out(h, G, dG, nG, st);
+      return;
+    }
+    // Cartesian: expand the per-level constants on the host
+    std::vector<double> hostG(nG, 0.0);
+    for (int64_t c = 0; c < L.n_cells; ++c)
+      for (int64_t q = 0; q < nq; ++q) {
+        const int q0 = (int)(q % N), q1 = (int)((q / N) % N), q2 = (int)(q / (N * N));
+        const double w = h->tab.qw[q0] * h->tab.qw[q1] * h->tab.qw[q2];
+        hostG[c * 6 * nq + 0 * nq + q] = L.cart[0] * w;
+        hostG[c * 6 * nq + 3 * nq + q] = L.cart[1] * w;
+        hostG[c * 6 * nq + 5 * nq + q] = L.cart[2] * w;
+      }
+    if (is_device_ptr(G))
+      FEM_CUDA_TRY(cudaMemcpy(G, hostG.data(), sizeof(double) * nG, cudaMemcpyHostToDevice));
+    else
+      std::memcpy(G, hostG.data(), sizeof(double) * nG);
+  });
+}
+
+int mg_smooth(fem_handle h, int32_t level, const double* b, int64_t nb, double* x, int64_t nx,
+              int32_t x_is_zero) {
+  return guarded([&] {
+    check_handle(h);
+    Level& L = level_at(h, level);
+    if (level < 1) throw Error{FEM_E_ARG, "smoothing needs level >= 1"};
+    if (!b || !x) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nb, L.n_dofs, "b");
+    check_size(nx, L.n_dofs, "x");
+    const double* db = in_vec(h, b, nb, 0);
+    bool st;
+    double* dx = out_vec(h, x, nx, 1, !x_is_zero, &st);
+    // copy inputs into level buffers so the smoother's work buffers never alias them
+    launch_copy(h, L.b, db, L.n_dofs);
+    if (!x_is_zero) launch_copy(h, L.x, dx, L.n_dofs);
+    chebyshev(h, L, L.b, x_is_zero ? nullptr : L.x, dx, L.x2, L.x3, L.b2);
+    finish_out(h, x, dx, nx, st);
+  });
+}
+
+int mg_prolongate_add(fem_handle h, int32_t level, const double* xc, int64_t nc, double* xf,
+                      int64_t nf) {
+  return guarded([&] {
+    check_handle(h);
+    Level& F = level_at(h, level);
+    if (level < 1) throw Error{FEM_E_ARG, "prolongation needs level >= 1"};
+    Level& C = h->levels[level - 1];
+    if (!xc || !xf) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nc, C.n_dofs, "xc");
+    check_size(nf, F.n_dofs, "xf");
+    const double* dc = in_vec(h, xc, nc, 0);
+    bool st;
+    double* df = out_vec(h, xf, nf, 1, true, &st);
+    launch_prolongate_add(h, C, F, dc, df);
+    finish_out(h, xf, df, nf, st);
+  });
+}
+
+int mg_restrict(fem_handle h, int32_t level, const double* xf, int64_t nf, double* xc, int64_t nc) {
+  return guarded([&] {
+    check_handle(h);
+    Level& F = level_at(h, level);
+    if (level < 1) throw Error{FEM_E_ARG, "restriction needs level >= 1"};
+    Level& C = h->levels[level - 1];
+    if (!xc || !xf) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nc, C.n_dofs, "xc");
+    check_size(nf, F.n_dofs, "xf");
+    const double* df = in_vec(h, xf, nf, 0);
+    bool st;
+    double* dc = out_vec(h, xc, nc, 1, false, &st);
+    launch_restrict(h, C, F, df, nullptr, dc);
+    finish_out(h, xc, dc, nc, st);
+  });
+}
+
+int mg_coarse_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx) {
+  return guarded([&] {
+    check_handle(h);
+    Level& L0 = h->levels[0];
+    if (!b || !x) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nb, L0.n_dofs, "b");
+    check_size(nx, L0.n_dofs, "x");
+    setup_coarse(h);
+    const double* db = in_vec(h, b, nb, 0);
+    bool st;
+    double* dx = out_vec(h, x, nx, 1, false, &st);
+    launch_coarse_solve(h, db, dx);
+    finish_out(h, x, dx, nx, st);
+  });
+}
+
+int mg_vcycle(fem_handle h, const double* r, int64_t nr, double* z, int64_t nz) {
+  return guarded([&] {
+    check_handle(h);
+    Level& L = h->levels.back();
+    if (!r || !z) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nr, L.n_dofs, "r");
+    check_size(nz, L.n_dofs, "z");
+    const double* dr = in_vec(h, r, nr, 0);
+    bool st;
+    double* dz = out_vec(h, z, nz, 1, false, &st);
+    launch_copy(h, L.b, dr, L.n_dofs);
+    vcycle(h, (int)h->levels.size() - 1, L.b, dz);
+    finish_out(h, z, dz, nz, st);
+  });
+}
+
+int fem_rhs(fem_handle h, double* b, int64_t nb) {
+  return guarded([&] {
+    check_handle(h);
+    Level& L = h->levels.back();
+    if (!b) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nb, L.n_dofs, "b");
+    bool st;
+    double* db = out_vec(h, b, nb, 0, false, &st);
+    launch_zero(h, db, L.n_dofs);
+    launch_rhs(h, L, db);
+    finish_out(h, b, db, nb, st);
+  });
+}
+
+int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, double rtol,
+             int32_t maxit, int32_t* iters, double* relres) {
+  int result = FEM_OK;
+  int rc = guarded([&] {
+    check_handle(h);
+    Level& L = h->levels.back();
+    const int fine = (int)h->levels.size() - 1;
+    if (!b || !x) throw Error{FEM_E_ARG, "null vector"};
+    check_size(nb, L.n_dofs, "b");
+    check_size(nx, L.n_dofs, "x");
+    if (!(rtol > 0) || maxit < 0) throw Error{FEM_E_ARG, "rtol must be > 0 and maxit >= 0"};
+    const int64_t n = L.n_dofs;
+    const double* db = in_vec(h, b, nb, 0);
+    bool st;
+    double* dx = out_vec(h, x, nx, 1, true, &st);
+    if (!L.pcg_r) {
+      L.pcg_r = dalloc(n);
+      L.pcg_p = dalloc(n);
+      L.pcg_q = dalloc(n);
+      L.pcg_z = dalloc(n);
+    }
+    double *r = L.pcg_r, *p = L.pcg_p, *q = L.pcg_q, *z = L.pcg_z;
+    // CG Dirichlet rows: identity, so x_c = b_c and r_c = 0 (the system decouples)
+    if (is_cg(h)) launch_set_constrained(h, L, db, dx);
+    apply_level(h, L, dx, q, true);
+    launch_sub(h, r, db, q, n);
+    launch_dot(h, db, db, n, 6);
+    launch_dot(h, r, r, n, 2);
+    FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, h->stream));
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    const double bnorm = std::sqrt(h->hscal[6]);
+    double rnorm = std::sqrt(h->hscal[2]);
+    int it = 0;
+    if (!std::isfinite(rnorm)) throw Error{FEM_E_BREAKDOWN, "non-finite initial residual"};
+    if (rnorm > rtol * bnorm) {
+      vcycle(h, fine, r, z);
+      launch_copy(h, p, z, n);
+      launch_dot(h, r, z, n, 0);
+      while (it < maxit) {
+        apply_level(h, L, p, q, false);
+        launch_dot(h, p, q, n, 1);
+        launch_pcg_update_xr(h, dx, r, p, q, n);
+        FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, h->stream));
+        FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        ++it;
+        const double pq = h->hscal[1];
+        rnorm = std::sqrt(h->hscal[2]);
+        if (!(pq > 0) || !std::isfinite(rnorm))
+          throw Error{FEM_E_BREAKDOWN, "PCG breakdown at iteration " + std::to_string(it) +
+                                           " (p^T A p = " + std::to_string(pq) + ")"};
+        if (rnorm <= rtol * bnorm) break;
+        vcycle(h, fine, r, z);
+        launch_dot(h, r, z, n, 3);
+        launch_pcg_update_p(h, p, z, n);
+      }
+    }
+    if (iters) *iters = it;
+    if (relres) *relres = bnorm > 0 ? rnorm / bnorm : rnorm;
+    if (rnorm > rtol * bnorm) result = FEM_NOT_CONVERGED;
+    finish_out(h, x, dx, nx, st);
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  });
+  return rc != FEM_OK ? rc : result;
+}
+
+int fem_sync(fem_handle h) {
+  return guarded([&] {
+    check_handle(h);
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int fem_profile_read(fem_handle h, double* ms, int64_t* launches, int32_t reset) {
+  return guarded([&] {
+    check_handle(h);
+    prof_collect(h);
+    if (ms) *ms = h->prof.ms;
+    if (launches) *launches = h->prof.launches;
+    if (reset) {
+      h->prof.ms = 0;
+      h->prof.launches = 0;
+    }
+  });
+}
+
+void fem_destroy(fem_handle h) { destroy(h); }
+
+}  // extern "C"

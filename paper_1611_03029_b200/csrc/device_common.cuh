@@ -1,0 +1,129 @@
+// Device-side helpers shared by the libfem kernels (sm_100a, FP64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace fem {
+
+// Per-degree 1-D tables passed by value (they live in the kernel-parameter
+// constant bank, so the sweeps' DFMAs read them as broadcast constant operands).
+template <int N>
+struct Tab {
+  double val[N][N];     // [q][i] GLL basis at Gauss points
+  double der[N][N];     // [q][i] GLL basis derivative at Gauss points
+  double colloc[N][N];  // [q][p] derivative of the Gauss-point Lagrange basis
+  double w[N];          // Gauss weights
+  double qp[N];         // Gauss points
+  double gll[N];        // GLL nodes
+  double dface[2][N];   // phi_i'(-1), phi_i'(+1)
+};
+
+template <int N>
+inline Tab<N> make_tab(const Tables1D& t) {
+  Tab<N> r;
+  for (int q = 0; q < N; ++q) {
+    for (int i = 0; i < N; ++i) {
+      r.val[q][i] = t.val[q][i];
+      r.der[q][i] = t.der[q][i];
+      r.colloc[q][i] = t.colloc[q][i];
+    }
+    r.w[q] = t.qw[q];
+    r.qp[q] = t.qp[q];
+    r.gll[q] = t.gll[q];
+    r.dface[0][q] = t.dface[0][q];
+    r.dface[1][q] = t.dface[1][q];
+  }
+  return r;
+}
+
+// out = M in  (out_i = sum_j M[i][j] in_j)
+template <int N>
+__device__ __forceinline__ void mv(const double (&M)[N][N], const double (&in)[N], double (&out)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(M[i][j], in[j], s);
+    out[i] = s;
+  }
+}
+
+// out = M^T in  (out_j = sum_i M[i][j] in_i)
+template <int N>
+__device__ __forceinline__ void mvt(const double (&M)[N][N], const double (&in)[N], double (&out)[N]) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) s = fma(M[i][j], in[i], s);
+    out[j] = s;
+  }
+}
+
+// out += M^T in
+template <int N>
+__device__ __forceinline__ void mvt_add(const double (&M)[N][N], const double (&in)[N], double (&out)[N]) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double s = out[j];
+#pragma unroll
+    for (int i = 0; i < N; ++i) s = fma(M[i][j], in[i], s);
+    out[j] = s;
+  }
+}
+
+// Mesh map (reading R2): xhat = lo + h (c + (xi+1)/2), x = xhat + eps s(xhat) (1,1,1),
+// s = prod_e sin(pi t_e), t = (xhat - lo)/(hi - lo).
+struct MapArgs {
+  double lo[3], L[3], h[3];
+  double eps;
+  int cz0;  // global z offset of the rank's slab (cells)
+};
+
+struct PointGeo {
+  double xh[3];     // undeformed point
+  double g[3];      // grad s (w.r.t. xhat)
+  double s;         // s(xhat)
+  double det;       // det J
+  double beta;      // eps / (1 + eps sum g)
+  double fac;       // 1 + eps sum g  (det J / prod(h/2))
+};
+
+__device__ __forceinline__ PointGeo map_point(const MapArgs& m, int cx, int cy, int cz,
+                                              double xi0, double xi1, double xi2) {
+  PointGeo p;
+  const int c[3] = {cx, cy, cz + m.cz0};
+  const double xi[3] = {xi0, xi1, xi2};
+  double sn[3], cs[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    p.xh[d] = m.lo[d] + m.h[d] * (c[d] + 0.5 * (xi[d] + 1.0));
+    double t = (p.xh[d] - m.lo[d]) / m.L[d];
+    sincospi(t, &sn[d], &cs[d]);
+  }
+  p.s = sn[0] * sn[1] * sn[2];
+  p.g[0] = M_PI / m.L[0] * cs[0] * sn[1] * sn[2];
+  p.g[1] = M_PI / m.L[1] * sn[0] * cs[1] * sn[2];
+  p.g[2] = M_PI / m.L[2] * sn[0] * sn[1] * cs[2];
+  p.fac = 1.0 + m.eps * (p.g[0] + p.g[1] + p.g[2]);
+  p.det = p.fac * (0.5 * m.h[0]) * (0.5 * m.h[1]) * (0.5 * m.h[2]);
+  p.beta = m.eps / p.fac;
+  return p;
+}
+
+// J^-1 = H^-1 (I - beta 1 g^T)  (Sherman-Morrison):  Jinv[d][e] = (2/h_d)(delta_de - beta g_e)
+__device__ __forceinline__ double jinv(const MapArgs& m, const PointGeo& p, int d, int e) {
+  return (2.0 / m.h[d]) * ((d == e ? 1.0 : 0.0) - p.beta * p.g[e]);
+}
+
+__device__ __forceinline__ bool cg_constrained(int bcmask, int gx, int gy, int gz, int nn0, int nn1,
+                                               int nn2) {
+  return ((bcmask & 1) && gx == 0) || ((bcmask & 2) && gx == nn0 - 1) ||
+         ((bcmask & 4) && gy == 0) || ((bcmask & 8) && gy == nn1 - 1) ||
+         ((bcmask & 16) && gz == 0) || ((bcmask & 32) && gz == nn2 - 1);
+}
+
+}  // namespace fem

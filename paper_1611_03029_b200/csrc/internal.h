@@ -1,0 +1,137 @@
+// libfem internals: 1-D tables, level hierarchy, handle.  B200 / sm_100a, FP64.
+// Nothing here is shared with oracle/ (the CPU reference re-derives everything).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/fem.h"
+
+namespace fem {
+
+constexpr int kMaxDeg = 8;
+constexpr int kMaxN = kMaxDeg + 1;
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+#define FEM_CUDA_TRY(expr)                                                              \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw ::fem::Error{e_ == cudaErrorMemoryAllocation ? FEM_E_OOM : FEM_E_CUDA,       \
+                         std::string(#expr) + ": " + cudaGetErrorString(e_)};           \
+  } while (0)
+
+void count_launch(int n = 1);
+void check_launch(const char* what);
+
+// ---------------------------------------------------------------- 1-D tables
+// GLL Lagrange basis at the (k+1)-point Gauss rule.
+struct Tables1D {
+  int k = 0, n = 0;
+  double gll[kMaxN];              // GLL nodes on [-1,1]
+  double qp[kMaxN], qw[kMaxN];    // Gauss points / weights
+  double val[kMaxN][kMaxN];       // [q][i] phi_i(qp_q)
+  double der[kMaxN][kMaxN];       // [q][i] phi_i'(qp_q)
+  double colloc[kMaxN][kMaxN];    // [q][p] l_p'(qp_q), l = Lagrange basis on Gauss points
+  double dface[2][kMaxN];         // [side][i] phi_i'(-1), phi_i'(+1)
+  double cg_embed[2 * kMaxDeg + 1][kMaxN];  // [fine node r of the 2 children][coarse j]
+  double dg_embed[2][kMaxN][kMaxN];         // [child][fine i][coarse j]
+};
+void build_tables(int k, Tables1D& t);
+
+// ---------------------------------------------------------------- level data
+struct Level {
+  int idx = 0;
+  int n[3] = {0, 0, 0};          // cells per direction (rank-local in z)
+  int nn[3] = {0, 0, 0};         // CG nodes per direction
+  double h[3] = {0, 0, 0};
+  int64_t n_cells = 0, n_dofs = 0;
+  bool cartesian = true;
+  double cart[3] = {0, 0, 0};    // Cartesian metric: det(J) (2/h_d)^2
+  double* G = nullptr;           // deformed: [cell][6][q]
+  double* face = nullptr;        // SIPG deformed: face data, see kernels_dg.cu
+  double* diag = nullptr;        // diag(A)
+  double* dinv = nullptr;        // 1/diag on free DoFs, 0 on constrained
+  double lam = 0.0;
+  // work vectors for the V-cycle (level >= 1 need all, level 0 needs b, x)
+  double *b = nullptr, *x = nullptr, *x2 = nullptr, *x3 = nullptr, *t = nullptr, *b2 = nullptr;
+  // PCG vectors (finest level, allocated on first cg_solve)
+  double *pcg_r = nullptr, *pcg_p = nullptr, *pcg_q = nullptr, *pcg_z = nullptr;
+};
+
+struct Profile {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // pairs (start, stop)
+  size_t used = 0;
+  double ms = 0.0;
+  int64_t launches = 0;
+};
+
+}  // namespace fem
+
+struct fem_ctx {
+  int k = 0, method = 0;
+  fem_mesh mesh{};
+  fem_options opt{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  fem::Tables1D tab;
+  std::vector<fem::Level> levels;
+  // coarse solve: free DoFs of level 0 and the dense inverse (via Cholesky)
+  int n_coarse_free = 0;
+  int* coarse_free = nullptr;
+  double* coarse_inv = nullptr;
+  // reductions
+  double* red = nullptr;          // partial sums [kRedBlocks * 4]
+  double* scal = nullptr;         // device scalars [16]
+  double* hscal = nullptr;        // pinned host mirror [16]
+  // host staging
+  double* stage[3] = {nullptr, nullptr, nullptr};
+  int64_t stage_len = 0;
+  unsigned long long* geom_err = nullptr;  // device: first cell with det J <= 0
+  fem::Profile prof;
+};
+
+namespace fem {
+
+constexpr int kRedBlocks = 296;   // 2 x 148 SMs
+
+// kernels (kernels_*.cu)
+void launch_geometry(fem_ctx* h, Level& L);
+void launch_apply(fem_ctx* h, const Level& L, const double* x, double* y, bool accumulate_into_zeroed);
+void launch_diagonal(fem_ctx* h, Level& L);
+void launch_rhs(fem_ctx* h, const Level& L, double* b);
+void launch_prolongate_add(fem_ctx* h, const Level& coarse, const Level& fine, const double* xc,
+                           double* xf);
+void launch_restrict(fem_ctx* h, const Level& coarse, const Level& fine, const double* bf,
+                     const double* axf, double* xc);
+void launch_set_constrained(fem_ctx* h, const Level& L, const double* x, double* y);  // y_c = x_c (x null: 1)
+void launch_set_constrained_value(fem_ctx* h, const Level& L, double v, double* y);    // y_c = v
+void launch_zero(fem_ctx* h, double* p, int64_t n);
+void launch_copy(fem_ctx* h, double* dst, const double* src, int64_t n);
+void launch_dinv(fem_ctx* h, Level& L);
+void launch_splitmix(fem_ctx* h, const Level& L, uint64_t seed, double* s);
+// Chebyshev three-term step:  xn = x + c1 (x - xo) + c2 Dinv (b - Ax); Ax <- 0.
+void launch_cheb_step(fem_ctx* h, const Level& L, double* xn, const double* x, const double* xo,
+                      const double* b, double* ax, double c1, double c2, bool has_xo);
+// reductions into h->scal[slot] (device)
+void launch_dot(fem_ctx* h, const double* a, const double* b, int64_t n, int slot);
+// PCG pieces
+void launch_pcg_update_xr(fem_ctx* h, double* x, double* r, const double* p, double* q, int64_t n);
+void launch_pcg_update_p(fem_ctx* h, double* p, const double* z, int64_t n);
+void launch_coarse_solve(fem_ctx* h, const double* b, double* x);
+void launch_axpby(fem_ctx* h, double* y, const double* x, double a, double b, int64_t n);
+void launch_sub(fem_ctx* h, double* r, const double* b, const double* ax, int64_t n);
+
+// level helpers
+inline bool is_cg(const fem_ctx* h) { return h->method == FEM_CG; }
+
+}  // namespace fem

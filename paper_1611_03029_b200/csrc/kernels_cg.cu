@@ -1,0 +1,447 @@
+// CG Q_k cell kernels: operator apply (K1), diagonal (K4), geometry tables (R2),
+// manufactured load vector (O8), Dirichlet rows.
+//
+// Operator (eq:mf_eval): per cell, gather x_e (constrained entries
+// read as 0), interpolate to the (k+1)^3 Gauss points (3 sweeps with the 1-D
+// GLL->Gauss matrix), collocation derivatives (3 sweeps), q-point operation
+// f_q = G_q grad_xi u_q with G_q = w_q det J J^-1 J^-T, transposed sweeps, and
+// scatter-add (sum factorization).
+//
+// Thread layout (B200 design): one block handles CPB cells, a
+// cell is handled by (k+1)^2 threads; in each phase a thread owns one 1-D line
+// of the cell in the sweep direction, keeping the line in registers (the
+// sweep is a register-only (k+1)x(k+1) mat-vec with the table in the constant
+// bank); switching direction is a transpose through shared memory.
+#include <algorithm>
+
+#include "device_common.cuh"
+
+namespace fem {
+
+template <int K>
+struct CPB {  // cells per block: about 128-200 threads per block
+  static constexpr int N = K + 1;
+  static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? 8 : (N * N <= 49) ? 4 : 2;
+};
+
+struct OpArgs {
+  const double* __restrict__ x;
+  double* __restrict__ y;
+  const double* __restrict__ G;  // deformed: [cell][6][q]
+  int n0, n1, n2;                // cells per direction
+  int nn0, nn1, nn2;             // nodes per direction
+  int bcmask;
+  int64_t n_cells;
+  double c0, c1, c2;             // Cartesian metric det(J) (2/h_d)^2
+};
+
+template <int K, bool DEFORMED>
+__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
+    cg_apply_kernel(OpArgs a, Tab<K + 1> T) {
+  constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
+  constexpr int C = CPB<K>::value;
+  extern __shared__ double smem[];
+  const int t = threadIdx.x;
+  const int ci = threadIdx.y;
+  const int64_t cell = (int64_t)blockIdx.x * C + ci;
+  const bool active = cell < a.n_cells;
+  double* s0 = smem + ci * 3 * N3;
+  double* s1 = s0 + N3;
+  double* s2 = s1 + N3;
+  const int ta = t % N, tb = t / N;
+  int cx = 0, cy = 0, cz = 0;
+  if (active) {
+    cx = (int)(cell % a.n0);
+    int64_t r = cell / a.n0;
+    cy = (int)(r % a.n1);
+    cz = (int)(r / a.n1);
+  }
+  double u[N], v[N], g[N];
+
+  // ---- Z: gather the z-line (x=ta, y=tb) and interpolate in z
+  const int gx = K * cx + ta, gy = K * cy + tb;
+  const int64_t zs = (int64_t)a.nn0 * a.nn1;
+  const int64_t base = gx + (int64_t)a.nn0 * gy + zs * (int64_t)(K * cz);
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    const bool m = cg_constrained(a.bcmask, gx, gy, K * cz + l, a.nn0, a.nn1, a.nn2);
+    u[l] = (active && !m) ? __ldg(a.x + base + l * zs) : 0.0;
+  }
+  mv<N>(T.val, u, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[t + N2 * l] = v[l];
+  __syncthreads();
+  // ---- Y: y-line (x=ta, z=tb)
+#pragma unroll
+  for (int l = 0; l < N; ++l) u[l] = s0[ta + N * l + N2 * tb];
+  mv<N>(T.val, u, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = v[l];
+  __syncthreads();
+  // ---- X: x-line (y=ta, z=tb): interpolate, then d/dxi_x by collocation
+#pragma unroll
+  for (int l = 0; l < N; ++l) u[l] = s0[l + N * ta + N2 * tb];
+  mv<N>(T.val, u, v);
+  mv<N>(T.colloc, v, g);
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    s0[l + N * ta + N2 * tb] = v[l];
+    s2[l + N * ta + N2 * tb] = g[l];
+  }
+  __syncthreads();
+  // ---- Y: d/dxi_y
+#pragma unroll
+  for (int l = 0; l < N; ++l) u[l] = s0[ta + N * l + N2 * tb];
+  mv<N>(T.colloc, u, g);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s1[ta + N * l + N2 * tb] = g[l];
+  __syncthreads();
+  // ---- Z: d/dxi_z, quadrature-point operation, transposed d/dxi_z
+#pragma unroll
+  for (int l = 0; l < N; ++l) u[l] = s0[t + N2 * l];
+  mv<N>(T.colloc, u, g);  // g = d/dxi_z
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    const int q = t + N2 * l;
+    const double gxq = s2[q], gyq = s1[q], gzq = g[l];
+    double fx, fy, fz;
+    if (DEFORMED) {
+      const double* Gc = a.G + (size_t)cell * 6 * N3 + q;
+      double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
+      if (active) {
+        G00 = __ldg(Gc);
+        G01 = __ldg(Gc + N3);
+        G02 = __ldg(Gc + 2 * N3);
+        G11 = __ldg(Gc + 3 * N3);
+        G12 = __ldg(Gc + 4 * N3);
+        G22 = __ldg(Gc + 5 * N3);
+      }
+      fx = G00 * gxq + G01 * gyq + G02 * gzq;
+      fy = G01 * gxq + G11 * gyq + G12 * gzq;
+      fz = G02 * gxq + G12 * gyq + G22 * gzq;
+    } else {
+      const double w3 = T.w[ta] * T.w[tb] * T.w[l];
+      fx = a.c0 * w3 * gxq;
+      fy = a.c1 * w3 * gyq;
+      fz = a.c2 * w3 * gzq;
+    }
+    s2[q] = fx;
+    s1[q] = fy;
+    v[l] = fz;
+  }
+  mvt<N>(T.colloc, v, u);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[t + N2 * l] = u[l];
+  __syncthreads();
+  // ---- Y: += colloc^T f_y
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    v[l] = s1[ta + N * l + N2 * tb];
+    u[l] = s0[ta + N * l + N2 * tb];
+  }
+  mvt_add<N>(T.colloc, v, u);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = u[l];
+  __syncthreads();
+  // ---- X: += colloc^T f_x, then interpolate back in x (val^T)
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    v[l] = s2[l + N * ta + N2 * tb];
+    u[l] = s0[l + N * ta + N2 * tb];
+  }
+  mvt_add<N>(T.colloc, v, u);
+  mvt<N>(T.val, u, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[l + N * ta + N2 * tb] = v[l];
+  __syncthreads();
+  // ---- Y: val^T
+#pragma unroll
+  for (int l = 0; l < N; ++l) u[l] = s0[ta + N * l + N2 * tb];
+  mvt<N>(T.val, u, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = v[l];
+  __syncthreads();
+  // ---- Z: val^T and scatter-add (constrained rows skipped; set afterwards)
+#pragma unroll
+  for (int l = 0; l < N; ++l) u[l] = s0[t + N2 * l];
+  mvt<N>(T.val, u, v);
+  if (active) {
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      const bool m = cg_constrained(a.bcmask, gx, gy, K * cz + l, a.nn0, a.nn1, a.nn2);
+      if (!m) atomicAdd(a.y + base + l * zs, v[l]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- diagonal
+// d_i = sum_cells sum_q sum_ab G_ab(q) B_a(q,i) B_b(q,i),  B_a = d phi_i/d xi_a at q.
+template <int K, bool DEFORMED>
+__global__ void cg_diag_kernel(OpArgs a, Tab<K + 1> T) {
+  constexpr int N = K + 1, N3 = N * N * N;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= a.n_cells * N3) return;
+  const int64_t cell = id / N3;
+  const int i = (int)(id % N3);
+  const int i0 = i % N, i1 = (i / N) % N, i2 = i / (N * N);
+  double d = 0.0;
+  for (int q2 = 0; q2 < N; ++q2)
+    for (int q1 = 0; q1 < N; ++q1)
+      for (int q0 = 0; q0 < N; ++q0) {
+        const double bx = T.der[q0][i0] * T.val[q1][i1] * T.val[q2][i2];
+        const double by = T.val[q0][i0] * T.der[q1][i1] * T.val[q2][i2];
+        const double bz = T.val[q0][i0] * T.val[q1][i1] * T.der[q2][i2];
+        if (DEFORMED) {
+          const int q = q0 + N * (q1 + N * q2);
+          const double* Gc = a.G + (size_t)cell * 6 * N3 + q;
+          d += Gc[0] * bx * bx + Gc[3 * N3] * by * by + Gc[5 * N3] * bz * bz +
+               2.0 * (Gc[N3] * bx * by + Gc[2 * N3] * bx * bz + Gc[4 * N3] * by * bz);
+        } else {
+          const double w3 = T.w[q0] * T.w[q1] * T.w[q2];
+          d += w3 * (a.c0 * bx * bx + a.c1 * by * by + a.c2 * bz * bz);
+        }
+      }
+  const int cx = (int)(cell % a.n0);
+  const int64_t r = cell / a.n0;
+  const int cy = (int)(r % a.n1), cz = (int)(r / a.n1);
+  const int gx = K * cx + i0, gy = K * cy + i1, gz = K * cz + i2;
+  if (cg_constrained(a.bcmask, gx, gy, gz, a.nn0, a.nn1, a.nn2)) return;
+  atomicAdd(a.y + gx + (int64_t)a.nn0 * (gy + (int64_t)a.nn1 * gz), d);
+}
+
+// ---------------------------------------------------------------- geometry (R2)
+// G_q = w_q det J J^-1 J^-T with J = (I + eps 1 grad s^T) diag(h/2):
+// G_df = w det J (4 / (h_d h_f)) (delta_df - beta (g_d + g_f) + beta^2 |g|^2).
+template <int K>
+__global__ void geometry_kernel(MapArgs m, int n0, int n1, int64_t n_cells, Tab<K + 1> T,
+                                double* __restrict__ G, unsigned long long* __restrict__ err) {
+  constexpr int N = K + 1, N3 = N * N * N;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= n_cells * N3) return;
+  const int64_t cell = id / N3;
+  const int q = (int)(id % N3);
+  const int q0 = q % N, q1 = (q / N) % N, q2 = q / (N * N);
+  const int cx = (int)(cell % n0);
+  const int64_t r = cell / n0;
+  const int cy = (int)(r % n1), cz = (int)(r / n1);
+  const PointGeo p = map_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]);
+  if (!(p.fac > 0.0)) {
+    // record the first bad cell (as a double, exact for < 2^53)
+    atomicMin((unsigned long long*)err, (unsigned long long)cell);
+  }
+  const double w = T.w[q0] * T.w[q1] * T.w[q2] * p.det;
+  const double g2 = p.g[0] * p.g[0] + p.g[1] * p.g[1] + p.g[2] * p.g[2];
+  const double b = p.beta;
+  const int comp[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    const int d = comp[c][0], f = comp[c][1];
+    const double v = (d == f ? 1.0 : 0.0) - b * (p.g[d] + p.g[f]) + b * b * g2;
+    G[(size_t)cell * 6 * N3 + c * N3 + q] = w * (4.0 / (m.h[d] * m.h[f])) * v;
+  }
+}
+
+// ---------------------------------------------------------------- load vector (O8)
+// b_i = sum_q f(x_q) phi_i(xi_q) w_q det J_q, f = pi^2 sum_d L_d^-2 prod_e sin(pi t_e(x)).
+// One block per cell, (k+1)^3 threads.
+template <int K, bool DG>
+__global__ void rhs_kernel(MapArgs m, OpArgs a, Tab<K + 1> T) {
+  constexpr int N = K + 1, N3 = N * N * N;
+  __shared__ double fq[N3];
+  const int64_t cell = blockIdx.x;
+  const int cx = (int)(cell % a.n0);
+  const int64_t r = cell / a.n0;
+  const int cy = (int)(r % a.n1), cz = (int)(r / a.n1);
+  for (int q = threadIdx.x; q < N3; q += blockDim.x) {
+    const int q0 = q % N, q1 = (q / N) % N, q2 = q / (N * N);
+    const PointGeo p = map_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]);
+    double u = 1.0, lap = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double xd = p.xh[d] + m.eps * p.s;  // physical coordinate
+      u *= sinpi((xd - m.lo[d]) / m.L[d]);
+      lap += 1.0 / (m.L[d] * m.L[d]);
+    }
+    fq[q] = M_PI * M_PI * lap * u * T.w[q0] * T.w[q1] * T.w[q2] * p.det;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < N3; i += blockDim.x) {
+    const int i0 = i % N, i1 = (i / N) % N, i2 = i / (N * N);
+    double s = 0.0;
+    for (int q2 = 0; q2 < N; ++q2)
+      for (int q1 = 0; q1 < N; ++q1) {
+        const double v12 = T.val[q1][i1] * T.val[q2][i2];
+        for (int q0 = 0; q0 < N; ++q0) s += fq[q0 + N * (q1 + N * q2)] * T.val[q0][i0] * v12;
+      }
+    if (DG) {
+      a.y[cell * N3 + i] = s;
+    } else {
+      const int gx = K * cx + i0, gy = K * cy + i1, gz = K * cz + i2;
+      if (!cg_constrained(a.bcmask, gx, gy, gz, a.nn0, a.nn1, a.nn2))
+        atomicAdd(a.y + gx + (int64_t)a.nn0 * (gy + (int64_t)a.nn1 * gz), s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Dirichlet rows
+// y_c = x_c (x == nullptr: y_c = 1) on the six boundary planes of Dirichlet sides.
+__global__ void set_constrained_kernel(const double* __restrict__ x, double val, double* __restrict__ y,
+                                       int nn0, int nn1, int nn2, int bcmask) {
+  const int side = blockIdx.y;
+  if (!(bcmask & (1 << side))) return;
+  const int d = side / 2;
+  const int fixed = (side % 2) ? ((d == 0 ? nn0 : d == 1 ? nn1 : nn2) - 1) : 0;
+  const int na = (d == 0) ? nn1 : nn0;
+  const int nb = (d == 2) ? nn1 : nn2;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)na * nb) return;
+  const int ia = (int)(id % na), ib = (int)(id / na);
+  int g[3];
+  g[d] = fixed;
+  if (d == 0) { g[1] = ia; g[2] = ib; }
+  if (d == 1) { g[0] = ia; g[2] = ib; }
+  if (d == 2) { g[0] = ia; g[1] = ib; }
+  const int64_t idx = g[0] + (int64_t)nn0 * (g[1] + (int64_t)nn1 * g[2]);
+  y[idx] = x ? x[idx] : val;
+}
+
+// ---------------------------------------------------------------- launchers
+namespace {
+
+OpArgs op_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
+  OpArgs a;
+  a.x = x;
+  a.y = y;
+  a.G = L.G;
+  a.n0 = L.n[0];
+  a.n1 = L.n[1];
+  a.n2 = L.n[2];
+  a.nn0 = L.nn[0];
+  a.nn1 = L.nn[1];
+  a.nn2 = L.nn[2];
+  int mask = 0;
+  for (int s = 0; s < 6; ++s)
+    if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
+  a.bcmask = mask;
+  a.n_cells = L.n_cells;
+  a.c0 = L.cart[0];
+  a.c1 = L.cart[1];
+  a.c2 = L.cart[2];
+  return a;
+}
+
+MapArgs map_args(const fem_ctx* h, const Level& L) {
+  MapArgs m;
+  for (int d = 0; d < 3; ++d) {
+    m.lo[d] = h->mesh.lo[d];
+    m.L[d] = h->mesh.hi[d] - h->mesh.lo[d];
+    m.h[d] = L.h[d];
+  }
+  m.eps = h->mesh.deform_eps;
+  m.cz0 = 0;
+  return m;
+}
+
+template <int K>
+void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
+  constexpr int N = K + 1, C = CPB<K>::value;
+  const OpArgs a = op_args(h, L, x, y);
+  const Tab<N> T = make_tab<N>(h->tab);
+  const dim3 block(N * N, C);
+  const int64_t grid = (L.n_cells + C - 1) / C;
+  const size_t sm = sizeof(double) * 3 * N * N * N * C;
+  if (L.cartesian)
+    cg_apply_kernel<K, false><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
+  else
+    cg_apply_kernel<K, true><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
+  count_launch();
+  check_launch("cg_apply_kernel");
+}
+
+template <int K>
+void diag_k(fem_ctx* h, Level& L) {
+  constexpr int N = K + 1;
+  const OpArgs a = op_args(h, L, nullptr, L.diag);
+  const Tab<N> T = make_tab<N>(h->tab);
+  const int64_t tot = L.n_cells * N * N * N;
+  const unsigned grid = (unsigned)((tot + 255) / 256);
+  if (L.cartesian)
+    cg_diag_kernel<K, false><<<grid, 256, 0, h->stream>>>(a, T);
+  else
+    cg_diag_kernel<K, true><<<grid, 256, 0, h->stream>>>(a, T);
+  count_launch();
+  check_launch("cg_diag_kernel");
+}
+
+template <int K>
+void geometry_k(fem_ctx* h, Level& L) {
+  constexpr int N = K + 1;
+  const Tab<N> T = make_tab<N>(h->tab);
+  const int64_t tot = L.n_cells * N * N * N;
+  geometry_kernel<K><<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(
+      map_args(h, L), L.n[0], L.n[1], L.n_cells, T, L.G, h->geom_err);
+  count_launch();
+  check_launch("geometry_kernel");
+}
+
+template <int K>
+void rhs_k(fem_ctx* h, const Level& L, double* b) {
+  constexpr int N = K + 1;
+  const Tab<N> T = make_tab<N>(h->tab);
+  const OpArgs a = op_args(h, L, nullptr, b);
+  const int threads = N * N * N < 128 ? 128 : (N * N * N > 512 ? 512 : N * N * N);
+  if (h->method == FEM_CG)
+    rhs_kernel<K, false><<<(unsigned)L.n_cells, threads, 0, h->stream>>>(map_args(h, L), a, T);
+  else
+    rhs_kernel<K, true><<<(unsigned)L.n_cells, threads, 0, h->stream>>>(map_args(h, L), a, T);
+  count_launch();
+  check_launch("rhs_kernel");
+}
+
+#define FEM_DISPATCH_K(k, fn, ...)              \
+  switch (k) {                                  \
+    case 1: fn<1>(__VA_ARGS__); break;          \
+    case 2: fn<2>(__VA_ARGS__); break;          \
+    case 3: fn<3>(__VA_ARGS__); break;          \
+    case 4: fn<4>(__VA_ARGS__); break;          \
+    case 5: fn<5>(__VA_ARGS__); break;          \
+    case 6: fn<6>(__VA_ARGS__); break;          \
+    case 7: fn<7>(__VA_ARGS__); break;          \
+    case 8: fn<8>(__VA_ARGS__); break;          \
+    default: throw Error{FEM_E_ARG, "degree out of range"}; \
+  }
+
+}  // namespace
+
+void launch_cg_apply(fem_ctx* h, const Level& L, const double* x, double* y) {
+  FEM_DISPATCH_K(h->k, apply_k, h, L, x, y);
+}
+
+void launch_cg_diagonal(fem_ctx* h, Level& L) { FEM_DISPATCH_K(h->k, diag_k, h, L); }
+
+void launch_geometry(fem_ctx* h, Level& L) { FEM_DISPATCH_K(h->k, geometry_k, h, L); }
+
+void launch_rhs(fem_ctx* h, const Level& L, double* b) { FEM_DISPATCH_K(h->k, rhs_k, h, L, b); }
+
+namespace {
+void set_constrained_impl(fem_ctx* h, const Level& L, const double* x, double v, double* y) {
+  const OpArgs a = op_args(h, L, x, y);
+  if (a.bcmask == 0) return;
+  int64_t mx = std::max<int64_t>((int64_t)L.nn[0] * L.nn[1],
+                                 std::max<int64_t>((int64_t)L.nn[0] * L.nn[2], (int64_t)L.nn[1] * L.nn[2]));
+  dim3 grid((unsigned)((mx + 255) / 256), 6);
+  set_constrained_kernel<<<grid, 256, 0, h->stream>>>(x, v, y, L.nn[0], L.nn[1], L.nn[2], a.bcmask);
+  count_launch();
+  check_launch("set_constrained_kernel");
+}
+}  // namespace
+
+void launch_set_constrained(fem_ctx* h, const Level& L, const double* x, double* y) {
+  set_constrained_impl(h, L, x, 1.0, y);
+}
+
+void launch_set_constrained_value(fem_ctx* h, const Level& L, double v, double* y) {
+  set_constrained_impl(h, L, nullptr, v, y);
+}
+
+}  // namespace fem

@@ -1,0 +1,486 @@
+// Multigrid and vector kernels: level transfer (K6), Chebyshev step (K5),
+// fused PCG vector updates and deterministic reductions (K7), coarse solve (K8),
+// splitmix64 start vector.
+//
+// Transfer ("geometric embedding operations ... implemented by
+// tensorial techniques"): one block per coarse cell applies the 1-D embedding
+// matrix E [M x (k+1)] in three sweeps (CG: M = 2k+1 fine nodes of the two
+// children; DG: M = 2(k+1), child matrices stacked).  CG prolongation writes each
+// fine node from exactly one coarse cell (half-open ownership), so x_f += P x_c
+// needs no atomics; CG restriction reads each fine node in its owning coarse cell
+// only, which reproduces P^T exactly (a coarse basis function of a neighbour
+// vanishes on the shared face unless its node lies on it), and adds into the
+// coarse vector with atomics.  DG transfers touch only the 8 children.
+#include <algorithm>
+
+#include "device_common.cuh"
+
+namespace fem {
+
+template <int K, bool DG>
+struct Embed {
+  static constexpr int N = K + 1;
+  static constexpr int M = DG ? 2 * N : 2 * K + 1;
+  double E[M][N];
+};
+
+struct TransferArgs {
+  int nc0, nc1, nc2;     // coarse cells
+  int nnc0, nnc1, nnc2;  // coarse CG nodes
+  int nnf0, nnf1, nnf2;  // fine CG nodes
+  int bcmask;
+};
+
+__device__ __forceinline__ int64_t cg_index(int gx, int gy, int gz, int nn0, int nn1) {
+  return gx + (int64_t)nn0 * (gy + (int64_t)nn1 * gz);
+}
+
+// xf += P xc
+template <int K, bool DG>
+__global__ void prolongate_kernel(TransferArgs a, Embed<K, DG> E, const double* __restrict__ xc,
+                                  double* __restrict__ xf) {
+  constexpr int N = K + 1, M = Embed<K, DG>::M;
+  extern __shared__ double smem[];
+  double* s_in = smem;               // N^3
+  double* s_1 = smem + N * N * N;    // M N^2
+  double* s_2 = s_1 + M * N * N;     // M^2 N
+  const int64_t cell = blockIdx.x;
+  const int cx = (int)(cell % a.nc0);
+  const int64_t rr = cell / a.nc0;
+  const int cy = (int)(rr % a.nc1), cz = (int)(rr / a.nc1);
+  for (int i = threadIdx.x; i < N * N * N; i += blockDim.x) {
+    const int i0 = i % N, i1 = (i / N) % N, i2 = i / (N * N);
+    double v;
+    if (DG) {
+      v = xc[cell * N * N * N + i];
+    } else {
+      const int gx = K * cx + i0, gy = K * cy + i1, gz = K * cz + i2;
+      v = cg_constrained(a.bcmask, gx, gy, gz, a.nnc0, a.nnc1, a.nnc2)
+              ? 0.0
+              : xc[cg_index(gx, gy, gz, a.nnc0, a.nnc1)];
+    }
+    s_in[i] = v;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < M * N * N; o += blockDim.x) {  // x sweep: [l][j][r]
+    const int r = o % M, jl = o / M;
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) s = fma(E.E[r][i], s_in[i + N * jl], s);
+    s_1[o] = s;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < M * M * N; o += blockDim.x) {  // y sweep: [l][s][r]
+    const int r = o % M, sidx = (o / M) % M, l = o / (M * M);
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(E.E[sidx][j], s_1[r + M * (j + N * l)], s);
+    s_2[o] = s;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < M * M * M; o += blockDim.x) {  // z sweep + write
+    const int r = o % M, sidx = (o / M) % M, tt = o / (M * M);
+    double s = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) s = fma(E.E[tt][l], s_2[r + M * (sidx + M * l)], s);
+    if (DG) {
+      // fine cell (2cx + r/N, ...), local (r%N, ...)
+      const int fx = 2 * cx + r / N, fy = 2 * cy + sidx / N, fz = 2 * cz + tt / N;
+      const int64_t fcell = fx + (int64_t)(2 * a.nc0) * (fy + (int64_t)(2 * a.nc1) * fz);
+      const int loc = r % N + N * ((sidx % N) + N * (tt % N));
+      xf[fcell * N * N * N + loc] += s;
+    } else {
+      // owned: local fine index < 2K unless this is the last coarse cell
+      if ((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
+          (tt == 2 * K && cz != a.nc2 - 1))
+        continue;
+      const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
+      if (cg_constrained(a.bcmask, gx, gy, gz, a.nnf0, a.nnf1, a.nnf2)) continue;
+      xf[cg_index(gx, gy, gz, a.nnf0, a.nnf1)] += s;
+    }
+  }
+}
+
+// xc (+)= P^T (bf - axf)   [axf may be null: P^T bf].  CG: xc must be zeroed (atomics).
+template <int K, bool DG>
+__global__ void restrict_kernel(TransferArgs a, Embed<K, DG> E, const double* __restrict__ bf,
+                                const double* __restrict__ axf, double* __restrict__ xc) {
+  constexpr int N = K + 1, M = Embed<K, DG>::M;
+  extern __shared__ double smem[];
+  double* s_in = smem;               // M^3
+  double* s_1 = smem + M * M * M;    // N M^2
+  double* s_2 = smem;                // N^2 M (aliases s_in, dead after the x sweep)
+  const int64_t cell = blockIdx.x;
+  const int cx = (int)(cell % a.nc0);
+  const int64_t rr = cell / a.nc0;
+  const int cy = (int)(rr % a.nc1), cz = (int)(rr / a.nc1);
+  for (int o = threadIdx.x; o < M * M * M; o += blockDim.x) {
+    const int r = o % M, sidx = (o / M) % M, tt = o / (M * M);
+    double v = 0.0;
+    if (DG) {
+      const int fx = 2 * cx + r / N, fy = 2 * cy + sidx / N, fz = 2 * cz + tt / N;
+      const int64_t fcell = fx + (int64_t)(2 * a.nc0) * (fy + (int64_t)(2 * a.nc1) * fz);
+      const int64_t idx = fcell * N * N * N + r % N + N * ((sidx % N) + N * (tt % N));
+      v = bf[idx] - (axf ? axf[idx] : 0.0);
+    } else {
+      const bool owned = !((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
+                           (tt == 2 * K && cz != a.nc2 - 1));
+      const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
+      if (owned && !cg_constrained(a.bcmask, gx, gy, gz, a.nnf0, a.nnf1, a.nnf2)) {
+        const int64_t idx = cg_index(gx, gy, gz, a.nnf0, a.nnf1);
+        v = bf[idx] - (axf ? axf[idx] : 0.0);
+      }
+    }
+    s_in[o] = v;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < N * M * M; o += blockDim.x) {  // x: [t][s][i]
+    const int i = o % N, st = o / N;
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < M; ++r) s = fma(E.E[r][i], s_in[r + M * st], s);
+    s_1[o] = s;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < N * N * M; o += blockDim.x) {  // y: [t][j][i]
+    const int i = o % N, j = (o / N) % N, tt = o / (N * N);
+    double s = 0.0;
+#pragma unroll
+    for (int sidx = 0; sidx < M; ++sidx) s = fma(E.E[sidx][j], s_1[i + N * (sidx + M * tt)], s);
+    s_2[o] = s;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < N * N * N; o += blockDim.x) {  // z: [l][j][i]
+    const int i = o % N, j = (o / N) % N, l = o / (N * N);
+    double s = 0.0;
+#pragma unroll
+    for (int tt = 0; tt < M; ++tt) s = fma(E.E[tt][l], s_2[i + N * (j + N * tt)], s);
+    if (DG) {
+      xc[cell * N * N * N + o] = s;
+    } else {
+      const int gx = K * cx + i, gy = K * cy + j, gz = K * cz + l;
+      if (!cg_constrained(a.bcmask, gx, gy, gz, a.nnc0, a.nnc1, a.nnc2))
+        atomicAdd(xc + cg_index(gx, gy, gz, a.nnc0, a.nnc1), s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- vectors
+__global__ void cheb_step_kernel(double* __restrict__ xn, const double* __restrict__ x,
+                                 const double* __restrict__ xo, const double* __restrict__ b,
+                                 double* __restrict__ ax, const double* __restrict__ dinv, double c1,
+                                 double c2, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double xi = x ? x[i] : 0.0;
+    const double xoi = xo ? xo[i] : 0.0;
+    const double r = b[i] - (ax ? ax[i] : 0.0);
+    xn[i] = xi + c1 * (xi - xoi) + c2 * dinv[i] * r;
+  }
+}
+
+__global__ void axpby_kernel(double* __restrict__ y, const double* __restrict__ x, double a, double b,
+                             int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = a * x[i] + b * y[i];
+}
+
+__global__ void sub_kernel(double* __restrict__ r, const double* __restrict__ b,
+                           const double* __restrict__ ax, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = b[i] - ax[i];
+}
+
+__global__ void dinv_kernel(const double* __restrict__ d, double* __restrict__ di, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    di[i] = 1.0 / d[i];
+}
+
+__device__ __forceinline__ double u01_splitmix(uint64_t seed, uint64_t i) {
+  uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  z = z ^ (z >> 31);
+  return 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+}
+
+__global__ void splitmix_kernel(double* __restrict__ s, uint64_t seed, int64_t first, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s[i] = u01_splitmix(seed, (uint64_t)(first + i));
+}
+
+// ---- deterministic block reduction with a last-block finisher
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+  __syncthreads();
+  return s;
+}
+
+__device__ unsigned int g_red_counter[16];
+
+__device__ __forceinline__ void finish_reduction(double part, double* red, double* out, int slot) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    red[blockIdx.x] = part;
+    __threadfence();
+    const unsigned prev = atomicAdd(&g_red_counter[slot], 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __shared__ double sh[32];
+    double v = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v += ((volatile double*)red)[i];
+    const double s = block_sum(v, sh);
+    if (threadIdx.x == 0) {
+      out[slot] = s;
+      g_red_counter[slot] = 0;
+    }
+  }
+}
+
+__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                           double* red, double* out, int slot) {
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v = fma(a[i], b[i], v);
+  const double s = block_sum(v, sh);
+  finish_reduction(s, red, out, slot);
+}
+
+// alpha = scal[0]/scal[1]  (rz / pq);  x += alpha p;  r -= alpha q;  scal[2] = (r, r)
+__global__ void pcg_update_xr_kernel(double* __restrict__ x, double* __restrict__ r,
+                                     const double* __restrict__ p, const double* __restrict__ q,
+                                     int64_t n, double* red, double* scal) {
+  __shared__ double sh[32];
+  const double alpha = scal[0] / scal[1];
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    v = fma(ri, ri, v);
+  }
+  const double s = block_sum(v, sh);
+  finish_reduction(s, red, scal, 2);
+}
+
+// beta = scal[3]/scal[0] (rz_new / rz);  p = z + beta p
+__global__ void pcg_update_p_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                                    const double* scal) {
+  const double beta = scal[3] / scal[0];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+__global__ void copy_scalar_kernel(double* scal, int dst, int src) { scal[dst] = scal[src]; }
+
+// x = A0^{-1} b on the free DoFs (dense inverse from the Cholesky factor); x = 0 elsewhere.
+__global__ void coarse_solve_kernel(const double* __restrict__ Ainv, const int* __restrict__ free_idx,
+                                    int nf, const double* __restrict__ b, double* __restrict__ x,
+                                    int64_t n) {
+  extern __shared__ double sb[];
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) sb[i] = b[free_idx[i]];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = 0.0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < nf; ++j) s = fma(Ainv[(int64_t)i * nf + j], sb[j], s);
+    x[free_idx[i]] = s;
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+namespace {
+
+inline unsigned vec_grid(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+TransferArgs transfer_args(const fem_ctx* h, const Level& c, const Level& f) {
+  TransferArgs a;
+  a.nc0 = c.n[0];
+  a.nc1 = c.n[1];
+  a.nc2 = c.n[2];
+  a.nnc0 = c.nn[0];
+  a.nnc1 = c.nn[1];
+  a.nnc2 = c.nn[2];
+  a.nnf0 = f.nn[0];
+  a.nnf1 = f.nn[1];
+  a.nnf2 = f.nn[2];
+  int mask = 0;
+  for (int s = 0; s < 6; ++s)
+    if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
+  a.bcmask = mask;
+  return a;
+}
+
+template <int K, bool DG>
+Embed<K, DG> make_embed(const Tables1D& t) {
+  Embed<K, DG> e;
+  constexpr int N = K + 1;
+  for (int r = 0; r < Embed<K, DG>::M; ++r)
+    for (int j = 0; j < N; ++j) e.E[r][j] = DG ? t.dg_embed[r / N][r % N][j] : t.cg_embed[r][j];
+  return e;
+}
+
+template <int K, bool DG>
+void prolongate_kd(fem_ctx* h, const Level& c, const Level& f, const double* xc, double* xf) {
+  constexpr int N = K + 1, M = Embed<K, DG>::M;
+  const size_t sm = sizeof(double) * (N * N * N + M * N * N + M * M * N);
+  static bool attr = false;
+  if (!attr) {
+    FEM_CUDA_TRY(cudaFuncSetAttribute(prolongate_kernel<K, DG>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  prolongate_kernel<K, DG><<<(unsigned)c.n_cells, 128, sm, h->stream>>>(
+      transfer_args(h, c, f), make_embed<K, DG>(h->tab), xc, xf);
+  count_launch();
+  check_launch("prolongate_kernel");
+}
+
+template <int K, bool DG>
+void restrict_kd(fem_ctx* h, const Level& c, const Level& f, const double* bf, const double* axf,
+                 double* xc) {
+  constexpr int N = K + 1, M = Embed<K, DG>::M;
+  const size_t sm = sizeof(double) * (M * M * M + N * M * M);
+  static bool attr = false;
+  if (!attr) {
+    FEM_CUDA_TRY(cudaFuncSetAttribute(restrict_kernel<K, DG>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  restrict_kernel<K, DG><<<(unsigned)c.n_cells, 128, sm, h->stream>>>(
+      transfer_args(h, c, f), make_embed<K, DG>(h->tab), bf, axf, xc);
+  count_launch();
+  check_launch("restrict_kernel");
+}
+
+template <int K>
+void prolongate_k(fem_ctx* h, const Level& c, const Level& f, const double* xc, double* xf) {
+  if (h->method == FEM_CG) prolongate_kd<K, false>(h, c, f, xc, xf);
+  else prolongate_kd<K, true>(h, c, f, xc, xf);
+}
+
+template <int K>
+void restrict_k(fem_ctx* h, const Level& c, const Level& f, const double* bf, const double* axf,
+                double* xc) {
+  if (h->method == FEM_CG) restrict_kd<K, false>(h, c, f, bf, axf, xc);
+  else restrict_kd<K, true>(h, c, f, bf, axf, xc);
+}
+
+#define FEM_DISPATCH_K(k, fn, ...)                           \
+  switch (k) {                                               \
+    case 1: fn<1>(__VA_ARGS__); break;                       \
+    case 2: fn<2>(__VA_ARGS__); break;                       \
+    case 3: fn<3>(__VA_ARGS__); break;                       \
+    case 4: fn<4>(__VA_ARGS__); break;                       \
+    case 5: fn<5>(__VA_ARGS__); break;                       \
+    case 6: fn<6>(__VA_ARGS__); break;                       \
+    case 7: fn<7>(__VA_ARGS__); break;                       \
+    case 8: fn<8>(__VA_ARGS__); break;                       \
+    default: throw Error{FEM_E_ARG, "degree out of range"}; \
+  }
+
+}  // namespace
+
+void launch_prolongate_add(fem_ctx* h, const Level& c, const Level& f, const double* xc, double* xf) {
+  FEM_DISPATCH_K(h->k, prolongate_k, h, c, f, xc, xf);
+}
+
+void launch_restrict(fem_ctx* h, const Level& c, const Level& f, const double* bf, const double* axf,
+                     double* xc) {
+  if (h->method == FEM_CG) launch_zero(h, xc, c.n_dofs);
+  FEM_DISPATCH_K(h->k, restrict_k, h, c, f, bf, axf, xc);
+}
+
+void launch_zero(fem_ctx* h, double* p, int64_t n) {
+  FEM_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double) * n, h->stream));
+}
+
+void launch_copy(fem_ctx* h, double* dst, const double* src, int64_t n) {
+  FEM_CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, h->stream));
+}
+
+void launch_dinv(fem_ctx* h, Level& L) {
+  dinv_kernel<<<vec_grid(L.n_dofs), 256, 0, h->stream>>>(L.diag, L.dinv, L.n_dofs);
+  count_launch();
+  check_launch("dinv_kernel");
+}
+
+void launch_splitmix(fem_ctx* h, const Level& L, uint64_t seed, double* s) {
+  splitmix_kernel<<<vec_grid(L.n_dofs), 256, 0, h->stream>>>(s, seed, 0, L.n_dofs);
+  count_launch();
+  check_launch("splitmix_kernel");
+}
+
+void launch_cheb_step(fem_ctx* h, const Level& L, double* xn, const double* x, const double* xo,
+                      const double* b, double* ax, double c1, double c2, bool has_xo) {
+  cheb_step_kernel<<<vec_grid(L.n_dofs), 256, 0, h->stream>>>(xn, x, has_xo ? xo : nullptr, b, ax,
+                                                              L.dinv, c1, c2, L.n_dofs);
+  count_launch();
+  check_launch("cheb_step_kernel");
+}
+
+void launch_dot(fem_ctx* h, const double* a, const double* b, int64_t n, int slot) {
+  dot_kernel<<<kRedBlocks, kRedThreads, 0, h->stream>>>(a, b, n, h->red + slot * kRedBlocks, h->scal,
+                                                        slot);
+  count_launch();
+  check_launch("dot_kernel");
+}
+
+void launch_pcg_update_xr(fem_ctx* h, double* x, double* r, const double* p, double* q, int64_t n) {
+  pcg_update_xr_kernel<<<kRedBlocks, kRedThreads, 0, h->stream>>>(x, r, p, q, n,
+                                                                  h->red + 2 * kRedBlocks, h->scal);
+  count_launch();
+  check_launch("pcg_update_xr_kernel");
+}
+
+void launch_pcg_update_p(fem_ctx* h, double* p, const double* z, int64_t n) {
+  pcg_update_p_kernel<<<vec_grid(n), 256, 0, h->stream>>>(p, z, n, h->scal);
+  count_launch();
+  check_launch("pcg_update_p_kernel");
+  copy_scalar_kernel<<<1, 1, 0, h->stream>>>(h->scal, 0, 3);
+  count_launch();
+  check_launch("copy_scalar_kernel");
+}
+
+void launch_coarse_solve(fem_ctx* h, const double* b, double* x) {
+  const Level& L0 = h->levels[0];
+  coarse_solve_kernel<<<1, 512, sizeof(double) * h->n_coarse_free, h->stream>>>(
+      h->coarse_inv, h->coarse_free, h->n_coarse_free, b, x, L0.n_dofs);
+  count_launch();
+  check_launch("coarse_solve_kernel");
+}
+
+void launch_axpby(fem_ctx* h, double* y, const double* x, double a, double b, int64_t n) {
+  axpby_kernel<<<vec_grid(n), 256, 0, h->stream>>>(y, x, a, b, n);
+  count_launch();
+  check_launch("axpby_kernel");
+}
+
+void launch_sub(fem_ctx* h, double* r, const double* b, const double* ax, int64_t n) {
+  sub_kernel<<<vec_grid(n), 256, 0, h->stream>>>(r, b, ax, n);
+  count_launch();
+  check_launch("sub_kernel");
+}
+
+}  // namespace fem

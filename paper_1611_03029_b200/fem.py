@@ -1,0 +1,267 @@
+"""Thin ctypes binding of libfem (include/fem.h): argument marshalling only.
+
+Every step of the hot path runs in libfem's CUDA kernels; this module converts
+torch tensors / numpy arrays to (pointer, length) pairs and return codes to
+exceptions.  There is no fallback: if libfem.so is missing or fails to load,
+importing the binding raises.
+
+Names follow the C ABI: fem_setup -> Fem(...), fem_apply -> Fem.fem_apply, etc.
+Vectors may be CUDA tensors (used in place, asynchronous on the handle's
+stream) or host numpy arrays / CPU tensors (staged by libfem, synchronous).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfem.so")
+
+FEM_OK, FEM_NOT_CONVERGED = 0, 1
+ERRORS = {-1: "FEM_E_ARG", -2: "FEM_E_SIZE", -3: "FEM_E_GEOMETRY", -4: "FEM_E_BREAKDOWN",
+          -5: "FEM_E_CUDA", -6: "FEM_E_NCCL", -7: "FEM_E_OOM"}
+FEM_CG, FEM_SIPG = 0, 1
+FEM_BC_DIRICHLET, FEM_BC_NEUMANN = 0, 1
+
+
+class FemError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class fem_mesh(C.Structure):
+    _fields_ = [("n", C.c_int32 * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3),
+                ("deform_eps", C.c_double), ("bc", C.c_int32 * 6), ("rank", C.c_int32),
+                ("nranks", C.c_int32), ("nccl_id", C.c_void_p)]
+
+
+class fem_options(C.Structure):
+    _fields_ = [("penalty_factor", C.c_double), ("cheb_degree", C.c_int32),
+                ("cheb_lo", C.c_double), ("cheb_hi", C.c_double), ("eig_iters", C.c_int32),
+                ("coarse_cells", C.c_int32), ("eig_seed", C.c_uint64),
+                ("lambda_override", C.POINTER(C.c_double)), ("stream", C.c_void_p),
+                ("device", C.c_int32), ("profile", C.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libfem.so not built ({LIB_PATH}); run `python -m paper_1611_03029_b200.build`")
+    lib = C.CDLL(LIB_PATH)
+    P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    sig = {
+        "fem_default_options": (C.c_int, [C.POINTER(fem_options)]),
+        "fem_setup": (C.c_int, [C.POINTER(fem_mesh), I32, I32, C.POINTER(fem_options), C.POINTER(P)]),
+        "fem_info": (C.c_int, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I32)]),
+        "fem_apply": (C.c_int, [P, P, I64, P, I64]),
+        "fem_diagonal": (C.c_int, [P, P, I64]),
+        "mg_vcycle": (C.c_int, [P, P, I64, P, I64]),
+        "cg_solve": (C.c_int, [P, P, I64, P, I64, D, I32, C.POINTER(I32), C.POINTER(D)]),
+        "fem_rhs": (C.c_int, [P, P, I64]),
+        "fem_level_info": (C.c_int, [P, I32, C.POINTER(I64), C.POINTER(I32)]),
+        "fem_level_apply": (C.c_int, [P, I32, P, I64, P, I64]),
+        "fem_level_diagonal": (C.c_int, [P, I32, P, I64]),
+        "fem_level_lambda": (C.c_int, [P, I32, C.POINTER(D)]),
+        "fem_level_geometry": (C.c_int, [P, I32, P, I64]),
+        "mg_smooth": (C.c_int, [P, I32, P, I64, P, I64, I32]),
+        "mg_prolongate_add": (C.c_int, [P, I32, P, I64, P, I64]),
+        "mg_restrict": (C.c_int, [P, I32, P, I64, P, I64]),
+        "mg_coarse_solve": (C.c_int, [P, P, I64, P, I64]),
+        "fem_sync": (C.c_int, [P]),
+        "fem_kernel_launches": (I64, []),
+        "fem_profile_read": (C.c_int, [P, C.POINTER(D), C.POINTER(I64), I32]),
+        "fem_last_error": (C.c_char_p, []),
+        "fem_destroy": (None, [P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
+
+
+_lib = _load()
+
+# exported symbol list (tests check it against include/fem.h)
+SYMBOLS = ("fem_default_options", "fem_setup", "fem_info", "fem_apply", "fem_diagonal", "mg_vcycle",
+           "cg_solve", "fem_rhs", "fem_level_info", "fem_level_apply", "fem_level_diagonal",
+           "fem_level_lambda", "fem_level_geometry", "mg_smooth", "mg_prolongate_add", "mg_restrict",
+           "mg_coarse_solve", "fem_sync", "fem_kernel_launches", "fem_profile_read", "fem_last_error",
+           "fem_destroy")
+
+
+def lib():
+    return _lib
+
+
+def kernel_launches() -> int:
+    return int(_lib.fem_kernel_launches())
+
+
+def _check(rc: int, allow=(FEM_OK,)):
+    if rc not in allow:
+        raise FemError(rc, _lib.fem_last_error().decode())
+    return rc
+
+
+def _vec(v, writable=False):
+    """(pointer, length) of a contiguous float64 torch tensor or numpy array."""
+    if hasattr(v, "data_ptr"):            # torch tensor
+        import torch
+        if v.dtype != torch.float64 or not v.is_contiguous():
+            raise TypeError("vectors must be contiguous float64 tensors")
+        return C.c_void_p(v.data_ptr()), v.numel()
+    a = v
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+        raise TypeError("vectors must be contiguous float64 numpy arrays or torch tensors")
+    if writable and not a.flags["WRITEABLE"]:
+        raise TypeError("output array is read-only")
+    return C.c_void_p(a.ctypes.data), a.size
+
+
+class Fem:
+    """One libfem handle (fem_setup ... fem_destroy)."""
+
+    def __init__(self, cells, degree, method=FEM_CG, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0),
+                 deform_eps=0.0, bc=(FEM_BC_DIRICHLET,) * 6, penalty_factor=None, cheb_degree=None,
+                 cheb_lo=None, cheb_hi=None, eig_iters=None, coarse_cells=None, eig_seed=None,
+                 lambda_override=None, stream=None, device=None, profile=False):
+        m = fem_mesh()
+        m.n[:] = list(cells)
+        m.lo[:] = list(lo)
+        m.hi[:] = list(hi)
+        m.deform_eps = deform_eps
+        m.bc[:] = list(bc)
+        m.rank, m.nranks, m.nccl_id = 0, 1, None
+        o = fem_options()
+        _check(_lib.fem_default_options(C.byref(o)))
+        for name, val in (("penalty_factor", penalty_factor), ("cheb_degree", cheb_degree),
+                          ("cheb_lo", cheb_lo), ("cheb_hi", cheb_hi), ("eig_iters", eig_iters),
+                          ("coarse_cells", coarse_cells), ("eig_seed", eig_seed)):
+            if val is not None:
+                setattr(o, name, val)
+        self._lam = None
+        if lambda_override is not None:
+            self._lam = (C.c_double * len(lambda_override))(*lambda_override)
+            o.lambda_override = C.cast(self._lam, C.POINTER(C.c_double))
+        if stream is not None:
+            o.stream = C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+        if device is not None:
+            o.device = device
+        o.profile = 1 if profile else 0
+        h = C.c_void_p()
+        _check(_lib.fem_setup(C.byref(m), degree, method, C.byref(o), C.byref(h)))
+        self.h = h
+        self.degree, self.method, self.cells = degree, method, tuple(cells)
+        nl, ng, fg, lv = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+        _check(_lib.fem_info(h, C.byref(nl), C.byref(ng), C.byref(fg), C.byref(lv)))
+        self.n_local, self.n_global, self.first_global, self.n_levels = nl.value, ng.value, fg.value, lv.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.fem_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- finest level
+    def fem_apply(self, x, y):
+        px, nx = _vec(x)
+        py, ny = _vec(y, True)
+        _check(_lib.fem_apply(self.h, px, nx, py, ny))
+        return y
+
+    def fem_diagonal(self, d):
+        p, n = _vec(d, True)
+        _check(_lib.fem_diagonal(self.h, p, n))
+        return d
+
+    def mg_vcycle(self, r, z):
+        pr, nr = _vec(r)
+        pz, nz = _vec(z, True)
+        _check(_lib.mg_vcycle(self.h, pr, nr, pz, nz))
+        return z
+
+    def cg_solve(self, b, x, rtol=1e-10, maxit=1000):
+        pb, nb = _vec(b)
+        px, nx = _vec(x, True)
+        its, rel = C.c_int32(), C.c_double()
+        rc = _check(_lib.cg_solve(self.h, pb, nb, px, nx, rtol, maxit, C.byref(its), C.byref(rel)),
+                    (FEM_OK, FEM_NOT_CONVERGED))
+        return its.value, rel.value, rc == FEM_OK
+
+    def fem_rhs(self, b):
+        p, n = _vec(b, True)
+        _check(_lib.fem_rhs(self.h, p, n))
+        return b
+
+    # ---- level-wise
+    def level_info(self, level):
+        n = C.c_int64()
+        cells = (C.c_int32 * 3)()
+        _check(_lib.fem_level_info(self.h, level, C.byref(n), cells))
+        return n.value, tuple(cells)
+
+    def fem_level_apply(self, level, x, y):
+        px, nx = _vec(x)
+        py, ny = _vec(y, True)
+        _check(_lib.fem_level_apply(self.h, level, px, nx, py, ny))
+        return y
+
+    def fem_level_diagonal(self, level, d):
+        p, n = _vec(d, True)
+        _check(_lib.fem_level_diagonal(self.h, level, p, n))
+        return d
+
+    def fem_level_lambda(self, level):
+        v = C.c_double()
+        _check(_lib.fem_level_lambda(self.h, level, C.byref(v)))
+        return v.value
+
+    def fem_level_geometry(self, level, G):
+        p, n = _vec(G, True)
+        _check(_lib.fem_level_geometry(self.h, level, p, n))
+        return G
+
+    def mg_smooth(self, level, b, x, x_is_zero):
+        pb, nb = _vec(b)
+        px, nx = _vec(x, True)
+        _check(_lib.mg_smooth(self.h, level, pb, nb, px, nx, 1 if x_is_zero else 0))
+        return x
+
+    def mg_prolongate_add(self, level, xc, xf):
+        pc, nc = _vec(xc)
+        pf, nf = _vec(xf, True)
+        _check(_lib.mg_prolongate_add(self.h, level, pc, nc, pf, nf))
+        return xf
+
+    def mg_restrict(self, level, xf, xc):
+        pf, nf = _vec(xf)
+        pc, nc = _vec(xc, True)
+        _check(_lib.mg_restrict(self.h, level, pf, nf, pc, nc))
+        return xc
+
+    def mg_coarse_solve(self, b, x):
+        pb, nb = _vec(b)
+        px, nx = _vec(x, True)
+        _check(_lib.mg_coarse_solve(self.h, pb, nb, px, nx))
+        return x
+
+    def fem_sync(self):
+        _check(_lib.fem_sync(self.h))
+
+    def fem_profile_read(self, reset=False):
+        ms, n = C.c_double(), C.c_int64()
+        _check(_lib.fem_profile_read(self.h, C.byref(ms), C.byref(n), 1 if reset else 0))
+        return ms.value, n.value

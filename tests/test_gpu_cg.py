@@ -1,0 +1,238 @@
+"""GPU parity of the CG path (libfem through the C ABI) against the CPU oracle.
+
+Tolerances: operator/diagonal/transfer/geometry relative max-norm <= 1e-12
+(north_star: per-apply agreement within relative 1e-12 in the max norm);
+V-cycle with lambda pinned <= 1e-11; PCG iterations within +-1,
+both true residuals <= tol, L2 errors within 3 significant digits.
+"""
+import numpy as np
+import pytest
+import torch
+
+import fem_inputs
+from oracle import cg as ocg, multigrid as omg, problem as oprob, transfer as otr
+from oracle.mesh import Mesh, CG, DIRICHLET, NEUMANN
+
+pytestmark = pytest.mark.gpu
+
+MIXED = (DIRICHLET, NEUMANN, DIRICHLET, DIRICHLET, NEUMANN, DIRICHLET)
+
+
+def fem_mod():
+    from paper_1611_03029_b200 import fem
+    return fem
+
+
+def relmax(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def make(cells, k, eps=0.0, bc=(DIRICHLET,) * 6, **kw):
+    f = fem_mod()
+    return f.Fem(cells, k, f.FEM_CG, deform_eps=eps, bc=bc, **kw), Mesh(cells, k, eps=eps, bc=bc)
+
+
+@pytest.mark.parametrize("k,cells,eps,bc", [
+    (2, (8, 8, 8), 0.0, (DIRICHLET,) * 6),       # C1
+    (1, (5, 3, 4), 0.05, MIXED),
+    (2, (3, 4, 5), 0.05, MIXED),
+    (3, (4, 3, 2), 0.05, (DIRICHLET,) * 6),
+    (4, (6, 4, 3), 0.05, MIXED),                 # several cell batches + ragged tail
+    (4, (7, 5, 3), 0.0, (DIRICHLET,) * 6),
+    (5, (3, 2, 3), 0.05, MIXED),
+    (6, (2, 3, 2), 0.05, (DIRICHLET,) * 6),
+    (7, (2, 2, 2), 0.05, MIXED),
+    (8, (2, 1, 2), 0.0, (DIRICHLET,) * 6),
+])
+def test_apply_and_diagonal_match_oracle(k, cells, eps, bc):
+    F, m = make(cells, k, eps, bc)
+    x = fem_inputs.uniform_pm1(0, m.cg_n_dofs())
+    y = torch.zeros(m.cg_n_dofs(), dtype=torch.float64, device="cuda")
+    F.fem_apply(dev(x), y)
+    torch.cuda.synchronize()
+    yo = ocg.apply(m, x)
+    assert relmax(host(y), yo) <= 1e-12
+    d = torch.zeros_like(y)
+    F.fem_diagonal(d)
+    assert relmax(host(d), ocg.diagonal(m)) <= 1e-12
+    F.close()
+
+
+def test_c1_exact_diagonal_and_host_vectors():
+    from tests.conftest import golden
+    g = golden("c1_diagonal.json")
+    w = fem_inputs.C1
+    F, m = make(w.cells, w.degree)
+    d = np.zeros(m.cg_n_dofs())
+    F.fem_diagonal(d)                          # host vector path
+    gc = m.cg_node_coords()
+    n_mid = (gc % 2 == 1).sum(axis=1)
+    vals = np.array([g["free_values"][kk] for kk in ("vvv", "one_m", "two_m", "mmm")])[n_mid]
+    mask = m.cg_dirichlet_mask()
+    assert np.all(d[mask] == 1.0)
+    assert np.allclose(d[~mask], vals[~mask], rtol=1e-14, atol=0)
+    # host and device apply agree bit for bit (same kernels)
+    x = fem_inputs.uniform_pm1(w.seed, m.cg_n_dofs())
+    yh = np.zeros_like(x)
+    F.fem_apply(x, yh)
+    assert relmax(yh, ocg.apply(m, x)) <= 1e-12
+
+
+def test_geometry_table_matches_oracle_metric():
+    F, m = make((3, 4, 2), 3, 0.05, MIXED)
+    nl = F.n_levels
+    n_dofs, cells = F.level_info(nl - 1)
+    N = 4
+    G = np.zeros(np.prod(cells) * 6 * N ** 3)
+    F.fem_level_geometry(nl - 1, G)
+    Go = ocg.metric(m, np.arange(m.n_cells), ocg.CellQuadrature(3))     # [C, q, 3, 3]
+    comps = [(0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2)]
+    Gr = G.reshape(m.n_cells, 6, N ** 3)
+    for c, (a, b) in enumerate(comps):
+        assert relmax(Gr[:, c, :], Go[:, :, a, b]) <= 1e-13
+
+
+def test_rhs_matches_oracle():
+    F, m = make((4, 4, 2), 4, 0.05)
+    b = np.zeros(m.cg_n_dofs())
+    F.fem_rhs(b)
+    assert relmax(b, oprob.rhs(m, CG)) <= 1e-12
+
+
+def test_errors():
+    f = fem_mod()
+    F, m = make((2, 2, 2), 2)
+    with pytest.raises(f.FemError) as e:
+        F.fem_apply(np.zeros(5), np.zeros(m.cg_n_dofs()))
+    assert e.value.code == -2
+    with pytest.raises(f.FemError) as e:
+        F.fem_level_apply(17, np.zeros(5), np.zeros(5))
+    assert e.value.code == -1
+    with pytest.raises(f.FemError) as e:
+        f.Fem((2, 2, 2), 2, f.FEM_CG, deform_eps=-0.9)   # folds cells: det J <= 0
+    assert e.value.code == -3 and "cell" in str(e.value)
+
+
+@pytest.mark.parametrize("k,cells,eps", [(2, (8, 4, 4), 0.05), (4, (4, 4, 8), 0.0), (3, (4, 2, 4), 0.05)])
+def test_levels_transfers_coarse_lambda(k, cells, eps):
+    F, m = make(cells, k, eps, MIXED)
+    mg = omg.Multigrid(m, CG)
+    assert F.n_levels == len(mg.levels)
+    for l, lev in enumerate(mg.levels):
+        n, c = F.level_info(l)
+        assert c == lev.mesh.n and n == lev.n_dofs
+        x = fem_inputs.uniform_pm1(l, n) * lev.free
+        y = np.zeros(n)
+        F.fem_level_apply(l, x, y)
+        assert relmax(y, lev.apply(x)) <= 1e-12
+        d = np.zeros(n)
+        F.fem_level_diagonal(l, d)
+        assert relmax(d, lev.diagonal()) <= 1e-12
+        if l >= 1:
+            assert abs(F.fem_level_lambda(l) - lev.lam) <= 1e-10 * lev.lam
+            cm = mg.levels[l - 1]
+            xc = fem_inputs.uniform_pm1(100 + l, cm.n_dofs) * cm.free
+            xf = fem_inputs.uniform_pm1(200 + l, n) * lev.free
+            out = xf.copy()
+            F.mg_prolongate_add(l, xc, out)
+            assert relmax(out, xf + mg.prolongate(l, xc)) <= 1e-12
+            rc = np.zeros(cm.n_dofs)
+            F.mg_restrict(l, xf, rc)
+            assert relmax(rc, mg.restrict(l, xf)) <= 1e-12
+    b0 = fem_inputs.uniform_pm1(9, mg.levels[0].n_dofs) * mg.levels[0].free
+    x0 = np.zeros_like(b0)
+    F.mg_coarse_solve(b0, x0)
+    assert relmax(x0, mg.coarse_solve(b0)) <= 1e-11
+
+
+def test_smoother_and_vcycle_with_pinned_lambda():
+    cells, k, eps = (8, 8, 4), 3, 0.05
+    m = Mesh(cells, k, eps=eps, bc=MIXED)
+    mg = omg.Multigrid(m, CG)
+    lam = [0.0] + [lev.lam for lev in mg.levels[1:]]
+    F = fem_mod().Fem(cells, k, fem_mod().FEM_CG, deform_eps=eps, bc=MIXED, lambda_override=lam)
+    L = len(mg.levels) - 1
+    b = fem_inputs.uniform_pm1(3, mg.fine.n_dofs) * mg.fine.free
+    x = np.zeros_like(b)
+    F.mg_smooth(L, b, x, True)
+    xo = omg.chebyshev(mg.fine, b, None, 5, 0.06, 1.2, True)
+    assert relmax(x, xo) <= 1e-12
+    x2 = x.copy()
+    F.mg_smooth(L, b, x2, False)
+    assert relmax(x2, omg.chebyshev(mg.fine, b, xo, 5, 0.06, 1.2, False)) <= 1e-12
+    z = np.zeros_like(b)
+    F.mg_vcycle(b, z)
+    assert relmax(z, mg.vcycle(b)) <= 1e-11
+
+
+@pytest.mark.parametrize("cells,eps", [((8, 8, 8), 0.05), ((8, 8, 8), 0.0)])
+def test_pcg_matches_oracle(cells, eps):
+    k = 4
+    F, m = make(cells, k, eps)
+    mg = omg.Multigrid(m, CG)
+    b = oprob.rhs(m, CG)
+    hist = []
+    xo, its_o, rr_o = mg.pcg(b, tol=1e-10, history=hist)
+    x = np.zeros_like(b)
+    its, rr, ok = F.cg_solve(b, x, rtol=1e-10)
+    assert ok and rr <= 1e-10
+    assert abs(its - its_o) <= 1
+    true_res = np.linalg.norm(b - mg.fine.apply(x)) / np.linalg.norm(b)
+    assert true_res <= 1e-9
+    e_gpu, e_or = oprob.l2_error(m, CG, x), oprob.l2_error(m, CG, xo)
+    assert abs(e_gpu - e_or) <= 5e-4 * e_or
+
+
+@pytest.mark.slow
+def test_c2_full_solve_matches_oracle():
+    w = fem_inputs.C2
+    F, m = make(w.cells, w.degree, w.deform_eps)
+    b = np.zeros(m.cg_n_dofs())
+    F.fem_rhs(b)
+    assert relmax(b, oprob.rhs(m, CG)) <= 1e-12
+    mg = omg.Multigrid(m, CG)
+    for l in range(1, len(mg.levels)):
+        assert abs(F.fem_level_lambda(l) - mg.levels[l].lam) <= 1e-9 * mg.levels[l].lam
+    xo, its_o, _ = mg.pcg(b, tol=1e-10)
+    x = np.zeros_like(b)
+    its, rr, ok = F.cg_solve(b, x, rtol=1e-10)
+    assert ok and abs(its - its_o) <= 1
+    assert np.linalg.norm(b - mg.fine.apply(x)) / np.linalg.norm(b) <= 1e-9
+    e_gpu, e_or = oprob.l2_error(m, CG, x), oprob.l2_error(m, CG, xo)
+    assert abs(e_gpu - e_or) <= 5e-4 * e_or
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled_apply_and_exact_solution():
+    w = fem_inputs.C4
+    F, m = make(w.cells, w.degree)
+    n = m.cg_n_dofs()
+    x7 = fem_inputs.uniform_pm1(w.seed, n)
+    xd = dev(x7)
+    y = torch.zeros_like(xd)
+    F.fem_apply(xd, y)
+    rows = np.unique(np.concatenate([
+        np.random.default_rng(0).integers(0, n, 400),
+        [0, 1, m.nn[0], n // 2, n - 1, n - 2],
+    ]))
+    yo = ocg.apply_rows(m, x7, rows)
+    yh = host(y)
+    assert np.abs(yh[rows] - yo).max() <= 1e-12 * np.abs(yo).max()
+    # R15: b = A x7 with Dirichlet rows zeroed -> the solution is x7 on free DoFs
+    b = y.clone()
+    bm = torch.from_numpy(m.cg_dirichlet_mask()).cuda()
+    b[bm] = 0.0
+    xs = torch.zeros_like(b)
+    its, rr, ok = F.cg_solve(b, xs, rtol=1e-10)
+    assert ok and its <= 8
+    err = (xs - xd)[~bm]
+    assert (err.norm() / xd[~bm].norm()).item() < 1e-8

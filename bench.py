@@ -1,0 +1,356 @@
+"""Benchmark: GMG-preconditioned CG solve of BASELINE.json configs[1] (C2) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+One step = one complete solve (operator applies, Chebyshev
+smoothing, transfers, coarse solve, PCG vector work) from x = 0 to ||r|| <= 1e-10 ||b||,
+with the right-hand side already resident in HBM.  value = DoFs solved per second
+over all ranks; ms_per_step = time to solution.  The dominant kernel (the
+finest-level operator apply) is timed live with CUDA events on the library's
+stream (fem_options.profile) and reported against the HBM roofline.
+
+--impl reference times the CPU oracle (oracle/, the "reference" of this tier) on
+the host cores: warm-up runs one full oracle solve (iteration count), each timed
+step is one oracle PCG iteration; value = n_dofs / (t_iteration * iterations).
+Multi-GPU (torchrun): the slab-partitioned path is not built yet, so N > 1 runs
+N independent replicas (weak scaling, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import fem_inputs  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+METRIC = "GMG-CG solve throughput (DoFs solved per second; ms_per_step = time to solution)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rtol", type=float, default=1e-10)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def workload_desc(w):
+    return (f"{w.name}: {'CG' if w.method == fem_inputs.CG else 'SIPG'} Q{w.degree} "
+            f"{'deformed (eps=%g)' % w.deform_eps if w.deform_eps else 'Cartesian'} "
+            f"{w.cells[0]}x{w.cells[1]}x{w.cells[2]} on [0,1]^3, Dirichlet, "
+            f"{'manufactured u=prod sin(pi x_d)' if w.rhs == 'manufactured' else 'b = A x_seed%d' % w.seed}")
+
+
+def algorithmic_apply_bytes(w, n_dofs):
+    """read x once + write y once (16 B/DoF) plus the streamed geometry
+    table on deformed meshes (6 doubles per quadrature point per cell)."""
+    n_cells = int(np.prod(w.cells))
+    geo = 48 * (w.degree + 1) ** 3 * n_cells if w.deform_eps else 0
+    return 16 * n_dofs + geo
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 3.0:   # sampler running before the load
+                time.sleep(0.02)
+            self.samples.clear()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=os.cpu_count())
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_solver(w):
+    from oracle import multigrid as omg, problem as oprob
+    from oracle.mesh import Mesh
+    m = Mesh(w.cells, w.degree, eps=w.deform_eps, bc=w.bc)
+    mg = omg.Multigrid(m, w.method, penalty_factor=w.penalty_factor)
+    if w.rhs == "manufactured":
+        b = oprob.rhs(m, w.method)
+    else:
+        x7 = fem_inputs.uniform_pm1(w.seed, mg.fine.n_dofs)
+        b = mg.fine.apply(x7)
+        b[~mg.fine.free] = 0.0
+    return mg, b
+
+
+def cpu_baseline(w, rtol):
+    """The oracle as it stands: one full PCG solve of the same workload (setup excluded)."""
+    mg, b = oracle_solver(w)
+    t0 = time.perf_counter()
+    _, its, rr = mg.pcg(b, tol=rtol)
+    t = time.perf_counter() - t0
+    n = mg.fine.n_dofs
+    return {"value": n / t, "unit": "DoF/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"one full oracle PCG solve of {w.name} ({its} iterations, relres {rr:.2e}), "
+                      f"setup (geometry, lambda estimates, coarse Cholesky) excluded",
+            "seconds": t}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, w):
+    rank, world, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    from oracle import multigrid as omg
+    mg, b = oracle_solver(w)
+    n = mg.fine.n_dofs
+    A = mg.fine.apply
+    # warm-up: one complete solve gives the oracle's own iteration count
+    _, its, rr = mg.pcg(b, tol=args.rtol)
+    for _ in range(max(args.warmup - 1, 0)):
+        mg.vcycle(b)
+    # timed steps: one PCG iteration each (apply, two dots, updates, V-cycle)
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = mg.vcycle(r)
+    p = z.copy()
+    rz = r @ z
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        q = A(p)
+        alpha = rz / (p @ q)
+        x += alpha * p
+        r -= alpha * q
+        _ = np.linalg.norm(r)
+        z = mg.vcycle(r)
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+        times.append(time.perf_counter() - t0)
+    t_iter = sum(times) / len(times)
+    t_solve = t_iter * its
+    value = n / t_solve
+    line = {
+        "impl": "reference", "metric": METRIC,
+        "value": value, "unit": "DoF/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_solve * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": {"workload": workload_desc(w), "n_dofs": n,
+                                                         "rtol": args.rtol, "iterations": its},
+        "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cpu_threads(), "kind": "oracle",
+                         "sample": f"each step = one oracle PCG iteration on the full {w.name} problem; "
+                                   f"value = n_dofs / (mean iteration time x {its} iterations)"},
+        "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def constrained_mask(w, n):
+    """Dirichlet-constrained CG nodes (input preparation only; index arithmetic)."""
+    import torch
+    k = w.degree
+    nn = [k * c + 1 for c in w.cells]
+    i = torch.arange(n, device="cuda")
+    g = [i % nn[0], (i // nn[0]) % nn[1], i // (nn[0] * nn[1])]
+    m = torch.zeros(n, dtype=torch.bool, device="cuda")
+    for d in range(3):
+        if w.bc[2 * d] == fem_inputs.DIRICHLET:
+            m |= g[d] == 0
+        if w.bc[2 * d + 1] == fem_inputs.DIRICHLET:
+            m |= g[d] == nn[d] - 1
+    return m
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, w):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1611_03029_b200 import fem
+
+    stream = torch.cuda.current_stream()
+    F = fem.Fem(w.cells, w.degree, w.method, deform_eps=w.deform_eps, bc=w.bc,
+                penalty_factor=w.penalty_factor, stream=stream, profile=True)
+    n = F.n_local
+    b = torch.zeros(n, dtype=torch.float64, device="cuda")
+    if w.rhs == "manufactured":
+        F.fem_rhs(b)
+    else:
+        xs = torch.from_numpy(fem_inputs.uniform_pm1(w.seed, n)).cuda()
+        F.fem_apply(xs, b)
+        del xs
+        b[constrained_mask(w, n)] = 0.0     # reading R15: b = A x_seed with Dirichlet rows zeroed
+    x = torch.zeros_like(b)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > L2
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()                                   # runs through warm-up and the timed region
+    its = 0
+    for _ in range(args.warmup):
+        x.zero_()
+        its, rr, ok = F.cg_solve(b, x, rtol=args.rtol)
+        assert ok, "warm-up solve did not converge"
+    F.fem_profile_read(reset=True)
+    launches0 = fem.kernel_launches()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(float(i))                       # evict L2 between steps (not timed)
+        x.zero_()
+        starts[i].record(stream)
+        its, rr, ok = F.cg_solve(b, x, rtol=args.rtol)
+        ends[i].record(stream)
+        assert ok and rr <= args.rtol
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = fem.kernel_launches() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_ms = sum(step_ms)
+    apply_ms, apply_launches = F.fem_profile_read(reset=True)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = tt.item()
+    value = world * n * args.steps / (t_ms * 1e-3)
+
+    # end to end through the C ABI with host buffers (copies inside the timed region)
+    bh = b.cpu().pin_memory()
+    xh = torch.zeros(n, dtype=torch.float64).pin_memory()
+    F.cg_solve(bh, xh, rtol=args.rtol)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for i in range(max(1, min(args.steps, 3))):
+        flush.fill_(float(i))
+        xh.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        F.cg_solve(bh, xh, rtol=args.rtol)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_value = world * n / (sum(e2e_t) / len(e2e_t))
+
+    hbm, hbm_src = peaks()
+    bytes_per_launch = algorithmic_apply_bytes(w, n)
+    avg_apply_s = apply_ms * 1e-3 / max(apply_launches, 1)
+    achieved = bytes_per_launch / avg_apply_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(w.name)
+    line = {
+        "metric": METRIC,
+        "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(w), "n_dofs": n, "rtol": args.rtol, "iterations": its,
+                   "l2": "flushed between steps (256 MiB write, outside the per-step events)",
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "step_ms": [round(s, 4) for s in step_ms]},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic,
+                     "kernel": "cg_apply_kernel (finest-level operator apply)",
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "avg_launch_us": avg_apply_s * 1e6, "launches": apply_launches,
+                     "peak_source": hbm_src},
+        "apply": {"dofs_per_s": n / avg_apply_s,
+                  "equivalent_dofs_per_s": int(np.prod(w.cells)) * w.degree ** 3 / avg_apply_s},
+        "clocks": clk,
+        "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 16 * n,
+                "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": launches,
+    }
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(w, args.rtol)
+        line["cpu_baseline"].pop("seconds", None)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    F.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    w = fem_inputs.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_ours(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -309,7 +309,8 @@ def run_ours(args, w):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(w.name)
+            entry = json.load(f).get(w.name)
+        traffic = entry["bytes_per_launch"] if entry else None
     line = {
         "metric": METRIC,
         "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

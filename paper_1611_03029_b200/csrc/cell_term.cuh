@@ -1,0 +1,132 @@
+// Sum-factorized cell term of the Laplace operator (eq:mf_eval),
+// shared by the CG (K1) and SIPG (K2) kernels.
+//
+// A cell is handled by (k+1)^2 threads; thread t = ta + N tb owns one 1-D line of
+// the cell per phase (z-line (x=ta,y=tb), y-line (x=ta,z=tb) or x-line (y=ta,z=tb)),
+// held in registers; direction changes are transposes through the cell's three
+// shared-memory buffers s0, s1, s2 (N^3 doubles each).
+//   in : u[] = the thread's z-line of nodal values (constrained entries already 0)
+//   out: v[] = the thread's z-line of the cell residual  sum_q grad phi . G_q grad u
+// The caller must __syncthreads() before reusing s0..s2.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace fem {
+
+template <int N>
+struct CellGeo {
+  const double* G;  // deformed: &G[cell][0][0] of layout [6][N^3]; nullptr => Cartesian
+  double c0, c1, c2;
+  bool active;
+};
+
+template <int N, bool DEFORMED>
+__device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& geo, double* s0,
+                                             double* s1, double* s2, int t, double (&u)[N],
+                                             double (&v)[N]) {
+  constexpr int N2 = N * N, N3 = N2 * N;
+  const int ta = t % N, tb = t / N;
+  double g[N], w[N];
+  // Z: interpolate in z
+  mv<N>(T.val, u, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[t + N2 * l] = v[l];
+  __syncthreads();
+  // Y: interpolate in y
+#pragma unroll
+  for (int l = 0; l < N; ++l) w[l] = s0[ta + N * l + N2 * tb];
+  mv<N>(T.val, w, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = v[l];
+  __syncthreads();
+  // X: interpolate in x, d/dxi_x by collocation
+#pragma unroll
+  for (int l = 0; l < N; ++l) w[l] = s0[l + N * ta + N2 * tb];
+  mv<N>(T.val, w, v);
+  mv<N>(T.colloc, v, g);
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    s0[l + N * ta + N2 * tb] = v[l];
+    s2[l + N * ta + N2 * tb] = g[l];
+  }
+  __syncthreads();
+  // Y: d/dxi_y
+#pragma unroll
+  for (int l = 0; l < N; ++l) w[l] = s0[ta + N * l + N2 * tb];
+  mv<N>(T.colloc, w, g);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s1[ta + N * l + N2 * tb] = g[l];
+  __syncthreads();
+  // Z: d/dxi_z, quadrature-point operation, transposed d/dxi_z
+#pragma unroll
+  for (int l = 0; l < N; ++l) w[l] = s0[t + N2 * l];
+  mv<N>(T.colloc, w, g);
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    const int q = t + N2 * l;
+    const double gxq = s2[q], gyq = s1[q], gzq = g[l];
+    double fx, fy, fz;
+    if (DEFORMED) {
+      double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
+      if (geo.active) {
+        const double* Gc = geo.G + q;
+        G00 = __ldg(Gc);
+        G01 = __ldg(Gc + N3);
+        G02 = __ldg(Gc + 2 * N3);
+        G11 = __ldg(Gc + 3 * N3);
+        G12 = __ldg(Gc + 4 * N3);
+        G22 = __ldg(Gc + 5 * N3);
+      }
+      fx = G00 * gxq + G01 * gyq + G02 * gzq;
+      fy = G01 * gxq + G11 * gyq + G12 * gzq;
+      fz = G02 * gxq + G12 * gyq + G22 * gzq;
+    } else {
+      const double w3 = T.w[ta] * T.w[tb] * T.w[l];
+      fx = geo.c0 * w3 * gxq;
+      fy = geo.c1 * w3 * gyq;
+      fz = geo.c2 * w3 * gzq;
+    }
+    s2[q] = fx;
+    s1[q] = fy;
+    v[l] = fz;
+  }
+  mvt<N>(T.colloc, v, w);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[t + N2 * l] = w[l];
+  __syncthreads();
+  // Y: += colloc^T f_y
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    v[l] = s1[ta + N * l + N2 * tb];
+    w[l] = s0[ta + N * l + N2 * tb];
+  }
+  mvt_add<N>(T.colloc, v, w);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = w[l];
+  __syncthreads();
+  // X: += colloc^T f_x, then interpolate back in x
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    v[l] = s2[l + N * ta + N2 * tb];
+    w[l] = s0[l + N * ta + N2 * tb];
+  }
+  mvt_add<N>(T.colloc, v, w);
+  mvt<N>(T.val, w, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[l + N * ta + N2 * tb] = v[l];
+  __syncthreads();
+  // Y: interpolate back in y
+#pragma unroll
+  for (int l = 0; l < N; ++l) w[l] = s0[ta + N * l + N2 * tb];
+  mvt<N>(T.val, w, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = v[l];
+  __syncthreads();
+  // Z: interpolate back in z
+#pragma unroll
+  for (int l = 0; l < N; ++l) w[l] = s0[t + N2 * l];
+  mvt<N>(T.val, w, v);
+}
+
+}  // namespace fem

@@ -14,6 +14,7 @@
 // bank); switching direction is a transpose through shared memory.
 #include <algorithm>
 
+#include "cell_term.cuh"
 #include "device_common.cuh"
 
 namespace fem {
@@ -46,8 +47,6 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
   const int64_t cell = (int64_t)blockIdx.x * C + ci;
   const bool active = cell < a.n_cells;
   double* s0 = smem + ci * 3 * N3;
-  double* s1 = s0 + N3;
-  double* s2 = s1 + N3;
   const int ta = t % N, tb = t / N;
   int cx = 0, cy = 0, cz = 0;
   if (active) {
@@ -56,9 +55,8 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     cy = (int)(r % a.n1);
     cz = (int)(r / a.n1);
   }
-  double u[N], v[N], g[N];
-
-  // ---- Z: gather the z-line (x=ta, y=tb) and interpolate in z
+  // gather the z-line (x=ta, y=tb); constrained entries read as 0 (reading R5)
+  double u[N], v[N];
   const int gx = K * cx + ta, gy = K * cy + tb;
   const int64_t zs = (int64_t)a.nn0 * a.nn1;
   const int64_t base = gx + (int64_t)a.nn0 * gy + zs * (int64_t)(K * cz);
@@ -67,104 +65,10 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     const bool m = cg_constrained(a.bcmask, gx, gy, K * cz + l, a.nn0, a.nn1, a.nn2);
     u[l] = (active && !m) ? __ldg(a.x + base + l * zs) : 0.0;
   }
-  mv<N>(T.val, u, v);
-#pragma unroll
-  for (int l = 0; l < N; ++l) s0[t + N2 * l] = v[l];
-  __syncthreads();
-  // ---- Y: y-line (x=ta, z=tb)
-#pragma unroll
-  for (int l = 0; l < N; ++l) u[l] = s0[ta + N * l + N2 * tb];
-  mv<N>(T.val, u, v);
-#pragma unroll
-  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = v[l];
-  __syncthreads();
-  // ---- X: x-line (y=ta, z=tb): interpolate, then d/dxi_x by collocation
-#pragma unroll
-  for (int l = 0; l < N; ++l) u[l] = s0[l + N * ta + N2 * tb];
-  mv<N>(T.val, u, v);
-  mv<N>(T.colloc, v, g);
-#pragma unroll
-  for (int l = 0; l < N; ++l) {
-    s0[l + N * ta + N2 * tb] = v[l];
-    s2[l + N * ta + N2 * tb] = g[l];
-  }
-  __syncthreads();
-  // ---- Y: d/dxi_y
-#pragma unroll
-  for (int l = 0; l < N; ++l) u[l] = s0[ta + N * l + N2 * tb];
-  mv<N>(T.colloc, u, g);
-#pragma unroll
-  for (int l = 0; l < N; ++l) s1[ta + N * l + N2 * tb] = g[l];
-  __syncthreads();
-  // ---- Z: d/dxi_z, quadrature-point operation, transposed d/dxi_z
-#pragma unroll
-  for (int l = 0; l < N; ++l) u[l] = s0[t + N2 * l];
-  mv<N>(T.colloc, u, g);  // g = d/dxi_z
-#pragma unroll
-  for (int l = 0; l < N; ++l) {
-    const int q = t + N2 * l;
-    const double gxq = s2[q], gyq = s1[q], gzq = g[l];
-    double fx, fy, fz;
-    if (DEFORMED) {
-      const double* Gc = a.G + (size_t)cell * 6 * N3 + q;
-      double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
-      if (active) {
-        G00 = __ldg(Gc);
-        G01 = __ldg(Gc + N3);
-        G02 = __ldg(Gc + 2 * N3);
-        G11 = __ldg(Gc + 3 * N3);
-        G12 = __ldg(Gc + 4 * N3);
-        G22 = __ldg(Gc + 5 * N3);
-      }
-      fx = G00 * gxq + G01 * gyq + G02 * gzq;
-      fy = G01 * gxq + G11 * gyq + G12 * gzq;
-      fz = G02 * gxq + G12 * gyq + G22 * gzq;
-    } else {
-      const double w3 = T.w[ta] * T.w[tb] * T.w[l];
-      fx = a.c0 * w3 * gxq;
-      fy = a.c1 * w3 * gyq;
-      fz = a.c2 * w3 * gzq;
-    }
-    s2[q] = fx;
-    s1[q] = fy;
-    v[l] = fz;
-  }
-  mvt<N>(T.colloc, v, u);
-#pragma unroll
-  for (int l = 0; l < N; ++l) s0[t + N2 * l] = u[l];
-  __syncthreads();
-  // ---- Y: += colloc^T f_y
-#pragma unroll
-  for (int l = 0; l < N; ++l) {
-    v[l] = s1[ta + N * l + N2 * tb];
-    u[l] = s0[ta + N * l + N2 * tb];
-  }
-  mvt_add<N>(T.colloc, v, u);
-#pragma unroll
-  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = u[l];
-  __syncthreads();
-  // ---- X: += colloc^T f_x, then interpolate back in x (val^T)
-#pragma unroll
-  for (int l = 0; l < N; ++l) {
-    v[l] = s2[l + N * ta + N2 * tb];
-    u[l] = s0[l + N * ta + N2 * tb];
-  }
-  mvt_add<N>(T.colloc, v, u);
-  mvt<N>(T.val, u, v);
-#pragma unroll
-  for (int l = 0; l < N; ++l) s0[l + N * ta + N2 * tb] = v[l];
-  __syncthreads();
-  // ---- Y: val^T
-#pragma unroll
-  for (int l = 0; l < N; ++l) u[l] = s0[ta + N * l + N2 * tb];
-  mvt<N>(T.val, u, v);
-#pragma unroll
-  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = v[l];
-  __syncthreads();
-  // ---- Z: val^T and scatter-add (constrained rows skipped; set afterwards)
-#pragma unroll
-  for (int l = 0; l < N; ++l) u[l] = s0[t + N2 * l];
-  mvt<N>(T.val, u, v);
+  const CellGeo<N> geo{DEFORMED ? a.G + (size_t)(active ? cell : 0) * 6 * N3 : nullptr, a.c0, a.c1,
+                       a.c2, active};
+  cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
+  // scatter-add (constrained rows skipped; they are set to x_c afterwards)
   if (active) {
 #pragma unroll
     for (int l = 0; l < N; ++l) {

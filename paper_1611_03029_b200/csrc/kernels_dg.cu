@@ -1,12 +1,624 @@
-// SIPG kernels (cell + face terms).  Placeholder until the element-centric kernel lands.
+// SIPG kernels (K2 cell + K3 face terms), element-centric.
+//
+// Operator (eq:poisson_dgsip; boundary mirror values eq:bc_dgsip,
+// P:L248-255): per cell K the cell term of cell_term.cuh plus, for each of its
+// six faces F with outward normal n_K and neighbour K' (same orientation on the
+// structured mesh),
+//     int_F  sigma [u] v - {d_n u} v - (1/2) [u] d_n v ,
+//     [u] = u_K - u_K',  {d_n u} = (d_n u_K + d_n u_K')/2,  d_n = n_K . grad,
+// which is the part of -[v]{d_n u} - {d_n v}[u] + sigma [u][v] that tests the
+// functions of K.  Dirichlet (g = 0): [u] = 2 u_K, {d_n u} = d_n u_K; Neumann: 0.
+// Every cell evaluates its own faces (each interior face is visited twice, as in
+// the paper's <.,.>_{dT_h}), reading the neighbour's nodal lines from global
+// memory, so the result of a cell is written exactly once (no atomics, no zeroing).
+//
+// Face terms are sum-factorized (O((k+1)^d) per face): with GLL nodes
+// the trace of u on xi_d = +-1 is the nodal layer, the normal derivative is a
+// reduction of each d-line with phi_i'(+-1); both are interpolated to the
+// (k+1)^2 face Gauss points by two 1-D sweeps (tangential derivatives by
+// collocation on deformed meshes), and the flux is integrated back with the
+// transposed sweeps and expanded along the d-lines.
+#include "cell_term.cuh"
 #include "device_common.cuh"
 
 namespace fem {
 
-void launch_dg_apply(fem_ctx*, const Level&, const double*, double*) {
-  throw Error{FEM_E_ARG, "SIPG operator not built yet"};
+template <int K>
+struct DgCPB {
+  static constexpr int N = K + 1;
+  static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? 8 : (N * N <= 49) ? 4 : 2;
+};
+
+template <int N>
+struct DgSmem {  // per-cell shared memory layout (doubles)
+  static constexpr int N2 = N * N, N3 = N2 * N;
+  static constexpr int X = 0, S0 = N3, FWD = 4 * N3, BWD = FWD + 16 * N2, SIZE = BWD + 8 * N2;
+};
+
+struct DgArgs {
+  const double* __restrict__ x;
+  double* __restrict__ y;
+  const double* __restrict__ G;       // deformed cell metric [cell][6][q]
+  const double* __restrict__ faceq;   // deformed face records [face][7][N2]
+  const double* __restrict__ fsigma;  // [face]
+  int64_t face_off[3];                // first face record of direction d
+  int n[3];
+  int64_t n_cells;
+  int bcmask;
+  double c[3];      // Cartesian metric det J (2/h_d)^2
+  double h[3];
+  double sigma[3];  // Cartesian penalty c (k+1)^2 / h_d
+};
+
+// node index in the cell of (i along D, a along t1, b along t2)
+template <int N, int D>
+__device__ __forceinline__ int lidx(int i, int a, int b) {
+  if (D == 0) return i + N * a + N * N * b;
+  if (D == 1) return a + N * i + N * N * b;
+  return a + N * b + N * N * i;
 }
-void launch_dg_diagonal(fem_ctx*, Level&) { throw Error{FEM_E_ARG, "SIPG operator not built yet"}; }
-void launch_dg_face_geometry(fem_ctx*, Level&) {}
+
+template <int D> struct Tang;
+template <> struct Tang<0> { static constexpr int t1 = 1, t2 = 2; };
+template <> struct Tang<1> { static constexpr int t1 = 0, t2 = 2; };
+template <> struct Tang<2> { static constexpr int t1 = 0, t2 = 1; };
+
+__device__ __forceinline__ int64_t face_record(const DgArgs& A, int D, const int c[3], int p) {
+  const int t1 = D == 0 ? 1 : 0, t2 = D == 2 ? 1 : 2;
+  return A.face_off[D] + p + (int64_t)(A.n[D] + 1) * (c[t1] + (int64_t)A.n[t1] * c[t2]);
+}
+
+// Face terms of the two faces normal to D, accumulated into the residual R (nodal, shared).
+template <int K, bool DEFORMED, int D>
+__device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, double* sm, int64_t cell,
+                                         const int c[3], bool active, int t) {
+  constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
+  constexpr int t1 = Tang<D>::t1, t2 = Tang<D>::t2;
+  using L = DgSmem<N>;
+  const double* X = sm + L::X;
+  double* R = sm + L::S0;
+  double* F = sm + L::FWD;   // [s][8][N2]: 0 u, 1 d_D u, 2 u', 3 d_D u', 4 d_t1 u, 5 d_t2 u, 6 d_t1 u', 7 d_t2 u'
+  double* B = sm + L::BWD;   // [s][4][N2]: 0 A (value test), 1 B_D, 2 B_t1, 3 B_t2
+  const int a = t % N, b = t / N;
+  const int64_t stride = D == 0 ? 1 : (D == 1 ? (int64_t)A.n[0] : (int64_t)A.n[0] * A.n[1]);
+  int kind[2];  // 0 interior, 1 Dirichlet, 2 Neumann
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int nb = c[D] + (s ? 1 : -1);
+    kind[s] = (nb >= 0 && nb < A.n[D]) ? 0 : ((A.bcmask >> (2 * D + s)) & 1 ? 1 : 2);
+  }
+  // ---- F1: traces of the own and neighbour d-lines
+  {
+    double xl[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) xl[i] = X[lidx<N, D>(i, a, b)];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      double f1 = 0.0, g0 = 0.0, g1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) f1 = fma(T.dface[s][i], xl[i], f1);
+      if (active && kind[s] == 0) {
+        const double* xn = A.x + (cell + (s ? stride : -stride)) * N3;
+        double nl[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) nl[i] = __ldg(xn + lidx<N, D>(i, a, b));
+        g0 = nl[s ? 0 : K];
+#pragma unroll
+        for (int i = 0; i < N; ++i) g1 = fma(T.dface[1 - s][i], nl[i], g1);
+      }
+      double* Fs = F + s * 8 * N2;
+      Fs[0 * N2 + t] = xl[s ? K : 0];
+      Fs[1 * N2 + t] = f1;
+      Fs[2 * N2 + t] = g0;
+      Fs[3 * N2 + t] = g1;
+    }
+  }
+  __syncthreads();
+  // ---- F2: interpolate along t1 (rows b); deformed: d/dt1 of the traces
+  for (int task = t; task < 2 * 4 * N; task += N2) {
+    const int s = task / (4 * N), f = (task / N) % 4, row = task % N;
+    double* fld = F + (s * 8 + f) * N2 + N * row;
+    double in[N], out[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) in[i] = fld[i];
+    mv<N>(T.val, in, out);
+    if (DEFORMED && (f == 0 || f == 2)) {
+      double dd[N];
+      mv<N>(T.colloc, out, dd);
+      double* fd = F + (s * 8 + (f == 0 ? 4 : 6)) * N2 + N * row;
+#pragma unroll
+      for (int i = 0; i < N; ++i) fd[i] = dd[i];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) fld[i] = out[i];
+  }
+  __syncthreads();
+  // ---- F3: interpolate along t2 (columns); deformed: d/dt2 of the traces
+  {
+    constexpr int NF = DEFORMED ? 6 : 4;
+    for (int task = t; task < 2 * NF * N; task += N2) {
+      const int s = task / (NF * N), fi = (task / N) % NF, col = task % N;
+      const int f = fi < 4 ? fi : (fi == 4 ? 4 : 6);
+      double* fld = F + (s * 8 + f) * N2 + col;
+      double in[N], out[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) in[i] = fld[N * i];
+      mv<N>(T.val, in, out);
+      if (DEFORMED && (f == 0 || f == 2)) {
+        double dd[N];
+        mv<N>(T.colloc, out, dd);
+        double* fd = F + (s * 8 + (f == 0 ? 5 : 7)) * N2 + col;
+#pragma unroll
+        for (int i = 0; i < N; ++i) fd[N * i] = dd[i];
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) fld[N * i] = out[i];
+    }
+  }
+  __syncthreads();
+  // ---- F4: numerical flux at face point q = (a, b)
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const double* Fs = F + s * 8 * N2;
+    double* Bs = B + s * 4 * N2;
+    double vA = 0.0, vD = 0.0, v1 = 0.0, v2 = 0.0;
+    if (kind[s] != 2 && active) {
+      const double nsgn = s ? 1.0 : -1.0;
+      const double u_own = Fs[t];
+      double dn_own, dn_nb = 0.0, JxW, sig, Jn[3];
+      if (DEFORMED) {
+        const int64_t fr = face_record(A, D, c, c[D] + s);
+        const double* rec = A.faceq + fr * 7 * N2;
+        JxW = __ldg(rec + t);
+        sig = __ldg(A.fsigma + fr);
+        const int own = s ? 1 : 4, oth = s ? 4 : 1;  // own cell is the minus side iff s == 1
+        double Jo[3];
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          Jn[e] = nsgn * __ldg(rec + (own + e) * N2 + t);
+          Jo[e] = nsgn * __ldg(rec + (oth + e) * N2 + t);
+        }
+        dn_own = Jn[t1] * Fs[4 * N2 + t] + Jn[t2] * Fs[5 * N2 + t] + Jn[D] * Fs[1 * N2 + t];
+        if (kind[s] == 0)
+          dn_nb = Jo[t1] * Fs[6 * N2 + t] + Jo[t2] * Fs[7 * N2 + t] + Jo[D] * Fs[3 * N2 + t];
+      } else {
+        const double jac = 2.0 / A.h[D];
+        JxW = T.w[a] * T.w[b] * (0.5 * A.h[t1]) * (0.5 * A.h[t2]);
+        sig = A.sigma[D];
+        Jn[0] = Jn[1] = Jn[2] = 0.0;
+        Jn[D] = nsgn * jac;
+        dn_own = Jn[D] * Fs[1 * N2 + t];
+        if (kind[s] == 0) dn_nb = Jn[D] * Fs[3 * N2 + t];
+      }
+      double jump, avg;
+      if (kind[s] == 0) {
+        jump = u_own - Fs[2 * N2 + t];
+        avg = 0.5 * (dn_own + dn_nb);
+      } else {
+        jump = 2.0 * u_own;
+        avg = dn_own;
+      }
+      const double cu = JxW * (sig * jump - avg);
+      const double cg = -0.5 * JxW * jump;
+      vA = cu;
+      vD = cg * Jn[D];
+      v1 = cg * Jn[t1];
+      v2 = cg * Jn[t2];
+    }
+    Bs[0 * N2 + t] = vA;
+    Bs[1 * N2 + t] = vD;
+    Bs[2 * N2 + t] = v1;
+    Bs[3 * N2 + t] = v2;
+  }
+  __syncthreads();
+  // ---- F5: transposed t2 (columns): P = I^T (A + D^T B_t2), Q = I^T B_t1, W = I^T B_D
+  {
+    constexpr int NG = DEFORMED ? 3 : 2;
+    for (int task = t; task < 2 * NG * N; task += N2) {
+      const int s = task / (NG * N), g = (task / N) % NG, col = task % N;
+      double* Bs = B + s * 4 * N2;
+      double in[N], out[N];
+      if (g == 0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) in[i] = Bs[N * i + col];
+        if (DEFORMED) {
+          double b2[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) b2[i] = Bs[3 * N2 + N * i + col];
+          mvt_add<N>(T.colloc, b2, in);
+        }
+      } else {
+        const int f = (g == 1) ? 1 : 2;
+#pragma unroll
+        for (int i = 0; i < N; ++i) in[i] = Bs[f * N2 + N * i + col];
+      }
+      mvt<N>(T.val, in, out);
+      const int f = (g == 0) ? 0 : (g == 1 ? 1 : 2);
+#pragma unroll
+      for (int i = 0; i < N; ++i) Bs[f * N2 + N * i + col] = out[i];
+    }
+  }
+  __syncthreads();
+  // ---- F6: transposed t1 (rows): V = I^T (P + D^T Q), W = I^T W
+  for (int task = t; task < 2 * 2 * N; task += N2) {
+    const int s = task / (2 * N), g = (task / N) % 2, row = task % N;
+    double* Bs = B + s * 4 * N2;
+    double in[N], out[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) in[i] = Bs[g * N2 + N * row + i];
+    if (DEFORMED && g == 0) {
+      double q[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) q[i] = Bs[2 * N2 + N * row + i];
+      mvt_add<N>(T.colloc, q, in);
+    }
+    mvt<N>(T.val, in, out);
+#pragma unroll
+    for (int i = 0; i < N; ++i) Bs[g * N2 + N * row + i] = out[i];
+  }
+  __syncthreads();
+  // ---- F7: expand into the residual's d-line (a, b)
+  {
+    double r[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) r[i] = R[lidx<N, D>(i, a, b)];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const double V = B[(s * 4 + 0) * N2 + t], W = B[(s * 4 + 1) * N2 + t];
+      r[s ? K : 0] += V;
+#pragma unroll
+      for (int i = 0; i < N; ++i) r[i] = fma(T.dface[s][i], W, r[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) R[lidx<N, D>(i, a, b)] = r[i];
+  }
+  __syncthreads();
+}
+
+template <int K, bool DEFORMED>
+__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
+    dg_apply_kernel(DgArgs A, Tab<K + 1> T) {
+  constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
+  constexpr int C = DgCPB<K>::value;
+  using L = DgSmem<N>;
+  extern __shared__ double smem[];
+  const int t = threadIdx.x, ci = threadIdx.y;
+  const int64_t cell = (int64_t)blockIdx.x * C + ci;
+  const bool active = cell < A.n_cells;
+  double* sm = smem + ci * L::SIZE;
+  int c[3] = {0, 0, 0};
+  if (active) {
+    c[0] = (int)(cell % A.n[0]);
+    const int64_t r = cell / A.n[0];
+    c[1] = (int)(r % A.n[1]);
+    c[2] = (int)(r / A.n[1]);
+  }
+  double u[N], v[N];
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    u[l] = active ? __ldg(A.x + cell * N3 + t + N2 * l) : 0.0;
+    sm[L::X + t + N2 * l] = u[l];
+  }
+  const CellGeo<N> geo{DEFORMED ? A.G + (size_t)(active ? cell : 0) * 6 * N3 : nullptr, A.c[0], A.c[1],
+                       A.c[2], active};
+  double* s0 = sm + L::S0;
+  cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
+  __syncthreads();
+#pragma unroll
+  for (int l = 0; l < N; ++l) s0[t + N2 * l] = v[l];   // residual R (z-line layout)
+  __syncthreads();
+  dg_faces<K, DEFORMED, 2>(A, T, sm, cell, c, active, t);
+  dg_faces<K, DEFORMED, 1>(A, T, sm, cell, c, active, t);
+  dg_faces<K, DEFORMED, 0>(A, T, sm, cell, c, active, t);
+  if (active) {
+    const int ta = t % N, tb = t / N;   // x-line (y=ta, z=tb): contiguous in the DG layout
+#pragma unroll
+    for (int l = 0; l < N; ++l) A.y[cell * N3 + l + N * ta + N2 * tb] = s0[l + N * ta + N2 * tb];
+  }
+}
+
+// ---------------------------------------------------------------- diagonal (R6)
+// cell part as for CG; face part on the face layer of every face:
+//   interior sum_q JxW (-phi d_n phi + sigma phi^2), Dirichlet sum_q JxW (-2 phi d_n phi + 2 sigma phi^2).
+template <int K, bool DEFORMED>
+__global__ void dg_diag_kernel(DgArgs A, Tab<K + 1> T) {
+  constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= A.n_cells * N3) return;
+  const int64_t cell = id / N3;
+  const int i = (int)(id % N3);
+  const int ii[3] = {i % N, (i / N) % N, i / N2};
+  int c[3];
+  c[0] = (int)(cell % A.n[0]);
+  const int64_t r = cell / A.n[0];
+  c[1] = (int)(r % A.n[1]);
+  c[2] = (int)(r / A.n[1]);
+  double d = 0.0;
+  for (int q2 = 0; q2 < N; ++q2)
+    for (int q1 = 0; q1 < N; ++q1)
+      for (int q0 = 0; q0 < N; ++q0) {
+        const double bx = T.der[q0][ii[0]] * T.val[q1][ii[1]] * T.val[q2][ii[2]];
+        const double by = T.val[q0][ii[0]] * T.der[q1][ii[1]] * T.val[q2][ii[2]];
+        const double bz = T.val[q0][ii[0]] * T.val[q1][ii[1]] * T.der[q2][ii[2]];
+        if (DEFORMED) {
+          const double* Gc = A.G + (size_t)cell * 6 * N3 + q0 + N * (q1 + N * q2);
+          d += Gc[0] * bx * bx + Gc[3 * N3] * by * by + Gc[5 * N3] * bz * bz +
+               2.0 * (Gc[N3] * bx * by + Gc[2 * N3] * bx * bz + Gc[4 * N3] * by * bz);
+        } else {
+          const double w3 = T.w[q0] * T.w[q1] * T.w[q2];
+          d += w3 * (A.c[0] * bx * bx + A.c[1] * by * by + A.c[2] * bz * bz);
+        }
+      }
+  for (int D = 0; D < 3; ++D) {
+    const int t1 = D == 0 ? 1 : 0, t2 = D == 2 ? 1 : 2;
+    for (int s = 0; s < 2; ++s) {
+      if (ii[D] != (s ? K : 0)) continue;
+      const int nb = c[D] + (s ? 1 : -1);
+      const int kind = (nb >= 0 && nb < A.n[D]) ? 0 : (((A.bcmask >> (2 * D + s)) & 1) ? 1 : 2);
+      if (kind == 2) continue;
+      const double nsgn = s ? 1.0 : -1.0;
+      const double m = kind == 0 ? 1.0 : 2.0;
+      double sig = A.sigma[D];
+      const double* rec = nullptr;
+      if (DEFORMED) {
+        const int64_t fr = face_record(A, D, c, c[D] + s);
+        rec = A.faceq + fr * 7 * N2;
+        sig = A.fsigma[fr];
+      }
+      const int own = s ? 1 : 4;
+      for (int qb = 0; qb < N; ++qb)
+        for (int qa = 0; qa < N; ++qa) {
+          const int q = qa + N * qb;
+          const double phi = T.val[qa][ii[t1]] * T.val[qb][ii[t2]];
+          double dn, JxW;
+          if (DEFORMED) {
+            JxW = rec[q];
+            double g[3];
+            g[D] = T.dface[s][ii[D]] * phi;
+            g[t1] = T.der[qa][ii[t1]] * T.val[qb][ii[t2]];
+            g[t2] = T.val[qa][ii[t1]] * T.der[qb][ii[t2]];
+            dn = nsgn * (rec[(own + 0) * N2 + q] * g[0] + rec[(own + 1) * N2 + q] * g[1] +
+                         rec[(own + 2) * N2 + q] * g[2]);
+          } else {
+            JxW = T.w[qa] * T.w[qb] * (0.5 * A.h[t1]) * (0.5 * A.h[t2]);
+            dn = nsgn * (2.0 / A.h[D]) * T.dface[s][ii[D]] * phi;
+          }
+          d += m * JxW * (-phi * dn + sig * phi * phi);
+        }
+    }
+  }
+  A.y[cell * N3 + i] = d;
+}
+
+// ---------------------------------------------------------------- face geometry (deformed)
+// Record of face p along D (between cells p-1 and p): nf = unit normal in the
+// direction of increasing xi_D (Nanson: J^-T e_D / |J^-T e_D|), JxW = w det J |J^-T e_D|,
+// Jm = J_minus^-1 nf, Jp = J_plus^-1 nf (0 for a missing side); both sides agree on
+// the physical point, normal and JxW because the map is continuous (reading R2).
+template <int K>
+__global__ void dg_face_geometry_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double* faceq) {
+  constexpr int N = K + 1, N2 = N * N;
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = A.face_off[2] + (int64_t)(A.n[2] + 1) * A.n[0] * A.n[1];
+  if (id >= total * N2) return;
+  const int64_t fr = id / N2;
+  const int q = (int)(id % N2), qa = q % N, qb = q / N;
+  const int D = fr >= A.face_off[2] ? 2 : (fr >= A.face_off[1] ? 1 : 0);
+  const int t1 = D == 0 ? 1 : 0, t2 = D == 2 ? 1 : 2;
+  const int64_t loc = fr - A.face_off[D];
+  const int p = (int)(loc % (A.n[D] + 1));
+  const int64_t rest = loc / (A.n[D] + 1);
+  int c[3];
+  c[t1] = (int)(rest % A.n[t1]);
+  c[t2] = (int)(rest / A.n[t1]);
+  double xi[3];
+  xi[t1] = T.qp[qa];
+  xi[t2] = T.qp[qb];
+  double* rec = faceq + fr * 7 * N2;
+  double nf[3] = {0, 0, 0};
+  bool have_n = false;
+  for (int side = 0; side < 2; ++side) {     // 0 minus (cell p-1, xi_D=+1), 1 plus (cell p, xi_D=-1)
+    const int cd = side == 0 ? p - 1 : p;
+    double* Jn = rec + (side == 0 ? 1 : 4) * N2 + q;
+    if (cd < 0 || cd >= A.n[D]) {
+      Jn[0] = Jn[N2] = Jn[2 * N2] = 0.0;
+      continue;
+    }
+    c[D] = cd;
+    xi[D] = side == 0 ? 1.0 : -1.0;
+    const PointGeo g = map_point(m, c[0], c[1], c[2], xi[0], xi[1], xi[2]);
+    if (!have_n) {
+      double v[3], nrm = 0.0;
+      for (int e = 0; e < 3; ++e) {
+        v[e] = jinv(m, g, D, e);   // (J^-T e_D)_e = (J^-1)_{D e}
+        nrm += v[e] * v[e];
+      }
+      nrm = sqrt(nrm);
+      for (int e = 0; e < 3; ++e) nf[e] = v[e] / nrm;
+      rec[q] = T.w[qa] * T.w[qb] * g.det * nrm;
+      have_n = true;
+    }
+    for (int a = 0; a < 3; ++a) {
+      double s = 0.0;
+      for (int e = 0; e < 3; ++e) s += jinv(m, g, a, e) * nf[e];
+      Jn[a * N2] = s;
+    }
+  }
+}
+
+template <int K>
+__global__ void dg_cell_volume_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double* vol) {
+  constexpr int N = K + 1;
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= A.n_cells) return;
+  const int cx = (int)(cell % A.n[0]);
+  const int64_t r = cell / A.n[0];
+  const int cy = (int)(r % A.n[1]), cz = (int)(r / A.n[1]);
+  double v = 0.0;
+  for (int q2 = 0; q2 < N; ++q2)
+    for (int q1 = 0; q1 < N; ++q1)
+      for (int q0 = 0; q0 < N; ++q0)
+        v += T.w[q0] * T.w[q1] * T.w[q2] * map_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]).det;
+  vol[cell] = v;
+}
+
+// sigma_F = c (k+1)^2 / h_F, 1/h_F = (|F|/|K-| + |F|/|K+|)/2 (interior), |F|/|K| (boundary).
+template <int K>
+__global__ void dg_face_sigma_kernel(DgArgs A, double pen, const double* faceq, const double* vol,
+                                     double* fsigma) {
+  constexpr int N = K + 1, N2 = N * N;
+  const int64_t fr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = A.face_off[2] + (int64_t)(A.n[2] + 1) * A.n[0] * A.n[1];
+  if (fr >= total) return;
+  const int D = fr >= A.face_off[2] ? 2 : (fr >= A.face_off[1] ? 1 : 0);
+  const int t1 = D == 0 ? 1 : 0, t2 = D == 2 ? 1 : 2;
+  const int64_t loc = fr - A.face_off[D];
+  const int p = (int)(loc % (A.n[D] + 1));
+  const int64_t rest = loc / (A.n[D] + 1);
+  int c[3];
+  c[t1] = (int)(rest % A.n[t1]);
+  c[t2] = (int)(rest / A.n[t1]);
+  double area = 0.0;
+  for (int q = 0; q < N2; ++q) area += faceq[fr * 7 * N2 + q];
+  double inv_h = 0.0;
+  int cnt = 0;
+  for (int side = 0; side < 2; ++side) {
+    c[D] = side == 0 ? p - 1 : p;
+    if (c[D] < 0 || c[D] >= A.n[D]) continue;
+    inv_h += area / vol[c[0] + (int64_t)A.n[0] * (c[1] + (int64_t)A.n[1] * c[2])];
+    ++cnt;
+  }
+  fsigma[fr] = pen * (K + 1) * (K + 1) * inv_h / cnt;
+}
+
+// ---------------------------------------------------------------- launchers
+namespace {
+
+DgArgs dg_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
+  DgArgs A;
+  A.x = x;
+  A.y = y;
+  A.G = L.G;
+  int64_t off = 0;
+  for (int d = 0; d < 3; ++d) {
+    A.n[d] = L.n[d];
+    A.h[d] = L.h[d];
+    A.c[d] = L.cart[d];
+    A.sigma[d] = h->opt.penalty_factor * (h->k + 1) * (h->k + 1) / L.h[d];
+  }
+  for (int d = 0; d < 3; ++d) {
+    A.face_off[d] = off;
+    const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
+    off += (int64_t)(L.n[d] + 1) * L.n[t1] * L.n[t2];
+  }
+  const int N2 = (h->k + 1) * (h->k + 1);
+  A.faceq = L.face;
+  A.fsigma = L.face ? L.face + off * 7 * N2 : nullptr;
+  A.n_cells = L.n_cells;
+  int mask = 0;
+  for (int s = 0; s < 6; ++s)
+    if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
+  A.bcmask = mask;
+  return A;
+}
+
+int64_t n_faces(const Level& L) {
+  int64_t off = 0;
+  for (int d = 0; d < 3; ++d) {
+    const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
+    off += (int64_t)(L.n[d] + 1) * L.n[t1] * L.n[t2];
+  }
+  return off;
+}
+
+MapArgs dg_map_args(const fem_ctx* h, const Level& L) {
+  MapArgs m;
+  for (int d = 0; d < 3; ++d) {
+    m.lo[d] = h->mesh.lo[d];
+    m.L[d] = h->mesh.hi[d] - h->mesh.lo[d];
+    m.h[d] = L.h[d];
+  }
+  m.eps = h->mesh.deform_eps;
+  m.cz0 = 0;
+  return m;
+}
+
+template <int K, bool DEF>
+void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y) {
+  constexpr int N = K + 1, C = DgCPB<K>::value;
+  const size_t sm = sizeof(double) * DgSmem<N>::SIZE * C;
+  static bool attr = false;
+  if (!attr) {
+    FEM_CUDA_TRY(cudaFuncSetAttribute(dg_apply_kernel<K, DEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sm));
+    attr = true;
+  }
+  const unsigned grid = (unsigned)((L.n_cells + C - 1) / C);
+  dg_apply_kernel<K, DEF><<<grid, dim3(N * N, C), sm, h->stream>>>(dg_args(h, L, x, y), make_tab<N>(h->tab));
+  count_launch();
+  check_launch("dg_apply_kernel");
+}
+
+template <int K>
+void dg_apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
+  if (L.cartesian) dg_apply_kd<K, false>(h, L, x, y);
+  else dg_apply_kd<K, true>(h, L, x, y);
+}
+
+template <int K>
+void dg_diag_k(fem_ctx* h, Level& L) {
+  constexpr int N = K + 1;
+  const int64_t tot = L.n_cells * N * N * N;
+  const unsigned grid = (unsigned)((tot + 255) / 256);
+  if (L.cartesian)
+    dg_diag_kernel<K, false><<<grid, 256, 0, h->stream>>>(dg_args(h, L, nullptr, L.diag), make_tab<N>(h->tab));
+  else
+    dg_diag_kernel<K, true><<<grid, 256, 0, h->stream>>>(dg_args(h, L, nullptr, L.diag), make_tab<N>(h->tab));
+  count_launch();
+  check_launch("dg_diag_kernel");
+}
+
+template <int K>
+void dg_face_geometry_k(fem_ctx* h, Level& L) {
+  constexpr int N = K + 1, N2 = N * N;
+  const int64_t nf = n_faces(L);
+  FEM_CUDA_TRY(cudaMalloc(&L.face, sizeof(double) * (nf * 7 * N2 + nf)));
+  double* vol = nullptr;
+  FEM_CUDA_TRY(cudaMalloc(&vol, sizeof(double) * L.n_cells));
+  const DgArgs A = dg_args(h, L, nullptr, nullptr);
+  const MapArgs m = dg_map_args(h, L);
+  const Tab<N> T = make_tab<N>(h->tab);
+  dg_face_geometry_kernel<K><<<(unsigned)((nf * N2 + 255) / 256), 256, 0, h->stream>>>(m, A, T, L.face);
+  dg_cell_volume_kernel<K><<<(unsigned)((L.n_cells + 255) / 256), 256, 0, h->stream>>>(m, A, T, vol);
+  dg_face_sigma_kernel<K><<<(unsigned)((nf + 255) / 256), 256, 0, h->stream>>>(
+      A, h->opt.penalty_factor, L.face, vol, L.face + nf * 7 * N2);
+  count_launch(3);
+  check_launch("dg_face_geometry");
+  FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  cudaFree(vol);
+}
+
+#define FEM_DISPATCH_K(k, fn, ...)                           \
+  switch (k) {                                               \
+    case 1: fn<1>(__VA_ARGS__); break;                       \
+    case 2: fn<2>(__VA_ARGS__); break;                       \
+    case 3: fn<3>(__VA_ARGS__); break;                       \
+    case 4: fn<4>(__VA_ARGS__); break;                       \
+    case 5: fn<5>(__VA_ARGS__); break;                       \
+    case 6: fn<6>(__VA_ARGS__); break;                       \
+    case 7: fn<7>(__VA_ARGS__); break;                       \
+    case 8: fn<8>(__VA_ARGS__); break;                       \
+    default: throw Error{FEM_E_ARG, "degree out of range"}; \
+  }
+
+}  // namespace
+
+void launch_dg_apply(fem_ctx* h, const Level& L, const double* x, double* y) {
+  FEM_DISPATCH_K(h->k, dg_apply_k, h, L, x, y);
+}
+
+void launch_dg_diagonal(fem_ctx* h, Level& L) { FEM_DISPATCH_K(h->k, dg_diag_k, h, L); }
+
+void launch_dg_face_geometry(fem_ctx* h, Level& L) { FEM_DISPATCH_K(h->k, dg_face_geometry_k, h, L); }
 
 }  // namespace fem

@@ -28,10 +28,14 @@ void launch_dg_face_geometry(fem_ctx* h, Level& L);
 namespace {
 thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
+thread_local int64_t* g_capture_count = nullptr;   // set while a graph is captured
 }  // namespace
 
 void set_error(const std::string& msg) { g_last_error = msg; }
-void count_launch(int n) { g_launches += n; }
+void count_launch(int n) {
+  if (g_capture_count) *g_capture_count += n;
+  else g_launches += n;
+}
 void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw Error{FEM_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
@@ -51,8 +55,19 @@ void dfree(double*& p) {
 }
 
 // ---------------------------------------------------------------- profiling
+cudaEvent_t new_event() {
+  cudaEvent_t e;
+  FEM_CUDA_TRY(cudaEventCreate(&e));
+  return e;
+}
+
 void prof_begin(fem_ctx* h, bool finest) {
   if (!h->prof.on || !finest) return;
+  if (h->prof.capturing) {
+    h->prof.cap->push_back({new_event(), new_event()});
+    FEM_CUDA_TRY(cudaEventRecord(h->prof.cap->back().first, h->stream));
+    return;
+  }
   if (h->prof.used + 2 > h->prof.ev.size()) {
     for (int i = 0; i < 64; ++i) {
       cudaEvent_t e;
@@ -65,6 +80,10 @@ void prof_begin(fem_ctx* h, bool finest) {
 
 void prof_end(fem_ctx* h, bool finest) {
   if (!h->prof.on || !finest) return;
+  if (h->prof.capturing) {
+    FEM_CUDA_TRY(cudaEventRecord(h->prof.cap->back().second, h->stream));
+    return;
+  }
   FEM_CUDA_TRY(cudaEventRecord(h->prof.ev[h->prof.used + 1], h->stream));
   h->prof.used += 2;
   h->prof.launches += 1;
@@ -81,11 +100,22 @@ void prof_collect(fem_ctx* h) {
   h->prof.used = 0;
 }
 
+// elapsed time of the event pairs of a graph that has completed (stream synchronised)
+void prof_graph(fem_ctx* h, const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& ev) {
+  if (!h->prof.on) return;
+  for (const auto& p : ev) {
+    float ms = 0;
+    FEM_CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+    h->prof.ms += ms;
+    h->prof.launches += 1;
+  }
+}
+
 // ---------------------------------------------------------------- operator
 // y = A x on level L.  y is overwritten.  CG: constrained rows y_c = x_c.
 void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool set_constrained = true) {
   const bool finest = (&L == &h->levels.back());
-  if (h->prof.on && finest && h->prof.used + 2 > 4096) prof_collect(h);
+  if (h->prof.on && finest && !h->prof.capturing && h->prof.used + 2 > 4096) prof_collect(h);
   if (is_cg(h)) {
     launch_zero(h, y, L.n_dofs);
     prof_begin(h, finest);
@@ -314,6 +344,69 @@ void setup_coarse(fem_ctx* h) {
   FEM_CUDA_TRY(cudaMemcpy(h->coarse_inv, inv.data(), sizeof(double) * nf * nf, cudaMemcpyHostToDevice));
 }
 
+// ---------------------------------------------------------------- CUDA graphs
+struct Captured {
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
+};
+
+template <typename F>
+Captured capture(fem_ctx* h, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& ev, F&& body) {
+  cudaStream_t user = h->stream;
+  Captured c;
+  h->stream = h->cap_stream;
+  h->prof.capturing = true;
+  h->prof.cap = &ev;
+  g_capture_count = &c.kernels;
+  auto restore = [&] {
+    h->stream = user;
+    h->prof.capturing = false;
+    h->prof.cap = nullptr;
+    g_capture_count = nullptr;
+  };
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    restore();
+    throw Error{FEM_E_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e)};
+  }
+  try {
+    body();
+  } catch (...) {
+    cudaStreamEndCapture(h->cap_stream, &g);
+    if (g) cudaGraphDestroy(g);
+    restore();
+    throw;
+  }
+  e = cudaStreamEndCapture(h->cap_stream, &g);
+  restore();
+  if (e != cudaSuccess) throw Error{FEM_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e)};
+  e = cudaGraphInstantiate(&c.exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) throw Error{FEM_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e)};
+  return c;
+}
+
+void launch_graph(fem_ctx* h, cudaGraphExec_t g, int64_t kernels) {
+  FEM_CUDA_TRY(cudaGraphLaunch(g, h->stream));
+  g_launches += kernels;
+}
+
+void drop_solve_graphs(fem_ctx* h) {
+  if (h->sg.g_pre) cudaGraphExecDestroy(h->sg.g_pre);
+  if (h->sg.g_upd) cudaGraphExecDestroy(h->sg.g_upd);
+  for (auto* v : {&h->sg.ev_pre, &h->sg.ev_upd}) {
+    for (auto& p : *v) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+    v->clear();
+  }
+  h->sg.g_pre = h->sg.g_upd = nullptr;
+  h->sg.b = nullptr;
+  h->sg.x = nullptr;
+}
+
 // ---------------------------------------------------------------- setup
 void build_levels(fem_ctx* h) {
   std::vector<std::array<int, 3>> ns;
@@ -482,6 +575,8 @@ void destroy(fem_ctx* h) {
   for (auto& s : h->stage) dfree(s);
   if (h->geom_err) cudaFree(h->geom_err);
   for (auto e : h->prof.ev) cudaEventDestroy(e);
+  drop_solve_graphs(h);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   delete h;
 }
 
@@ -544,6 +639,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (h->opt.device >= 0) FEM_CUDA_TRY(cudaSetDevice(h->opt.device));
     FEM_CUDA_TRY(cudaGetDevice(&h->device));
     h->stream = (cudaStream_t)h->opt.stream;
+    FEM_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     h->prof.on = h->opt.profile != 0;
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks);
@@ -790,6 +886,7 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     check_size(nx, L.n_dofs, "x");
     if (!(rtol > 0) || maxit < 0) throw Error{FEM_E_ARG, "rtol must be > 0 and maxit >= 0"};
     const int64_t n = L.n_dofs;
+    setup_coarse(h);
     const double* db = in_vec(h, b, nb, 0);
     bool st;
     double* dx = out_vec(h, x, nx, 1, true, &st);
@@ -800,7 +897,7 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
       L.pcg_z = dalloc(n);
     }
     double *r = L.pcg_r, *p = L.pcg_p, *q = L.pcg_q, *z = L.pcg_z;
-    // CG Dirichlet rows: identity, so x_c = b_c and r_c = 0 (the system decouples)
+    // CG Dirichlet rows are identity rows: x_c = b_c, r_c = 0 (the system decouples)
     if (is_cg(h)) launch_set_constrained(h, L, db, dx);
     apply_level(h, L, dx, q, true);
     launch_sub(h, r, db, q, n);
@@ -813,15 +910,36 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     int it = 0;
     if (!std::isfinite(rnorm)) throw Error{FEM_E_BREAKDOWN, "non-finite initial residual"};
     if (rnorm > rtol * bnorm) {
-      vcycle(h, fine, r, z);
-      launch_copy(h, p, z, n);
-      launch_dot(h, r, z, n, 0);
+      if (!h->sg.g_pre || h->sg.b != db || h->sg.x != dx) {
+        drop_solve_graphs(h);
+        Captured cp = capture(h, h->sg.ev_pre, [&] {
+          vcycle(h, fine, r, z);
+          launch_dot(h, r, z, n, 3);
+          launch_pcg_update_p(h, p, z, n);      // beta = s3/s0, p = z + beta p, s0 = s3
+        });
+        Captured cu = capture(h, h->sg.ev_upd, [&] {
+          apply_level(h, L, p, q, false);
+          launch_dot(h, p, q, n, 1);
+          launch_pcg_update_xr(h, dx, r, p, q, n);   // alpha = s0/s1, (r,r) -> s2
+          FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 4, cudaMemcpyDeviceToHost,
+                                       h->stream));
+        });
+        h->sg.g_pre = cp.exec;
+        h->sg.g_upd = cu.exec;
+        h->sg.k_pre = cp.kernels;
+        h->sg.k_upd = cu.kernels;
+        h->sg.b = db;
+        h->sg.x = dx;
+      }
+      // first iteration through the same graphs: p = 0 and s0 = 1 make p = z + 0
+      launch_zero(h, p, n);
+      launch_set_scalar(h, 0, 1.0);
       while (it < maxit) {
-        apply_level(h, L, p, q, false);
-        launch_dot(h, p, q, n, 1);
-        launch_pcg_update_xr(h, dx, r, p, q, n);
-        FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, h->stream));
+        launch_graph(h, h->sg.g_pre, h->sg.k_pre);
+        launch_graph(h, h->sg.g_upd, h->sg.k_upd);
         FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        prof_graph(h, h->sg.ev_pre);
+        prof_graph(h, h->sg.ev_upd);
         ++it;
         const double pq = h->hscal[1];
         rnorm = std::sqrt(h->hscal[2]);
@@ -829,9 +947,6 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
           throw Error{FEM_E_BREAKDOWN, "PCG breakdown at iteration " + std::to_string(it) +
                                            " (p^T A p = " + std::to_string(pq) + ")"};
         if (rnorm <= rtol * bnorm) break;
-        vcycle(h, fine, r, z);
-        launch_dot(h, r, z, n, 3);
-        launch_pcg_update_p(h, p, z, n);
       }
     }
     if (iters) *iters = it;

@@ -16,9 +16,10 @@ namespace fem {
 
 template <int N>
 struct CellGeo {
-  const double* G;  // deformed: &G[cell][0][0] of layout [6][N^3]; nullptr => Cartesian
+  const double* G;  // deformed: &G[cell][0][0] of layout [6][N^3] (global or shared)
   double c0, c1, c2;
   bool active;
+  uint64_t* bar;    // if set: mbarrier of a bulk copy that fills G, waited on before the q-point phase
 };
 
 template <int N, bool DEFORMED>
@@ -62,6 +63,7 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
 #pragma unroll
   for (int l = 0; l < N; ++l) w[l] = s0[t + N2 * l];
   mv<N>(T.colloc, w, g);
+  if (DEFORMED && geo.bar) mbar_wait(geo.bar, 0);
 #pragma unroll
   for (int l = 0; l < N; ++l) {
     const int q = t + N2 * l;
@@ -71,12 +73,12 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
       double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
       if (geo.active) {
         const double* Gc = geo.G + q;
-        G00 = __ldg(Gc);
-        G01 = __ldg(Gc + N3);
-        G02 = __ldg(Gc + 2 * N3);
-        G11 = __ldg(Gc + 3 * N3);
-        G12 = __ldg(Gc + 4 * N3);
-        G22 = __ldg(Gc + 5 * N3);
+        G00 = Gc[0];
+        G01 = Gc[N3];
+        G02 = Gc[2 * N3];
+        G11 = Gc[3 * N3];
+        G12 = Gc[4 * N3];
+        G22 = Gc[5 * N3];
       }
       fx = G00 * gxq + G01 * gyq + G02 * gzq;
       fy = G01 * gxq + G11 * gyq + G12 * gzq;

@@ -69,10 +69,24 @@ struct Level {
 
 struct Profile {
   bool on = false;
-  std::vector<cudaEvent_t> ev;   // pairs (start, stop)
+  std::vector<cudaEvent_t> ev;   // pairs (start, stop) recorded eagerly
   size_t used = 0;
   double ms = 0.0;
   int64_t launches = 0;
+  // while a graph is being captured, event pairs go here (owned by the graph)
+  bool capturing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap = nullptr;
+};
+
+// One PCG iteration as two CUDA graphs (P:L1144-1148 loop body):
+//   g_pre = V-cycle z = V(r), (r,z), p = z + beta p
+//   g_upd = q = A p, (p,q), x += alpha p, r -= alpha q, (r,r), scalars -> pinned host
+struct SolveGraphs {
+  cudaGraphExec_t g_pre = nullptr, g_upd = nullptr;
+  int64_t k_pre = 0, k_upd = 0;   // kernels per replay
+  const double* b = nullptr;
+  double* x = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pre, ev_upd;
 };
 
 }  // namespace fem
@@ -98,6 +112,8 @@ struct fem_ctx {
   int64_t stage_len = 0;
   unsigned long long* geom_err = nullptr;  // device: first cell with det J <= 0
   fem::Profile prof;
+  cudaStream_t cap_stream = nullptr;   // non-blocking stream used only for graph capture
+  fem::SolveGraphs sg;
 };
 
 namespace fem {
@@ -128,6 +144,7 @@ void launch_dot(fem_ctx* h, const double* a, const double* b, int64_t n, int slo
 void launch_pcg_update_xr(fem_ctx* h, double* x, double* r, const double* p, double* q, int64_t n);
 void launch_pcg_update_p(fem_ctx* h, double* p, const double* z, int64_t n);
 void launch_coarse_solve(fem_ctx* h, const double* b, double* x);
+void launch_set_scalar(fem_ctx* h, int idx, double v);
 void launch_axpby(fem_ctx* h, double* y, const double* x, double a, double b, int64_t n);
 void launch_sub(fem_ctx* h, double* r, const double* b, const double* ax, int64_t n);
 

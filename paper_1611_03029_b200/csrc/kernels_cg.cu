@@ -65,8 +65,25 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     const bool m = cg_constrained(a.bcmask, gx, gy, K * cz + l, a.nn0, a.nn1, a.nn2);
     u[l] = (active && !m) ? __ldg(a.x + base + l * zs) : 0.0;
   }
-  const CellGeo<N> geo{DEFORMED ? a.G + (size_t)(active ? cell : 0) * 6 * N3 : nullptr, a.c0, a.c1,
-                       a.c2, active};
+  // Deformed: one TMA bulk copy stages the block's G slice (C cells x 6 x N^3 doubles,
+  // contiguous) into shared memory; it lands while the gather and the first five
+  // sweep phases run, and the q-point phase reads G from shared memory.
+  const double* Gs = nullptr;
+  __shared__ alignas(8) uint64_t gbar;
+  if (DEFORMED) {
+    double* sG = smem + C * 3 * N3;
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    if (t == 0 && ci == 0) {
+      const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
+      const uint32_t bytes = (uint32_t)(nc * 6 * N3 * sizeof(double));
+      mbar_init(&gbar, 1);
+      mbar_arrive_expect_tx(&gbar, bytes);
+      bulk_g2s(sG, a.G + c0 * 6 * N3, bytes, &gbar);
+    }
+    __syncthreads();       // barrier initialisation visible to all threads
+    Gs = sG + ci * 6 * N3;
+  }
+  const CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, DEFORMED ? &gbar : nullptr};
   cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
   // scatter-add (constrained rows skipped; they are set to x_c afterwards)
   if (active) {
@@ -253,11 +270,19 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
   const Tab<N> T = make_tab<N>(h->tab);
   const dim3 block(N * N, C);
   const int64_t grid = (L.n_cells + C - 1) / C;
-  const size_t sm = sizeof(double) * 3 * N * N * N * C;
-  if (L.cartesian)
+  if (L.cartesian) {
+    const size_t sm = sizeof(double) * 3 * N * N * N * C;
     cg_apply_kernel<K, false><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
-  else
+  } else {
+    const size_t sm = sizeof(double) * 9 * N * N * N * C;   // 3 work buffers + 6 G components
+    static bool attr = false;
+    if (!attr) {
+      FEM_CUDA_TRY(cudaFuncSetAttribute(cg_apply_kernel<K, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      attr = true;
+    }
     cg_apply_kernel<K, true><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
+  }
   count_launch();
   check_launch("cg_apply_kernel");
 }

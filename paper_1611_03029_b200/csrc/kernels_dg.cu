@@ -300,7 +300,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     sm[L::X + t + N2 * l] = u[l];
   }
   const CellGeo<N> geo{DEFORMED ? A.G + (size_t)(active ? cell : 0) * 6 * N3 : nullptr, A.c[0], A.c[1],
-                       A.c[2], active};
+                       A.c[2], active, nullptr};
   double* s0 = sm + L::S0;
   cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
   __syncthreads();

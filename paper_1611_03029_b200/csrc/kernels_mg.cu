@@ -291,6 +291,8 @@ __global__ void pcg_update_p_kernel(double* __restrict__ p, const double* __rest
 
 __global__ void copy_scalar_kernel(double* scal, int dst, int src) { scal[dst] = scal[src]; }
 
+__global__ void set_scalar_kernel(double* scal, int idx, double v) { scal[idx] = v; }
+
 // x = A0^{-1} b on the free DoFs (dense inverse from the Cholesky factor); x = 0 elsewhere.
 __global__ void coarse_solve_kernel(const double* __restrict__ Ainv, const int* __restrict__ free_idx,
                                     int nf, const double* __restrict__ b, double* __restrict__ x,
@@ -461,6 +463,12 @@ void launch_pcg_update_p(fem_ctx* h, double* p, const double* z, int64_t n) {
   copy_scalar_kernel<<<1, 1, 0, h->stream>>>(h->scal, 0, 3);
   count_launch();
   check_launch("copy_scalar_kernel");
+}
+
+void launch_set_scalar(fem_ctx* h, int idx, double v) {
+  set_scalar_kernel<<<1, 1, 0, h->stream>>>(h->scal, idx, v);
+  count_launch();
+  check_launch("set_scalar_kernel");
 }
 
 void launch_coarse_solve(fem_ctx* h, const double* b, double* x) {

@@ -10,6 +10,7 @@
 #include <array>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -117,7 +118,9 @@ void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool se
   const bool finest = (&L == &h->levels.back());
   if (h->prof.on && finest && !h->prof.capturing && h->prof.used + 2 > 4096) prof_collect(h);
   if (is_cg(h)) {
-    launch_zero(h, y, L.n_dofs);
+    // the Cartesian fast path zeroes y itself, chunk by chunk (kernels_cg.cu)
+    const bool tiled = L.cartesian && !h->general_path;
+    if (!tiled) launch_zero(h, y, L.n_dofs);
     prof_begin(h, finest);
     launch_cg_apply(h, L, x, y);
     prof_end(h, finest);
@@ -641,6 +644,8 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     h->stream = (cudaStream_t)h->opt.stream;
     FEM_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     h->prof.on = h->opt.profile != 0;
+    if (const char* e = std::getenv("FEM_GENERAL_PATH")) h->general_path = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_CHUNK_LAYERS")) h->chunk_layers = std::atoi(e);
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks);
     h->scal = dalloc(16);

@@ -114,6 +114,8 @@ struct fem_ctx {
   fem::Profile prof;
   cudaStream_t cap_stream = nullptr;   // non-blocking stream used only for graph capture
   fem::SolveGraphs sg;
+  int chunk_layers = 0;                 // Cartesian CG apply: cell layers per z-chunk (FEM_CHUNK_LAYERS; 0 = one launch)
+  bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
 };
 
 namespace fem {

@@ -236,3 +236,19 @@ def test_c4_full_size_sampled_apply_and_exact_solution():
     assert ok and its <= 8
     err = (xs - xd)[~bm]
     assert (err.norm() / xd[~bm].norm()).item() < 1e-8
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 6, 8])
+def test_cartesian_fast_path_and_general_quadrature_path_agree(k, monkeypatch):
+    """The Kronecker (App. B) kernel and the quadrature kernel give the same operator."""
+    cells = (5, 3, 2) if k < 6 else (2, 2, 1)
+    x = fem_inputs.uniform_pm1(11, (k * cells[0] + 1) * (k * cells[1] + 1) * (k * cells[2] + 1))
+    F1, m = make(cells, k, 0.0, MIXED)
+    y1 = np.zeros_like(x)
+    F1.fem_apply(x, y1)
+    monkeypatch.setenv("FEM_GENERAL_PATH", "1")
+    F2, _ = make(cells, k, 0.0, MIXED)
+    y2 = np.zeros_like(x)
+    F2.fem_apply(x, y2)
+    yo = ocg.apply(m, x)
+    assert relmax(y1, yo) <= 1e-12 and relmax(y2, yo) <= 1e-12

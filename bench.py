@@ -12,8 +12,10 @@ stream (fem_options.profile) and reported against the HBM roofline.
 --impl reference times the CPU oracle (oracle/, the "reference" of this tier) on
 the host cores: warm-up runs one full oracle solve (iteration count), each timed
 step is one oracle PCG iteration; value = n_dofs / (t_iteration * iterations).
-Multi-GPU (torchrun): the slab-partitioned path is not built yet, so N > 1 runs
-N independent replicas (weak scaling, no data-path collective).
+Multi-GPU (torchrun, one process per GPU): the mesh is split into z-slabs, one
+C2-sized slab (32x32x32 cells) per GPU on the box [0,1]^2 x [0,N] (weak scaling);
+libfem exchanges ghost planes with NCCL send/recv and all-reduces the PCG dot
+products; value = global DoFs / max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -40,7 +42,7 @@ METRIC = "GMG-CG solve throughput (DoFs solved per second; ms_per_step = time to
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2")
@@ -79,47 +81,76 @@ def algorithmic_apply_bytes(w, n_dofs):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region:
+    NVML polled every 2 ms from a thread (the timed region is tens of ms), with
+    nvidia-smi as the fallback when NVML is unavailable."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
-    def __init__(self, index):
-        self.index, self.samples, self.proc = index, [], None
+    def __init__(self, local_index):
+        self.local, self.samples, self.max_mhz, self.stop_flag = local_index, [], None, False
+        self.nv = self.handle = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            try:
+                uuid = str(torch.cuda.get_device_properties(local_index).uuid)
+                self.handle = nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.handle = nv.nvmlDeviceGetHandleByIndex(local_index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM)
+            self.nv = nv
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        nv = self.nv
+        while not self.stop_flag:
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                self.samples.append((mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        self.samples.clear()
+        self.stop_flag = False
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-            t0 = time.time()
-            while not self.samples and time.time() - t0 < 3.0:   # sampler running before the load
-                time.sleep(0.02)
-            self.samples.clear()
-        except OSError:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.samples.append(parts)
+        else:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.local}", "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
 
     def stop(self):
-        if self.proc:
+        self.stop_flag = True
+        names = [n for n, _ in self.REASONS]
+        if self.nv is not None:
+            self.t.join(timeout=1)
+            sm = [m for m, _ in self.samples]
+            bits = [(n, getattr(self.nv, c, 0)) for n, c in self.REASONS]
+            reasons = sorted({n for _, rs in self.samples for n, b in bits if b and rs & b})
+            mx = self.max_mhz
+            src = "nvml (2 ms polling)"
+        else:
             self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            out = self.proc.communicate(timeout=5)[0]
+            rows = [[p.strip() for p in ln.split(",")] for ln in out.splitlines() if ln.count(",") == 5]
+            sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+            mx = max((float(r[1]) for r in rows if r[1].replace(".", "").isdigit()), default=None)
+            reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+            src = "nvidia-smi (20 ms)"
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(sm), "source": src}
 
 
 def cpu_threads():
@@ -206,12 +237,12 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
-def constrained_mask(w, n):
-    """Dirichlet-constrained CG nodes (input preparation only; index arithmetic)."""
+def constrained_mask(w, n, cells, first=0):
+    """Dirichlet-constrained CG nodes of the owned slice (input preparation only; index arithmetic)."""
     import torch
     k = w.degree
-    nn = [k * c + 1 for c in w.cells]
-    i = torch.arange(n, device="cuda")
+    nn = [k * c + 1 for c in cells]
+    i = torch.arange(first, first + n, device="cuda")
     g = [i % nn[0], (i // nn[0]) % nn[1], i // (nn[0] * nn[1])]
     m = torch.zeros(n, dtype=torch.bool, device="cuda")
     for d in range(3):
@@ -233,17 +264,27 @@ def run_ours(args, w):
     from paper_1611_03029_b200 import fem
 
     stream = torch.cuda.current_stream()
-    F = fem.Fem(w.cells, w.degree, w.method, deform_eps=w.deform_eps, bc=w.bc,
-                penalty_factor=w.penalty_factor, stream=stream, profile=True)
+    cells, hi, mp = w.cells, w.hi, {}
+    if world > 1:
+        # weak scaling: one C2-sized z-slab per GPU, the box stretched to [0,1]^2 x [0,N]
+        # so cells stay cubic; NCCL halo exchange + all-reduced dots
+        import torch.distributed as dist
+        cells = (w.cells[0], w.cells[1], w.cells[2] * world)
+        hi = (w.hi[0], w.hi[1], w.hi[2] * world)
+        obj = [fem.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        mp = dict(rank=rank, nranks=world, nccl_id=obj[0])
+    F = fem.Fem(cells, w.degree, w.method, deform_eps=w.deform_eps, bc=w.bc, hi=hi,
+                penalty_factor=w.penalty_factor, stream=stream, profile=True, **mp)
     n = F.n_local
     b = torch.zeros(n, dtype=torch.float64, device="cuda")
     if w.rhs == "manufactured":
         F.fem_rhs(b)
     else:
-        xs = torch.from_numpy(fem_inputs.uniform_pm1(w.seed, n)).cuda()
+        xs = torch.from_numpy(fem_inputs.uniform_pm1(w.seed, n, F.first_global)).cuda()
         F.fem_apply(xs, b)
         del xs
-        b[constrained_mask(w, n)] = 0.0     # reading R15: b = A x_seed with Dirichlet rows zeroed
+        b[constrained_mask(w, n, cells, F.first_global)] = 0.0     # reading R15: b = A x_seed with Dirichlet rows zeroed
     x = torch.zeros_like(b)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > L2
 
@@ -253,7 +294,6 @@ def run_ours(args, w):
             dist.barrier()
 
     clocks = ClockSampler(local)
-    clocks.start()                                   # runs through warm-up and the timed region
     its = 0
     for _ in range(args.warmup):
         x.zero_()
@@ -265,6 +305,7 @@ def run_ours(args, w):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
+    clocks.start()
     for i in range(args.steps):
         flush.fill_(float(i))                       # evict L2 between steps (not timed)
         x.zero_()
@@ -284,7 +325,7 @@ def run_ours(args, w):
         tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = tt.item()
-    value = world * n * args.steps / (t_ms * 1e-3)
+    value = F.n_global * args.steps / (t_ms * 1e-3)
 
     # end to end through the C ABI with host buffers (copies inside the timed region)
     bh = b.cpu().pin_memory()
@@ -299,7 +340,13 @@ def run_ours(args, w):
         t0 = time.perf_counter()
         F.cg_solve(bh, xh, rtol=args.rtol)
         e2e_t.append(time.perf_counter() - t0)
-    e2e_value = world * n / (sum(e2e_t) / len(e2e_t))
+    e2e_s = sum(e2e_t) / len(e2e_t)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = tt.item()
+    e2e_value = F.n_global / e2e_s
 
     hbm, hbm_src = peaks()
     bytes_per_launch = algorithmic_apply_bytes(w, n)
@@ -318,7 +365,9 @@ def run_ours(args, w):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(w), "n_dofs": n, "rtol": args.rtol, "iterations": its,
                    "l2": "flushed between steps (256 MiB write, outside the per-step events)",
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "n_dofs_global": F.n_global, "cells": list(cells), "box_hi": list(hi),
+                   "parallelism": "single GPU" if world == 1 else
+                   f"{world} z-slabs (NCCL halo exchange + all-reduce), one C2-sized slab per GPU",
                    "step_ms": [round(s, 4) for s in step_ms]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,

@@ -76,8 +76,12 @@ typedef struct {
   double lo[3], hi[3];   /* box corners                                               */
   double deform_eps;     /* deformation amplitude; 0 => Cartesian fast path           */
   int32_t bc[6];         /* fem_bc of the sides -x,+x,-y,+y,-z,+z                      */
-  int32_t rank, nranks;  /* z-slab partition (nranks = 1: single GPU)                  */
-  const void* nccl_id;   /* host pointer to a 128-byte ncclUniqueId; NULL iff nranks==1 */
+  int32_t rank, nranks;  /* z-slab partition (nranks = 1: single GPU); n[2] % nranks == 0 */
+  const void* nccl_id;   /* host pointer to a 128-byte ncclUniqueId (fem_nccl_unique_id on
+                            one rank, broadcast by the caller), or NULL                     */
+  void* local_group;     /* fem_local_group_create() handle: the nranks ranks are threads of
+                            ONE process sharing one device (test transport), or NULL.
+                            nranks > 1 needs exactly one of nccl_id / local_group.        */
 } fem_mesh;
 
 /* Solver knobs; pass NULL to fem_setup for the defaults in brackets. */
@@ -92,6 +96,9 @@ typedef struct {
   void* stream;                   /* cudaStream_t; NULL => legacy default stream  */
   int32_t device;                 /* CUDA device ordinal; -1 => current device    */
   int32_t profile;                /* 1 => time the operator kernels with events   */
+  int32_t slab_min_layers;        /* multi-rank: a level is split into z-slabs while
+                                     every rank keeps >= this many cell layers;
+                                     coarser levels are replicated on every rank [2] */
 } fem_options;
 
 /* Fills *opt with the defaults above.  Returns FEM_OK or FEM_E_ARG (opt NULL). */
@@ -106,6 +113,51 @@ FEM_API int fem_default_options(fem_options* opt);
  * on success. */
 FEM_API int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_options* opt,
               fem_handle* out);
+
+/* ---- multi-rank z-slab partition ----
+ * Rank r of P owns the cell layers c_z in [r n_z/P, (r+1) n_z/P) of every
+ * distributed level.  CG: it owns the node planes [k z0, k z1) (the last rank also
+ * the top plane k n_z) and keeps the plane k z1 of rank r+1 as a ghost (imported
+ * before every operator apply, its contributions compress-added back after it).
+ * SIPG: it owns its cells' blocks and keeps one ghost cell layer from each
+ * neighbour rank.  PCG dot products are all-reduced.  Levels coarser than the
+ * last one that still gives every rank slab_min_layers layers are replicated: the
+ * residual of the last distributed level is gathered (all-reduce of zero-padded
+ * owned slices) and the coarse levels run redundantly on every rank.
+ * fem_partition is pure host arithmetic (no device needed): it describes, level by
+ * level (0 = coarsest), what fem_setup will build for `mesh->rank`. */
+typedef struct {
+  int32_t cells[3];          /* rank-local cells per direction                          */
+  int32_t global_cells[3];   /* cells per direction of the whole level                  */
+  int32_t cell_z0;           /* global index of the first local cell layer              */
+  int32_t distributed;       /* 1: z-slab of this rank; 0: replicated on every rank     */
+  int64_t n_owned;           /* owned DoFs = length of the rank-local vectors           */
+  int64_t first_global;      /* global index of the first owned DoF                     */
+  int64_t n_global;          /* DoFs of the whole level                                 */
+  int64_t n_stored;          /* owned + ghost DoFs the rank keeps                       */
+  int32_t ghost_lo, ghost_hi;/* neighbour ranks whose data is imported (-1: none)       */
+} fem_level_part;
+
+/* Fills out[0 .. *n_levels) (coarsest first) for mesh->rank; max_levels bounds out.
+ * opt may be NULL (defaults).  The finest level is always distributed and the
+ * coarsest always replicated when nranks > 1.  Errors: FEM_E_ARG (bad
+ * degree/method/mesh, n[2] not divisible by nranks, a multi-rank mesh that does
+ * not coarsen at least once, max_levels too small). */
+FEM_API int fem_partition(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_options* opt,
+                  fem_level_part* out, int32_t max_levels, int32_t* n_levels);
+
+/* Writes a fresh 128-byte ncclUniqueId into id (host memory, len >= 128); call on
+ * one rank and broadcast.  NCCL is loaded at run time (libnccl.so.2; the copy the
+ * process already has, e.g. torch's, is reused).  Errors: FEM_E_NCCL. */
+FEM_API int fem_nccl_unique_id(void* id, int64_t len);
+
+/* In-process transport for nranks threads sharing one device (tests, and to run
+ * the multi-rank path on a single GPU).  Each thread calls the collective entry
+ * points of its own handle; exchanges are device-to-device copies ordered by
+ * events between the ranks' streams (no kernel waits on another).  Destroy after
+ * every handle using it.  Errors: FEM_E_ARG. */
+FEM_API int fem_local_group_create(int32_t nranks, void** group);
+FEM_API void fem_local_group_destroy(void* group);
 
 /* Sizes: rank-local and global DoF counts of the finest level, first global
  * index owned, number of levels.  Any output pointer may be NULL. */
@@ -136,7 +188,8 @@ FEM_API int fem_rhs(fem_handle h, double* b, int64_t nb);
 
 /* ---- level-wise entry points (one per §8a row, used by the parity tests) ----
  * level in [0, n_levels): 0 = coarsest, n_levels-1 = finest.  Lengths are the
- * level's local DoF count (fem_level_info). */
+ * level's rank-local (owned) DoF count (fem_level_info); on multi-rank handles
+ * every call is collective. */
 FEM_API int fem_level_info(fem_handle h, int32_t level, int64_t* n_dofs, int32_t cells[3]);
 FEM_API int fem_level_apply(fem_handle h, int32_t level, const double* x, int64_t nx, double* y,
                     int64_t ny);

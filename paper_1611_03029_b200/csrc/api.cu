@@ -55,6 +55,18 @@ void dfree(double*& p) {
   p = nullptr;
 }
 
+// level vectors: owned block plus ghosts, pointer at the owned block (internal.h)
+double* valloc(const Level& L) {
+  double* p = dalloc(L.n_store);
+  FEM_CUDA_TRY(cudaMemset(p, 0, sizeof(double) * L.n_store));
+  return p + L.own_off;
+}
+
+void vfree(const Level& L, double*& p) {
+  if (p) cudaFree(p - L.own_off);
+  p = nullptr;
+}
+
 // ---------------------------------------------------------------- profiling
 cudaEvent_t new_event() {
   cudaEvent_t e;
@@ -65,8 +77,10 @@ cudaEvent_t new_event() {
 void prof_begin(fem_ctx* h, bool finest) {
   if (!h->prof.on || !finest) return;
   if (h->prof.capturing) {
+    // external record nodes: the events are really recorded on every replay, so
+    // cudaEventElapsedTime works on them after the graph has run
     h->prof.cap->push_back({new_event(), new_event()});
-    FEM_CUDA_TRY(cudaEventRecord(h->prof.cap->back().first, h->stream));
+    FEM_CUDA_TRY(cudaEventRecordWithFlags(h->prof.cap->back().first, h->stream, cudaEventRecordExternal));
     return;
   }
   if (h->prof.used + 2 > h->prof.ev.size()) {
@@ -82,7 +96,7 @@ void prof_begin(fem_ctx* h, bool finest) {
 void prof_end(fem_ctx* h, bool finest) {
   if (!h->prof.on || !finest) return;
   if (h->prof.capturing) {
-    FEM_CUDA_TRY(cudaEventRecord(h->prof.cap->back().second, h->stream));
+    FEM_CUDA_TRY(cudaEventRecordWithFlags(h->prof.cap->back().second, h->stream, cudaEventRecordExternal));
     return;
   }
   FEM_CUDA_TRY(cudaEventRecord(h->prof.ev[h->prof.used + 1], h->stream));
@@ -112,24 +126,111 @@ void prof_graph(fem_ctx* h, const std::vector<std::pair<cudaEvent_t, cudaEvent_t
   }
 }
 
+// ---------------------------------------------------------------- z-slab exchanges
+// Message tags (they only matter to the in-process transport; NCCL pairs the
+// single message per direction and neighbour pair by issue order).
+enum { kTagCgImport = 1, kTagCgExport = 2, kTagDgToUpper = 3, kTagDgToLower = 4 };
+
+}  // namespace
+
+void halo_import(fem_ctx* h, const Level& L, double* v) {
+  if (!L.dist || !h->comm) return;
+  std::vector<Comm::Msg> snd, rcv;
+  if (is_cg(h)) {
+    // ghost plane k n[2] <- plane 0 of the rank above
+    const int64_t plane = (int64_t)L.nn[0] * L.nn[1];
+    if (L.ghost_lo >= 0) snd.push_back({L.ghost_lo, kTagCgImport, v, plane});
+    if (L.ghost_hi >= 0) rcv.push_back({L.ghost_hi, kTagCgImport, v + (int64_t)h->k * L.n[2] * plane, plane});
+  } else {
+    const int64_t layer = (int64_t)L.n[0] * L.n[1] * (h->k + 1) * (h->k + 1) * (h->k + 1);
+    if (L.ghost_lo >= 0) {
+      snd.push_back({L.ghost_lo, kTagDgToUpper, v, layer});              // my bottom layer -> its top ghost
+      rcv.push_back({L.ghost_lo, kTagDgToLower, v - layer, layer});      // its top layer -> my bottom ghost
+    }
+    if (L.ghost_hi >= 0) {
+      snd.push_back({L.ghost_hi, kTagDgToLower, v + L.n_dofs - layer, layer});
+      rcv.push_back({L.ghost_hi, kTagDgToUpper, v + L.n_dofs, layer});
+    }
+  }
+  h->comm->exchange(snd, rcv, h->stream);
+}
+
+void halo_export_add(fem_ctx* h, const Level& L, double* v) {
+  if (!L.dist || !h->comm || !is_cg(h)) return;
+  const int64_t plane = (int64_t)L.nn[0] * L.nn[1];
+  std::vector<Comm::Msg> snd, rcv;
+  if (L.ghost_hi >= 0) snd.push_back({L.ghost_hi, kTagCgExport, v + (int64_t)h->k * L.n[2] * plane, plane});
+  if (L.ghost_lo >= 0) rcv.push_back({L.ghost_lo, kTagCgExport, L.halo, plane});
+  h->comm->exchange(snd, rcv, h->stream);
+  if (L.ghost_lo >= 0) launch_add(h, v, L.halo, plane);
+}
+
+void allreduce(fem_ctx* h, double* p, int64_t n) {
+  if (h->comm) h->comm->allreduce_sum(p, n, h->stream);
+}
+
+namespace {
+
+// dot product of owned entries into h->scal[slot], summed over ranks on distributed levels
+void dot(fem_ctx* h, const Level& L, const double* a, const double* b, int slot) {
+  launch_dot(h, a, b, L.n_dofs, slot);
+  if (L.dist) allreduce(h, h->scal + slot, 1);
+}
+
 // ---------------------------------------------------------------- operator
 // y = A x on level L.  y is overwritten.  CG: constrained rows y_c = x_c.
+// On a distributed level x must be a level (ghost-carrying) vector: its ghosts are
+// refreshed here; y's ghost plane is compress-added into the owner (CG).
 void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool set_constrained = true) {
   const bool finest = (&L == &h->levels.back());
   if (h->prof.on && finest && !h->prof.capturing && h->prof.used + 2 > 4096) prof_collect(h);
+  halo_import(h, L, const_cast<double*>(x));
   if (is_cg(h)) {
     // the Cartesian fast path zeroes y itself, chunk by chunk (kernels_cg.cu)
     const bool tiled = L.cartesian && !h->general_path;
-    if (!tiled) launch_zero(h, y, L.n_dofs);
+    if (!tiled) launch_zero(h, y, L.n_store);
     prof_begin(h, finest);
     launch_cg_apply(h, L, x, y);
     prof_end(h, finest);
+    halo_export_add(h, L, y);
     if (set_constrained) launch_set_constrained(h, L, x, y);
   } else {
     prof_begin(h, finest);
     launch_dg_apply(h, L, x, y);
     prof_end(h, finest);
   }
+}
+
+// ---------------------------------------------------------------- level transfer
+// xc = P^T (bf - axf) from level l to l-1 (axf may be null).  Distributed fine and
+// replicated coarse level: the fine residual is gathered (all-reduce of the
+// zero-padded owned slices) and restricted on the whole-level twin.
+void restrict_to(fem_ctx* h, int l, const double* bf, const double* axf, double* xc) {
+  Level& F = h->levels[l];
+  Level& C = h->levels[l - 1];
+  if (F.dist && !C.dist) {
+    launch_zero(h, F.gb, F.n_global);
+    launch_sub(h, F.gb + F.first_global, bf, axf, F.n_dofs);
+    allreduce(h, F.gb, F.n_global);
+    launch_restrict(h, C, *F.full, F.gb, nullptr, xc);
+    return;
+  }
+  launch_restrict(h, C, F, bf, axf, xc);
+  halo_export_add(h, C, xc);
+}
+
+// xf += P xc from level l-1 to l.  xc must be a level vector of l-1 (ghosts refreshed).
+void prolongate_from(fem_ctx* h, int l, double* xc, double* xf) {
+  Level& F = h->levels[l];
+  Level& C = h->levels[l - 1];
+  if (F.dist && !C.dist) {
+    launch_zero(h, F.gx, F.n_global);
+    launch_prolongate_add(h, C, *F.full, xc, F.gx);
+    launch_add(h, xf, F.gx + F.first_global, F.n_dofs);
+    return;
+  }
+  if (is_cg(h)) halo_import(h, C, xc);
+  launch_prolongate_add(h, C, F, xc, xf);
 }
 
 // ---------------------------------------------------------------- Chebyshev
@@ -201,9 +302,9 @@ void vcycle(fem_ctx* h, int l, const double* b, double* x_out) {
   chebyshev(h, L, b, nullptr, xs, L.x3, L.b2, wa);
   // residual, restriction: C.b = P^T (b - A xs)
   apply_level(h, L, xs, L.t, false);
-  launch_restrict(h, C, L, b, L.t, C.b);
+  restrict_to(h, l, b, L.t, C.b);
   vcycle(h, l - 1, C.b, C.x);
-  launch_prolongate_add(h, C, L, C.x, xs);
+  prolongate_from(h, l, C.x, xs);
   chebyshev(h, L, b, xs, x_out, L.x3, L.b2, wa);
 }
 
@@ -243,14 +344,14 @@ double estimate_lambda(fem_ctx* h, Level& L) {
   launch_copy(h, r, s, L.n_dofs);
   launch_cheb_step(h, L, z, nullptr, nullptr, r, nullptr, 0.0, 1.0, false);  // z = D^-1 r
   launch_copy(h, p, z, L.n_dofs);
-  launch_dot(h, r, z, L.n_dofs, 4);
+  dot(h, L, r, z, 4);
   FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal + 4, h->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
   double rz = h->hscal[4];
   std::vector<double> alpha, beta;
   for (int it = 0; it < h->opt.eig_iters; ++it) {
     apply_level(h, L, p, q, false);
-    launch_dot(h, p, q, L.n_dofs, 5);
+    dot(h, L, p, q, 5);
     FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal + 5, h->scal + 5, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
     const double pq = h->hscal[5];
@@ -258,7 +359,7 @@ double estimate_lambda(fem_ctx* h, Level& L) {
     const double a = rz / pq;
     launch_axpby(h, r, q, -a, 1.0, L.n_dofs);                                   // r -= a q
     launch_cheb_step(h, L, z, nullptr, nullptr, r, nullptr, 0.0, 1.0, false);  // z = D^-1 r
-    launch_dot(h, r, z, L.n_dofs, 4);
+    dot(h, L, r, z, 4);
     FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal + 4, h->scal + 4, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
     const double rz_new = h->hscal[4];
@@ -275,7 +376,18 @@ double estimate_lambda(fem_ctx* h, Level& L) {
     d[j] = 1.0 / alpha[j] + (j > 0 ? beta[j - 1] / alpha[j - 1] : 0.0);
     if (j + 1 < m) e[j] = std::sqrt(beta[j]) / alpha[j];
   }
-  return tridiag_max_eig(d, e);
+  double lam = tridiag_max_eig(d, e);
+  if (h->comm && !L.dist) {
+    // replicated level: every rank ran the same iteration up to rounding (atomics);
+    // agree on one value so that all ranks smooth with the same polynomial
+    h->hscal[7] = lam;
+    FEM_CUDA_TRY(cudaMemcpyAsync(h->scal + 7, h->hscal + 7, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    allreduce(h, h->scal + 7, 1);
+    FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal + 7, h->scal + 7, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    lam = h->hscal[7] / h->nranks;
+  }
+  return lam;
 }
 
 // ---------------------------------------------------------------- coarse solve
@@ -411,41 +523,114 @@ void drop_solve_graphs(fem_ctx* h) {
 }
 
 // ---------------------------------------------------------------- setup
-void build_levels(fem_ctx* h) {
+// Level hierarchy and z-slab partition (include/fem.h fem_partition): halve while
+// every n_d is even and max n_d > coarse_cells; a level is distributed while
+// n_z % P == 0 and every rank keeps >= slab_min_layers layers (the finest level
+// always is, for P > 1), coarser levels are replicated.
+std::vector<fem_level_part> partition(const fem_mesh& m, int k, int method, const fem_options& o) {
+  const int P = m.nranks, r = m.rank;
+  if (P < 1 || r < 0 || r >= P) throw Error{FEM_E_ARG, "rank must be in [0, nranks)"};
+  if (m.n[2] % P != 0) throw Error{FEM_E_ARG, "n[2] must be divisible by nranks (z-slabs)"};
   std::vector<std::array<int, 3>> ns;
-  std::array<int, 3> n = {h->mesh.n[0], h->mesh.n[1], h->mesh.n[2]};
+  std::array<int, 3> n = {m.n[0], m.n[1], m.n[2]};
   ns.push_back(n);
-  while (n[0] % 2 == 0 && n[1] % 2 == 0 && n[2] % 2 == 0 &&
-         std::max(n[0], std::max(n[1], n[2])) > h->opt.coarse_cells) {
+  while (n[0] % 2 == 0 && n[1] % 2 == 0 && n[2] % 2 == 0 && std::max(n[0], std::max(n[1], n[2])) > o.coarse_cells) {
     n = {n[0] / 2, n[1] / 2, n[2] / 2};
     ns.push_back(n);
   }
   const int nl = (int)ns.size();
+  if (P > 1 && nl < 2)
+    throw Error{FEM_E_ARG, "multi-rank needs a mesh that coarsens at least once (the coarsest level is "
+                           "replicated on every rank)"};
+  std::vector<fem_level_part> out(nl);
+  const int64_t N3 = (int64_t)(k + 1) * (k + 1) * (k + 1);
+  bool dist = P > 1;
+  for (int i = 0; i < nl; ++i) {            // i = 0: finest
+    const auto& c = ns[i];
+    fem_level_part& q = out[nl - 1 - i];
+    if (i > 0) dist = dist && c[2] % P == 0 && c[2] / P >= std::max(1, o.slab_min_layers) && i < nl - 1;
+    const int nzl = dist ? c[2] / P : c[2];
+    const int cz0 = dist ? r * nzl : 0;
+    for (int d = 0; d < 3; ++d) {
+      q.cells[d] = d == 2 ? nzl : c[d];
+      q.global_cells[d] = c[d];
+    }
+    q.cell_z0 = cz0;
+    q.distributed = dist ? 1 : 0;
+    q.ghost_lo = dist && r > 0 ? r - 1 : -1;
+    q.ghost_hi = dist && r < P - 1 ? r + 1 : -1;
+    if (method == FEM_CG) {
+      const int64_t plane = (int64_t)(k * c[0] + 1) * (k * c[1] + 1);
+      q.n_global = plane * (k * c[2] + 1);
+      const int64_t own_planes = (int64_t)k * nzl + ((!dist || r == P - 1) ? 1 : 0);
+      q.n_owned = own_planes * plane;
+      q.first_global = (int64_t)k * cz0 * plane;
+      q.n_stored = ((int64_t)k * nzl + 1) * plane;
+    } else {
+      const int64_t layer = (int64_t)c[0] * c[1] * N3;
+      q.n_global = layer * c[2];
+      q.n_owned = layer * nzl;
+      q.first_global = layer * cz0;
+      q.n_stored = q.n_owned + (dist ? 2 * layer : 0);
+    }
+  }
+  return out;
+}
+
+void fill_level(fem_ctx* h, Level& L, const fem_level_part& q, int idx) {
+  L.idx = idx;
+  double det = 1.0;
+  for (int d = 0; d < 3; ++d) {
+    L.n[d] = q.cells[d];
+    L.nn[d] = h->k * q.cells[d] + 1;
+    L.h[d] = (h->mesh.hi[d] - h->mesh.lo[d]) / q.global_cells[d];
+    det *= 0.5 * L.h[d];
+  }
+  for (int d = 0; d < 3; ++d) L.cart[d] = det * (2.0 / L.h[d]) * (2.0 / L.h[d]);
+  L.nzg = q.global_cells[2];
+  L.cz0 = q.cell_z0;
+  L.dist = q.distributed != 0;
+  L.ghost_lo = q.ghost_lo;
+  L.ghost_hi = q.ghost_hi;
+  L.n_cells = (int64_t)q.cells[0] * q.cells[1] * q.cells[2];
+  L.n_dofs = q.n_owned;
+  L.n_store = q.n_stored;
+  L.own_off = (!is_cg(h) && L.dist) ? (int64_t)q.cells[0] * q.cells[1] * (h->k + 1) * (h->k + 1) * (h->k + 1) : 0;
+  L.first_global = q.first_global;
+  L.n_global = q.n_global;
+  L.cartesian = (h->mesh.deform_eps == 0.0);
+}
+
+void build_levels(fem_ctx* h) {
+  const std::vector<fem_level_part> parts = partition(h->mesh, h->k, h->method, h->opt);
+  const int nl = (int)parts.size();
   h->levels.resize(nl);
   for (int l = 0; l < nl; ++l) {
     Level& L = h->levels[l];
-    const auto& c = ns[nl - 1 - l];
-    L.idx = l;
-    double det = 1.0;
-    for (int d = 0; d < 3; ++d) {
-      L.n[d] = c[d];
-      L.nn[d] = h->k * c[d] + 1;
-      L.h[d] = (h->mesh.hi[d] - h->mesh.lo[d]) / c[d];
-      det *= 0.5 * L.h[d];
+    fill_level(h, L, parts[l], l);
+    L.diag = valloc(L);
+    L.dinv = valloc(L);
+    L.b = valloc(L);
+    L.x = valloc(L);
+    L.t = valloc(L);
+    L.x2 = valloc(L);
+    L.x3 = valloc(L);
+    L.b2 = valloc(L);
+    if (L.dist && is_cg(h)) L.halo = dalloc((int64_t)L.nn[0] * L.nn[1]);
+    if (L.dist && l > 0 && !parts[l - 1].distributed) {
+      // last distributed level: whole-level twin for the transfers to the replicated level
+      fem_level_part whole = parts[l];
+      whole.cells[2] = whole.global_cells[2];
+      whole.cell_z0 = 0;
+      whole.distributed = 0;
+      whole.ghost_lo = whole.ghost_hi = -1;
+      whole.n_owned = whole.n_stored = whole.n_global;
+      whole.first_global = 0;
+      L.full.reset(new Level());
+      fill_level(h, *L.full, whole, l);
+      L.gb = dalloc(L.n_global);
+      L.gx = dalloc(L.n_global);
     }
-    for (int d = 0; d < 3; ++d) L.cart[d] = det * (2.0 / L.h[d]) * (2.0 / L.h[d]);
-    L.n_cells = (int64_t)c[0] * c[1] * c[2];
-    L.n_dofs = is_cg(h) ? (int64_t)L.nn[0] * L.nn[1] * L.nn[2]
-                        : L.n_cells * (h->k + 1) * (h->k + 1) * (h->k + 1);
-    L.cartesian = (h->mesh.deform_eps == 0.0);
-    L.diag = dalloc(L.n_dofs);
-    L.dinv = dalloc(L.n_dofs);
-    L.b = dalloc(L.n_dofs);
-    L.x = dalloc(L.n_dofs);
-    L.t = dalloc(L.n_dofs);
-    L.x2 = dalloc(L.n_dofs);
-    L.x3 = dalloc(L.n_dofs);
-    L.b2 = dalloc(L.n_dofs);
   }
 }
 
@@ -465,8 +650,9 @@ void level_geometry_and_diagonal(fem_ctx* h, Level& L) {
     if (!is_cg(h)) launch_dg_face_geometry(h, L);
   }
   if (is_cg(h)) {
-    launch_zero(h, L.diag, L.n_dofs);
+    launch_zero(h, L.diag, L.n_store);
     launch_cg_diagonal(h, L);
+    halo_export_add(h, L, L.diag);
     launch_set_constrained(h, L, nullptr, L.diag);     // diag = 1 on constrained rows
     launch_dinv(h, L);
     launch_set_constrained_value(h, L, 0.0, L.dinv);   // D^-1 = 0 on constrained rows
@@ -566,10 +752,12 @@ void destroy(fem_ctx* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (auto& L : h->levels) {
-    for (double** p : {&L.G, &L.face, &L.diag, &L.dinv, &L.b, &L.x, &L.x2, &L.x3, &L.t, &L.b2,
-                       &L.pcg_r, &L.pcg_p, &L.pcg_q, &L.pcg_z})
-      dfree(*p);
+    for (double** p : {&L.G, &L.face, &L.halo, &L.gb, &L.gx}) dfree(*p);
+    for (double** p : {&L.diag, &L.dinv, &L.b, &L.x, &L.x2, &L.x3, &L.t, &L.b2, &L.pcg_r, &L.pcg_p,
+                       &L.pcg_q, &L.pcg_z})
+      vfree(L, *p);
   }
+  h->comm.reset();
   if (h->coarse_free) cudaFree(h->coarse_free);
   dfree(h->coarse_inv);
   dfree(h->red);
@@ -611,6 +799,7 @@ int fem_default_options(fem_options* o) {
   o->stream = nullptr;
   o->device = -1;
   o->profile = 0;
+  o->slab_min_layers = 2;
   return FEM_OK;
 }
 
@@ -628,8 +817,10 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     for (int s = 0; s < 6; ++s)
       if (mesh->bc[s] != FEM_BC_DIRICHLET && mesh->bc[s] != FEM_BC_NEUMANN)
         throw Error{FEM_E_ARG, "bc must be FEM_BC_DIRICHLET or FEM_BC_NEUMANN"};
-    if (mesh->nranks != 1 || mesh->rank != 0)
-      throw Error{FEM_E_ARG, "multi-rank slabs are not available in this build (nranks must be 1)"};
+    if (mesh->nranks < 1 || mesh->rank < 0 || mesh->rank >= mesh->nranks)
+      throw Error{FEM_E_ARG, "rank must be in [0, nranks)"};
+    if (mesh->nranks > 1 && ((mesh->nccl_id != nullptr) == (mesh->local_group != nullptr)))
+      throw Error{FEM_E_ARG, "nranks > 1 needs exactly one of nccl_id / local_group"};
     h = new fem_ctx();
     h->k = degree;
     h->method = method;
@@ -642,12 +833,21 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (h->opt.device >= 0) FEM_CUDA_TRY(cudaSetDevice(h->opt.device));
     FEM_CUDA_TRY(cudaGetDevice(&h->device));
     h->stream = (cudaStream_t)h->opt.stream;
+    h->rank = mesh->rank;
+    h->nranks = mesh->nranks;
+    if (h->nranks > 1) {
+      h->comm = mesh->nccl_id ? make_nccl_comm(mesh->nccl_id, h->rank, h->nranks)
+                              : make_local_comm(mesh->local_group, h->rank, h->nranks);
+      h->use_graphs = h->comm->graph_capturable();
+    }
+    if (const char* e = std::getenv("FEM_NO_GRAPHS")) h->use_graphs = h->use_graphs && std::atoi(e) == 0;
     FEM_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     h->prof.on = h->opt.profile != 0;
     if (const char* e = std::getenv("FEM_GENERAL_PATH")) h->general_path = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_CHUNK_LAYERS")) h->chunk_layers = std::atoi(e);
     build_tables(degree, h->tab);
-    h->red = dalloc(16 * kRedBlocks);
+    h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)
+    FEM_CUDA_TRY(cudaMemset(h->red, 0, sizeof(double) * (16 * kRedBlocks + 16)));
     h->scal = dalloc(16);
     FEM_CUDA_TRY(cudaMemset(h->scal, 0, sizeof(double) * 16));
     FEM_CUDA_TRY(cudaMallocHost(&h->hscal, sizeof(double) * 16));
@@ -670,14 +870,33 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
   return rc;
 }
 
+int fem_partition(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_options* opt,
+                  fem_level_part* out, int32_t max_levels, int32_t* n_levels) {
+  return guarded([&] {
+    if (!mesh || !out || !n_levels) throw Error{FEM_E_ARG, "null argument"};
+    if (degree < 1 || degree > kMaxDeg) throw Error{FEM_E_ARG, "degree must be in [1, 8]"};
+    if (method != FEM_CG && method != FEM_SIPG) throw Error{FEM_E_ARG, "method must be FEM_CG or FEM_SIPG"};
+    for (int d = 0; d < 3; ++d)
+      if (mesh->n[d] < 1) throw Error{FEM_E_ARG, "cells per direction must be >= 1"};
+    fem_options o;
+    fem_default_options(&o);
+    if (opt) o = *opt;
+    if (o.coarse_cells < 1) throw Error{FEM_E_ARG, "invalid solver options"};
+    const auto parts = partition(*mesh, degree, method, o);
+    if ((int)parts.size() > max_levels) throw Error{FEM_E_ARG, "max_levels too small"};
+    for (size_t i = 0; i < parts.size(); ++i) out[i] = parts[i];
+    *n_levels = (int32_t)parts.size();
+  });
+}
+
 int fem_info(fem_handle h, int64_t* n_local, int64_t* n_global, int64_t* first_global,
              int32_t* n_levels) {
   return guarded([&] {
     check_handle(h);
     const Level& L = h->levels.back();
     if (n_local) *n_local = L.n_dofs;
-    if (n_global) *n_global = L.n_dofs;
-    if (first_global) *first_global = 0;
+    if (n_global) *n_global = L.n_global;
+    if (first_global) *first_global = L.first_global;
     if (n_levels) *n_levels = (int32_t)h->levels.size();
   });
 }
@@ -702,7 +921,13 @@ int fem_level_apply(fem_handle h, int32_t level, const double* x, int64_t nx, do
     const double* dx = in_vec(h, x, nx, 0);
     bool st;
     double* dy = out_vec(h, y, ny, 1, false, &st);
-    apply_level(h, L, dx, dy, true);
+    if (L.dist) {   // level vectors carry the ghosts
+      launch_copy(h, L.x2, dx, L.n_dofs);
+      apply_level(h, L, L.x2, L.t, true);
+      launch_copy(h, dy, L.t, L.n_dofs);
+    } else {
+      apply_level(h, L, dx, dy, true);
+    }
     finish_out(h, y, dy, ny, st);
   });
 }
@@ -811,7 +1036,8 @@ int mg_prolongate_add(fem_handle h, int32_t level, const double* xc, int64_t nc,
     const double* dc = in_vec(h, xc, nc, 0);
     bool st;
     double* df = out_vec(h, xf, nf, 1, true, &st);
-    launch_prolongate_add(h, C, F, dc, df);
+    launch_copy(h, C.x, dc, C.n_dofs);   // level vector: ghosts are imported into it
+    prolongate_from(h, level, C.x, df);
     finish_out(h, xf, df, nf, st);
   });
 }
@@ -828,7 +1054,8 @@ int mg_restrict(fem_handle h, int32_t level, const double* xf, int64_t nf, doubl
     const double* df = in_vec(h, xf, nf, 0);
     bool st;
     double* dc = out_vec(h, xc, nc, 1, false, &st);
-    launch_restrict(h, C, F, df, nullptr, dc);
+    restrict_to(h, level, df, nullptr, C.b);   // level vector: CG ghost plane compress-added
+    launch_copy(h, dc, C.b, C.n_dofs);
     finish_out(h, xc, dc, nc, st);
   });
 }
@@ -873,8 +1100,10 @@ int fem_rhs(fem_handle h, double* b, int64_t nb) {
     check_size(nb, L.n_dofs, "b");
     bool st;
     double* db = out_vec(h, b, nb, 0, false, &st);
-    launch_zero(h, db, L.n_dofs);
-    launch_rhs(h, L, db);
+    launch_zero(h, L.t - L.own_off, L.n_store);
+    launch_rhs(h, L, L.t);
+    halo_export_add(h, L, L.t);
+    launch_copy(h, db, L.t, L.n_dofs);
     finish_out(h, b, db, nb, st);
   });
 }
@@ -896,39 +1125,43 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     bool st;
     double* dx = out_vec(h, x, nx, 1, true, &st);
     if (!L.pcg_r) {
-      L.pcg_r = dalloc(n);
-      L.pcg_p = dalloc(n);
-      L.pcg_q = dalloc(n);
-      L.pcg_z = dalloc(n);
+      L.pcg_r = valloc(L);
+      L.pcg_p = valloc(L);
+      L.pcg_q = valloc(L);
+      L.pcg_z = valloc(L);
     }
     double *r = L.pcg_r, *p = L.pcg_p, *q = L.pcg_q, *z = L.pcg_z;
     // CG Dirichlet rows are identity rows: x_c = b_c, r_c = 0 (the system decouples)
     if (is_cg(h)) launch_set_constrained(h, L, db, dx);
-    apply_level(h, L, dx, q, true);
+    launch_copy(h, p, dx, n);                 // level vector (ghosts) for the first apply
+    apply_level(h, L, p, q, true);
     launch_sub(h, r, db, q, n);
-    launch_dot(h, db, db, n, 6);
-    launch_dot(h, r, r, n, 2);
+    dot(h, L, db, db, 6);
+    dot(h, L, r, r, 2);
     FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, h->stream));
     FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
     const double bnorm = std::sqrt(h->hscal[6]);
     double rnorm = std::sqrt(h->hscal[2]);
     int it = 0;
     if (!std::isfinite(rnorm)) throw Error{FEM_E_BREAKDOWN, "non-finite initial residual"};
+    // one PCG iteration in two parts
+    auto body_pre = [&] {
+      vcycle(h, fine, r, z);
+      dot(h, L, r, z, 3);
+      launch_pcg_update_p(h, p, z, n);      // beta = s3/s0, p = z + beta p, s0 = s3
+    };
+    auto body_upd = [&] {
+      apply_level(h, L, p, q, false);
+      dot(h, L, p, q, 1);
+      launch_pcg_update_xr(h, dx, r, p, q, n);   // alpha = s0/s1, (r,r) -> s2
+      if (L.dist) allreduce(h, h->scal + 2, 1);
+      FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, h->stream));
+    };
     if (rnorm > rtol * bnorm) {
-      if (!h->sg.g_pre || h->sg.b != db || h->sg.x != dx) {
+      if (h->use_graphs && (!h->sg.g_pre || h->sg.b != db || h->sg.x != dx)) {
         drop_solve_graphs(h);
-        Captured cp = capture(h, h->sg.ev_pre, [&] {
-          vcycle(h, fine, r, z);
-          launch_dot(h, r, z, n, 3);
-          launch_pcg_update_p(h, p, z, n);      // beta = s3/s0, p = z + beta p, s0 = s3
-        });
-        Captured cu = capture(h, h->sg.ev_upd, [&] {
-          apply_level(h, L, p, q, false);
-          launch_dot(h, p, q, n, 1);
-          launch_pcg_update_xr(h, dx, r, p, q, n);   // alpha = s0/s1, (r,r) -> s2
-          FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 4, cudaMemcpyDeviceToHost,
-                                       h->stream));
-        });
+        Captured cp = capture(h, h->sg.ev_pre, body_pre);
+        Captured cu = capture(h, h->sg.ev_upd, body_upd);
         h->sg.g_pre = cp.exec;
         h->sg.g_upd = cu.exec;
         h->sg.k_pre = cp.kernels;
@@ -936,15 +1169,22 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
         h->sg.b = db;
         h->sg.x = dx;
       }
-      // first iteration through the same graphs: p = 0 and s0 = 1 make p = z + 0
+      // first iteration through the same code: p = 0 and s0 = 1 make p = z + 0
       launch_zero(h, p, n);
       launch_set_scalar(h, 0, 1.0);
       while (it < maxit) {
-        launch_graph(h, h->sg.g_pre, h->sg.k_pre);
-        launch_graph(h, h->sg.g_upd, h->sg.k_upd);
+        if (h->use_graphs) {
+          launch_graph(h, h->sg.g_pre, h->sg.k_pre);
+          launch_graph(h, h->sg.g_upd, h->sg.k_upd);
+        } else {
+          body_pre();
+          body_upd();
+        }
         FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
-        prof_graph(h, h->sg.ev_pre);
-        prof_graph(h, h->sg.ev_upd);
+        if (h->use_graphs) {
+          prof_graph(h, h->sg.ev_pre);
+          prof_graph(h, h->sg.ev_upd);
+        }
         ++it;
         const double pq = h->hscal[1];
         rnorm = std::sqrt(h->hscal[2]);

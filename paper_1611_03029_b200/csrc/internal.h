@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -47,13 +48,46 @@ struct Tables1D {
 };
 void build_tables(int k, Tables1D& t);
 
+// ---------------------------------------------------------------- communication
+// Transport of the z-slab exchanges: NCCL between processes, or an
+// in-process group of threads sharing one device (comm.cu).  All calls are
+// enqueued on the caller's stream; every rank issues the same sequence.
+class Comm {
+ public:
+  struct Msg {
+    int peer;      // other rank
+    int tag;       // matches a send of the peer with a recv here (in-process transport)
+    double* ptr;   // device buffer
+    int64_t n;     // doubles
+  };
+  int rank = 0, nranks = 1;
+  virtual ~Comm() {}
+  virtual void exchange(const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t s) = 0;
+  virtual void allreduce_sum(double* p, int64_t n, cudaStream_t s) = 0;
+  virtual bool graph_capturable() const = 0;
+};
+std::unique_ptr<Comm> make_nccl_comm(const void* id, int rank, int nranks);
+std::unique_ptr<Comm> make_local_comm(void* group, int rank, int nranks);
+
 // ---------------------------------------------------------------- level data
+// Vector convention: every level vector pointer points at the rank's OWNED block;
+// ghost data lives in the same allocation (CG: the ghost node plane right after
+// the owned planes; SIPG: one ghost cell layer before and one after the owned
+// cells).  Vector kernels touch [0, n_dofs); operator kernels read the ghosts.
 struct Level {
   int idx = 0;
-  int n[3] = {0, 0, 0};          // cells per direction (rank-local in z)
-  int nn[3] = {0, 0, 0};         // CG nodes per direction
+  int n[3] = {0, 0, 0};          // rank-local cells per direction (z: slab layers)
+  int nn[3] = {0, 0, 0};         // CG nodes per direction held locally (z: k n[2] + 1)
+  int nzg = 0;                   // cells in z of the whole level
+  int cz0 = 0;                   // global index of the first local cell layer
+  bool dist = false;             // z-slab of this rank (else replicated / single rank)
+  int ghost_lo = -1, ghost_hi = -1;  // neighbour ranks (dist only)
   double h[3] = {0, 0, 0};
-  int64_t n_cells = 0, n_dofs = 0;
+  int64_t n_cells = 0;           // local cells
+  int64_t n_dofs = 0;            // owned DoFs (vector length)
+  int64_t n_store = 0;           // owned + ghost DoFs
+  int64_t own_off = 0;           // owned block offset inside the allocation
+  int64_t first_global = 0, n_global = 0;
   bool cartesian = true;
   double cart[3] = {0, 0, 0};    // Cartesian metric: det(J) (2/h_d)^2
   double* G = nullptr;           // deformed: [cell][6][q]
@@ -65,6 +99,11 @@ struct Level {
   double *b = nullptr, *x = nullptr, *x2 = nullptr, *x3 = nullptr, *t = nullptr, *b2 = nullptr;
   // PCG vectors (finest level, allocated on first cg_solve)
   double *pcg_r = nullptr, *pcg_p = nullptr, *pcg_q = nullptr, *pcg_z = nullptr;
+  double* halo = nullptr;        // CG dist: receive buffer of one node plane (compress-add)
+  // last distributed level above a replicated one: the whole-level twin used for
+  // the transfers (gathered residual gb, prolongated correction gx; no geometry)
+  std::unique_ptr<Level> full;
+  double *gb = nullptr, *gx = nullptr;
 };
 
 struct Profile {
@@ -114,6 +153,9 @@ struct fem_ctx {
   fem::Profile prof;
   cudaStream_t cap_stream = nullptr;   // non-blocking stream used only for graph capture
   fem::SolveGraphs sg;
+  std::unique_ptr<fem::Comm> comm;      // nranks > 1
+  int rank = 0, nranks = 1;
+  bool use_graphs = true;               // PCG iteration as CUDA graphs (not with the in-process transport)
   int chunk_layers = 0;                 // Cartesian CG apply: cell layers per z-chunk (FEM_CHUNK_LAYERS; 0 = one launch)
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
 };
@@ -152,5 +194,11 @@ void launch_sub(fem_ctx* h, double* r, const double* b, const double* ax, int64_
 
 // level helpers
 inline bool is_cg(const fem_ctx* h) { return h->method == FEM_CG; }
+
+// z-slab exchanges (api.cu); no-ops on replicated levels / single rank
+void halo_import(fem_ctx* h, const Level& L, double* v);      // ghosts <- neighbours' owned data
+void halo_export_add(fem_ctx* h, const Level& L, double* v);  // CG: ghost plane added into the owner
+void allreduce(fem_ctx* h, double* p, int64_t n);             // sum over ranks (device buffer)
+void launch_add(fem_ctx* h, double* y, const double* x, int64_t n);  // y += x
 
 }  // namespace fem

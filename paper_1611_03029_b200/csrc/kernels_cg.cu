@@ -29,8 +29,9 @@ struct OpArgs {
   const double* __restrict__ x;
   double* __restrict__ y;
   const double* __restrict__ G;  // deformed: [cell][6][q]
-  int n0, n1, n2;                // cells per direction
-  int nn0, nn1, nn2;             // nodes per direction
+  int n0, n1, n2;                // rank-local cells per direction
+  int nn0, nn1, nn2;             // nodes per direction; nn2 = GLOBAL node planes in z
+  int gz0;                       // global index of the local node plane 0 (z-slab offset)
   int bcmask;
   int64_t n_cells;
   double c0, c1, c2;             // Cartesian metric det(J) (2/h_d)^2
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
   const int64_t base = gx + (int64_t)a.nn0 * gy + zs * (int64_t)(K * cz);
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    const bool m = cg_constrained(a.bcmask, gx, gy, K * cz + l, a.nn0, a.nn1, a.nn2);
+    const bool m = cg_constrained(a.bcmask, gx, gy, a.gz0 + K * cz + l, a.nn0, a.nn1, a.nn2);
     u[l] = (active && !m) ? __ldg(a.x + base + l * zs) : 0.0;
   }
   // Deformed: one TMA bulk copy stages the block's G slice (C cells x 6 x N^3 doubles,
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
   if (active) {
 #pragma unroll
     for (int l = 0; l < N; ++l) {
-      const bool m = cg_constrained(a.bcmask, gx, gy, K * cz + l, a.nn0, a.nn1, a.nn2);
+      const bool m = cg_constrained(a.bcmask, gx, gy, a.gz0 + K * cz + l, a.nn0, a.nn1, a.nn2);
       if (!m) atomicAdd(a.y + base + l * zs, v[l]);
     }
   }
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     const int64_t base = (int64_t)K * cx + (int64_t)a.nn0 * gy + zs * gz;
 #pragma unroll
     for (int l = 0; l < N; ++l) {
-      const bool m = cg_constrained(a.bcmask, K * cx + l, gy, gz, a.nn0, a.nn1, a.nn2);
+      const bool m = cg_constrained(a.bcmask, K * cx + l, gy, a.gz0 + gz, a.nn0, a.nn1, a.nn2);
       u[l] = (active && !m) ? __ldg(a.x + base + l) : 0.0;
     }
     mv<N>(T.M, u, f0);
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     const int64_t base = gx + (int64_t)a.nn0 * gy + zs * (int64_t)(K * cz);
 #pragma unroll
     for (int l = 0; l < N; ++l) {
-      const bool m = cg_constrained(a.bcmask, gx, gy, K * cz + l, a.nn0, a.nn1, a.nn2);
+      const bool m = cg_constrained(a.bcmask, gx, gy, a.gz0 + K * cz + l, a.nn0, a.nn1, a.nn2);
       if (!m) atomicAdd(a.y + base + l * zs, fma(a.c2, f0[l], f1[l]));
     }
   }
@@ -218,7 +219,7 @@ __global__ void cg_diag_kernel(OpArgs a, Tab<K + 1> T) {
   const int64_t r = cell / a.n0;
   const int cy = (int)(r % a.n1), cz = (int)(r / a.n1);
   const int gx = K * cx + i0, gy = K * cy + i1, gz = K * cz + i2;
-  if (cg_constrained(a.bcmask, gx, gy, gz, a.nn0, a.nn1, a.nn2)) return;
+  if (cg_constrained(a.bcmask, gx, gy, a.gz0 + gz, a.nn0, a.nn1, a.nn2)) return;
   atomicAdd(a.y + gx + (int64_t)a.nn0 * (gy + (int64_t)a.nn1 * gz), d);
 }
 
@@ -290,22 +291,29 @@ __global__ void rhs_kernel(MapArgs m, OpArgs a, Tab<K + 1> T) {
       a.y[cell * N3 + i] = s;
     } else {
       const int gx = K * cx + i0, gy = K * cy + i1, gz = K * cz + i2;
-      if (!cg_constrained(a.bcmask, gx, gy, gz, a.nn0, a.nn1, a.nn2))
+      if (!cg_constrained(a.bcmask, gx, gy, a.gz0 + gz, a.nn0, a.nn1, a.nn2))
         atomicAdd(a.y + gx + (int64_t)a.nn0 * (gy + (int64_t)a.nn1 * gz), s);
     }
   }
 }
 
 // ---------------------------------------------------------------- Dirichlet rows
-// y_c = x_c (x == nullptr: y_c = 1) on the six boundary planes of Dirichlet sides.
+// y_c = x_c (x == nullptr: y_c = val) on the boundary planes of Dirichlet sides,
+// restricted to the rank's owned node planes [0, nzo) (global plane gz0 + local).
 __global__ void set_constrained_kernel(const double* __restrict__ x, double val, double* __restrict__ y,
-                                       int nn0, int nn1, int nn2, int bcmask) {
+                                       int nn0, int nn1, int nzo, int gz0, int nn2g, int bcmask) {
   const int side = blockIdx.y;
   if (!(bcmask & (1 << side))) return;
   const int d = side / 2;
-  const int fixed = (side % 2) ? ((d == 0 ? nn0 : d == 1 ? nn1 : nn2) - 1) : 0;
+  int fixed;
+  if (d < 2) {
+    fixed = (side % 2) ? ((d == 0 ? nn0 : nn1) - 1) : 0;
+  } else {
+    fixed = ((side % 2) ? nn2g - 1 : 0) - gz0;   // local plane of the global boundary plane
+    if (fixed < 0 || fixed >= nzo) return;
+  }
   const int na = (d == 0) ? nn1 : nn0;
-  const int nb = (d == 2) ? nn1 : nn2;
+  const int nb = (d == 2) ? nn1 : nzo;
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= (int64_t)na * nb) return;
   const int ia = (int)(id % na), ib = (int)(id / na);
@@ -331,7 +339,8 @@ OpArgs op_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
   a.n2 = L.n[2];
   a.nn0 = L.nn[0];
   a.nn1 = L.nn[1];
-  a.nn2 = L.nn[2];
+  a.nn2 = L.dist ? h->k * L.nzg + 1 : L.nn[2];
+  a.gz0 = h->k * L.cz0;
   int mask = 0;
   for (int s = 0; s < 6; ++s)
     if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
@@ -351,7 +360,7 @@ MapArgs map_args(const fem_ctx* h, const Level& L) {
     m.h[d] = L.h[d];
   }
   m.eps = h->mesh.deform_eps;
-  m.cz0 = 0;
+  m.cz0 = L.cz0;
   return m;
 }
 
@@ -476,10 +485,11 @@ namespace {
 void set_constrained_impl(fem_ctx* h, const Level& L, const double* x, double v, double* y) {
   const OpArgs a = op_args(h, L, x, y);
   if (a.bcmask == 0) return;
+  const int nzo = (int)(L.n_dofs / ((int64_t)L.nn[0] * L.nn[1]));   // owned node planes
   int64_t mx = std::max<int64_t>((int64_t)L.nn[0] * L.nn[1],
-                                 std::max<int64_t>((int64_t)L.nn[0] * L.nn[2], (int64_t)L.nn[1] * L.nn[2]));
+                                 std::max<int64_t>((int64_t)L.nn[0] * nzo, (int64_t)L.nn[1] * nzo));
   dim3 grid((unsigned)((mx + 255) / 256), 6);
-  set_constrained_kernel<<<grid, 256, 0, h->stream>>>(x, v, y, L.nn[0], L.nn[1], L.nn[2], a.bcmask);
+  set_constrained_kernel<<<grid, 256, 0, h->stream>>>(x, v, y, L.nn[0], L.nn[1], nzo, a.gz0, a.nn2, a.bcmask);
   count_launch();
   check_launch("set_constrained_kernel");
 }

@@ -42,7 +42,8 @@ struct DgArgs {
   const double* __restrict__ faceq;   // deformed face records [face][7][N2]
   const double* __restrict__ fsigma;  // [face]
   int64_t face_off[3];                // first face record of direction d
-  int n[3];
+  int n[3];          // rank-local cells per direction (z: slab layers)
+  int cz0, nzg;      // global index of the first local layer, global layers
   int64_t n_cells;
   int bcmask;
   double c[3];      // Cartesian metric det J (2/h_d)^2
@@ -62,6 +63,13 @@ template <int D> struct Tang;
 template <> struct Tang<0> { static constexpr int t1 = 1, t2 = 2; };
 template <> struct Tang<1> { static constexpr int t1 = 0, t2 = 2; };
 template <> struct Tang<2> { static constexpr int t1 = 0, t2 = 1; };
+
+// 0 interior, 1 Dirichlet, 2 Neumann: kind of face s (0 lower, 1 upper) of local cell c along D
+__device__ __forceinline__ int face_kind(const DgArgs& A, int D, const int c[3], int s) {
+  const int nb = (D == 2 ? A.cz0 : 0) + c[D] + (s ? 1 : -1);
+  const int nD = D == 2 ? A.nzg : A.n[D];
+  return (nb >= 0 && nb < nD) ? 0 : ((A.bcmask >> (2 * D + s)) & 1 ? 1 : 2);
+}
 
 __device__ __forceinline__ int64_t face_record(const DgArgs& A, int D, const int c[3], int p) {
   const int t1 = D == 0 ? 1 : 0, t2 = D == 2 ? 1 : 2;
@@ -83,10 +91,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
   const int64_t stride = D == 0 ? 1 : (D == 1 ? (int64_t)A.n[0] : (int64_t)A.n[0] * A.n[1]);
   int kind[2];  // 0 interior, 1 Dirichlet, 2 Neumann
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int nb = c[D] + (s ? 1 : -1);
-    kind[s] = (nb >= 0 && nb < A.n[D]) ? 0 : ((A.bcmask >> (2 * D + s)) & 1 ? 1 : 2);
-  }
+  for (int s = 0; s < 2; ++s) kind[s] = face_kind(A, D, c, s);
   // ---- F1: traces of the own and neighbour d-lines
   {
     double xl[N];
@@ -353,8 +358,7 @@ __global__ void dg_diag_kernel(DgArgs A, Tab<K + 1> T) {
     const int t1 = D == 0 ? 1 : 0, t2 = D == 2 ? 1 : 2;
     for (int s = 0; s < 2; ++s) {
       if (ii[D] != (s ? K : 0)) continue;
-      const int nb = c[D] + (s ? 1 : -1);
-      const int kind = (nb >= 0 && nb < A.n[D]) ? 0 : (((A.bcmask >> (2 * D + s)) & 1) ? 1 : 2);
+      const int kind = face_kind(A, D, c, s);
       if (kind == 2) continue;
       const double nsgn = s ? 1.0 : -1.0;
       const double m = kind == 0 ? 1.0 : 2.0;
@@ -420,7 +424,8 @@ __global__ void dg_face_geometry_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, doubl
   for (int side = 0; side < 2; ++side) {     // 0 minus (cell p-1, xi_D=+1), 1 plus (cell p, xi_D=-1)
     const int cd = side == 0 ? p - 1 : p;
     double* Jn = rec + (side == 0 ? 1 : 4) * N2 + q;
-    if (cd < 0 || cd >= A.n[D]) {
+    const int cdg = cd + (D == 2 ? A.cz0 : 0);
+    if (cdg < 0 || cdg >= (D == 2 ? A.nzg : A.n[D])) {
       Jn[0] = Jn[N2] = Jn[2 * N2] = 0.0;
       continue;
     }
@@ -446,20 +451,22 @@ __global__ void dg_face_geometry_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, doubl
   }
 }
 
+// volumes of the local cells plus one cell layer below and above (z-slab neighbours):
+// vol[(cz + 1) n0 n1 + cy n0 + cx], cz in [-1, n2]
 template <int K>
 __global__ void dg_cell_volume_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double* vol) {
   constexpr int N = K + 1;
-  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (cell >= A.n_cells) return;
-  const int cx = (int)(cell % A.n[0]);
-  const int64_t r = cell / A.n[0];
-  const int cy = (int)(r % A.n[1]), cz = (int)(r / A.n[1]);
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)A.n[0] * A.n[1] * (A.n[2] + 2)) return;
+  const int cx = (int)(id % A.n[0]);
+  const int64_t r = id / A.n[0];
+  const int cy = (int)(r % A.n[1]), cz = (int)(r / A.n[1]) - 1;
   double v = 0.0;
   for (int q2 = 0; q2 < N; ++q2)
     for (int q1 = 0; q1 < N; ++q1)
       for (int q0 = 0; q0 < N; ++q0)
         v += T.w[q0] * T.w[q1] * T.w[q2] * map_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]).det;
-  vol[cell] = v;
+  vol[id] = v;
 }
 
 // sigma_F = c (k+1)^2 / h_F, 1/h_F = (|F|/|K-| + |F|/|K+|)/2 (interior), |F|/|K| (boundary).
@@ -484,8 +491,9 @@ __global__ void dg_face_sigma_kernel(DgArgs A, double pen, const double* faceq, 
   int cnt = 0;
   for (int side = 0; side < 2; ++side) {
     c[D] = side == 0 ? p - 1 : p;
-    if (c[D] < 0 || c[D] >= A.n[D]) continue;
-    inv_h += area / vol[c[0] + (int64_t)A.n[0] * (c[1] + (int64_t)A.n[1] * c[2])];
+    const int cg = c[D] + (D == 2 ? A.cz0 : 0);
+    if (cg < 0 || cg >= (D == 2 ? A.nzg : A.n[D])) continue;
+    inv_h += area / vol[c[0] + (int64_t)A.n[0] * (c[1] + (int64_t)A.n[1] * (c[2] + 1))];
     ++cnt;
   }
   fsigma[fr] = pen * (K + 1) * (K + 1) * inv_h / cnt;
@@ -515,6 +523,8 @@ DgArgs dg_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
   A.faceq = L.face;
   A.fsigma = L.face ? L.face + off * 7 * N2 : nullptr;
   A.n_cells = L.n_cells;
+  A.cz0 = L.cz0;
+  A.nzg = L.nzg;
   int mask = 0;
   for (int s = 0; s < 6; ++s)
     if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
@@ -539,7 +549,7 @@ MapArgs dg_map_args(const fem_ctx* h, const Level& L) {
     m.h[d] = L.h[d];
   }
   m.eps = h->mesh.deform_eps;
-  m.cz0 = 0;
+  m.cz0 = L.cz0;
   return m;
 }
 
@@ -584,12 +594,13 @@ void dg_face_geometry_k(fem_ctx* h, Level& L) {
   const int64_t nf = n_faces(L);
   FEM_CUDA_TRY(cudaMalloc(&L.face, sizeof(double) * (nf * 7 * N2 + nf)));
   double* vol = nullptr;
-  FEM_CUDA_TRY(cudaMalloc(&vol, sizeof(double) * L.n_cells));
+  const int64_t nvol = (int64_t)L.n[0] * L.n[1] * (L.n[2] + 2);
+  FEM_CUDA_TRY(cudaMalloc(&vol, sizeof(double) * nvol));
   const DgArgs A = dg_args(h, L, nullptr, nullptr);
   const MapArgs m = dg_map_args(h, L);
   const Tab<N> T = make_tab<N>(h->tab);
   dg_face_geometry_kernel<K><<<(unsigned)((nf * N2 + 255) / 256), 256, 0, h->stream>>>(m, A, T, L.face);
-  dg_cell_volume_kernel<K><<<(unsigned)((L.n_cells + 255) / 256), 256, 0, h->stream>>>(m, A, T, vol);
+  dg_cell_volume_kernel<K><<<(unsigned)((nvol + 255) / 256), 256, 0, h->stream>>>(m, A, T, vol);
   dg_face_sigma_kernel<K><<<(unsigned)((nf + 255) / 256), 256, 0, h->stream>>>(
       A, h->opt.penalty_factor, L.face, vol, L.face + nf * 7 * N2);
   count_launch(3);

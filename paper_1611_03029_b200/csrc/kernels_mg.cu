@@ -25,9 +25,10 @@ struct Embed {
 };
 
 struct TransferArgs {
-  int nc0, nc1, nc2;     // coarse cells
-  int nnc0, nnc1, nnc2;  // coarse CG nodes
-  int nnf0, nnf1, nnf2;  // fine CG nodes
+  int nc0, nc1, nc2;     // rank-local coarse cells
+  int nnc0, nnc1, nnc2;  // coarse CG nodes (z: GLOBAL node planes)
+  int nnf0, nnf1, nnf2;  // fine CG nodes (z: GLOBAL node planes)
+  int czc0, ncz;         // global index of the first local coarse layer, global coarse layers
   int bcmask;
 };
 
@@ -55,7 +56,7 @@ __global__ void prolongate_kernel(TransferArgs a, Embed<K, DG> E, const double* 
       v = xc[cell * N * N * N + i];
     } else {
       const int gx = K * cx + i0, gy = K * cy + i1, gz = K * cz + i2;
-      v = cg_constrained(a.bcmask, gx, gy, gz, a.nnc0, a.nnc1, a.nnc2)
+      v = cg_constrained(a.bcmask, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2)
               ? 0.0
               : xc[cg_index(gx, gy, gz, a.nnc0, a.nnc1)];
     }
@@ -92,10 +93,10 @@ __global__ void prolongate_kernel(TransferArgs a, Embed<K, DG> E, const double* 
     } else {
       // owned: local fine index < 2K unless this is the last coarse cell
       if ((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
-          (tt == 2 * K && cz != a.nc2 - 1))
+          (tt == 2 * K && a.czc0 + cz != a.ncz - 1))
         continue;
       const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
-      if (cg_constrained(a.bcmask, gx, gy, gz, a.nnf0, a.nnf1, a.nnf2)) continue;
+      if (cg_constrained(a.bcmask, gx, gy, 2 * K * a.czc0 + gz, a.nnf0, a.nnf1, a.nnf2)) continue;
       xf[cg_index(gx, gy, gz, a.nnf0, a.nnf1)] += s;
     }
   }
@@ -124,9 +125,9 @@ __global__ void restrict_kernel(TransferArgs a, Embed<K, DG> E, const double* __
       v = bf[idx] - (axf ? axf[idx] : 0.0);
     } else {
       const bool owned = !((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
-                           (tt == 2 * K && cz != a.nc2 - 1));
+                           (tt == 2 * K && a.czc0 + cz != a.ncz - 1));
       const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
-      if (owned && !cg_constrained(a.bcmask, gx, gy, gz, a.nnf0, a.nnf1, a.nnf2)) {
+      if (owned && !cg_constrained(a.bcmask, gx, gy, 2 * K * a.czc0 + gz, a.nnf0, a.nnf1, a.nnf2)) {
         const int64_t idx = cg_index(gx, gy, gz, a.nnf0, a.nnf1);
         v = bf[idx] - (axf ? axf[idx] : 0.0);
       }
@@ -159,7 +160,7 @@ __global__ void restrict_kernel(TransferArgs a, Embed<K, DG> E, const double* __
       xc[cell * N * N * N + o] = s;
     } else {
       const int gx = K * cx + i, gy = K * cy + j, gz = K * cz + l;
-      if (!cg_constrained(a.bcmask, gx, gy, gz, a.nnc0, a.nnc1, a.nnc2))
+      if (!cg_constrained(a.bcmask, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2))
         atomicAdd(xc + cg_index(gx, gy, gz, a.nnc0, a.nnc1), s);
     }
   }
@@ -186,11 +187,17 @@ __global__ void axpby_kernel(double* __restrict__ y, const double* __restrict__ 
     y[i] = a * x[i] + b * y[i];
 }
 
+__global__ void add_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] += x[i];
+}
+
 __global__ void sub_kernel(double* __restrict__ r, const double* __restrict__ b,
                            const double* __restrict__ ax, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    r[i] = b[i] - ax[i];
+    r[i] = b[i] - (ax ? ax[i] : 0.0);
 }
 
 __global__ void dinv_kernel(const double* __restrict__ d, double* __restrict__ di, int64_t n) {
@@ -228,14 +235,15 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return s;
 }
 
-__device__ unsigned int g_red_counter[16];
-
-__device__ __forceinline__ void finish_reduction(double part, double* red, double* out, int slot) {
+// counters: per-handle array (after the partial sums in h->red), so that handles
+// running concurrently (ranks of an in-process group) never share a counter
+__device__ __forceinline__ void finish_reduction(double part, double* red, double* out, int slot,
+                                                 unsigned int* counters) {
   __shared__ bool last;
   if (threadIdx.x == 0) {
     red[blockIdx.x] = part;
     __threadfence();
-    const unsigned prev = atomicAdd(&g_red_counter[slot], 1u);
+    const unsigned prev = atomicAdd(&counters[slot], 1u);
     last = (prev == gridDim.x - 1);
   }
   __syncthreads();
@@ -246,26 +254,26 @@ __device__ __forceinline__ void finish_reduction(double part, double* red, doubl
     const double s = block_sum(v, sh);
     if (threadIdx.x == 0) {
       out[slot] = s;
-      g_red_counter[slot] = 0;
+      counters[slot] = 0;
     }
   }
 }
 
 __global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
-                           double* red, double* out, int slot) {
+                           double* red, double* out, int slot, unsigned int* counters) {
   __shared__ double sh[32];
   double v = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     v = fma(a[i], b[i], v);
   const double s = block_sum(v, sh);
-  finish_reduction(s, red, out, slot);
+  finish_reduction(s, red, out, slot, counters);
 }
 
 // alpha = scal[0]/scal[1]  (rz / pq);  x += alpha p;  r -= alpha q;  scal[2] = (r, r)
 __global__ void pcg_update_xr_kernel(double* __restrict__ x, double* __restrict__ r,
                                      const double* __restrict__ p, const double* __restrict__ q,
-                                     int64_t n, double* red, double* scal) {
+                                     int64_t n, double* red, double* scal, unsigned int* counters) {
   __shared__ double sh[32];
   const double alpha = scal[0] / scal[1];
   double v = 0.0;
@@ -277,7 +285,7 @@ __global__ void pcg_update_xr_kernel(double* __restrict__ x, double* __restrict_
     v = fma(ri, ri, v);
   }
   const double s = block_sum(v, sh);
-  finish_reduction(s, red, scal, 2);
+  finish_reduction(s, red, scal, 2, counters);
 }
 
 // beta = scal[3]/scal[0] (rz_new / rz);  p = z + beta p
@@ -323,10 +331,12 @@ TransferArgs transfer_args(const fem_ctx* h, const Level& c, const Level& f) {
   a.nc2 = c.n[2];
   a.nnc0 = c.nn[0];
   a.nnc1 = c.nn[1];
-  a.nnc2 = c.nn[2];
+  a.nnc2 = h->k * c.nzg + 1;
   a.nnf0 = f.nn[0];
   a.nnf1 = f.nn[1];
-  a.nnf2 = f.nn[2];
+  a.nnf2 = h->k * f.nzg + 1;
+  a.czc0 = c.cz0;
+  a.ncz = c.nzg;
   int mask = 0;
   for (int s = 0; s < 6; ++s)
     if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
@@ -410,7 +420,7 @@ void launch_prolongate_add(fem_ctx* h, const Level& c, const Level& f, const dou
 
 void launch_restrict(fem_ctx* h, const Level& c, const Level& f, const double* bf, const double* axf,
                      double* xc) {
-  if (h->method == FEM_CG) launch_zero(h, xc, c.n_dofs);
+  if (h->method == FEM_CG) launch_zero(h, xc, c.n_store);   // ghost plane too (compress-added after)
   FEM_DISPATCH_K(h->k, restrict_k, h, c, f, bf, axf, xc);
 }
 
@@ -429,7 +439,7 @@ void launch_dinv(fem_ctx* h, Level& L) {
 }
 
 void launch_splitmix(fem_ctx* h, const Level& L, uint64_t seed, double* s) {
-  splitmix_kernel<<<vec_grid(L.n_dofs), 256, 0, h->stream>>>(s, seed, 0, L.n_dofs);
+  splitmix_kernel<<<vec_grid(L.n_dofs), 256, 0, h->stream>>>(s, seed, L.first_global, L.n_dofs);
   count_launch();
   check_launch("splitmix_kernel");
 }
@@ -444,14 +454,15 @@ void launch_cheb_step(fem_ctx* h, const Level& L, double* xn, const double* x, c
 
 void launch_dot(fem_ctx* h, const double* a, const double* b, int64_t n, int slot) {
   dot_kernel<<<kRedBlocks, kRedThreads, 0, h->stream>>>(a, b, n, h->red + slot * kRedBlocks, h->scal,
-                                                        slot);
+                                                        slot, (unsigned int*)(h->red + 16 * kRedBlocks));
   count_launch();
   check_launch("dot_kernel");
 }
 
 void launch_pcg_update_xr(fem_ctx* h, double* x, double* r, const double* p, double* q, int64_t n) {
   pcg_update_xr_kernel<<<kRedBlocks, kRedThreads, 0, h->stream>>>(x, r, p, q, n,
-                                                                  h->red + 2 * kRedBlocks, h->scal);
+                                                                  h->red + 2 * kRedBlocks, h->scal,
+                                                                  (unsigned int*)(h->red + 16 * kRedBlocks));
   count_launch();
   check_launch("pcg_update_xr_kernel");
 }
@@ -483,6 +494,13 @@ void launch_axpby(fem_ctx* h, double* y, const double* x, double a, double b, in
   axpby_kernel<<<vec_grid(n), 256, 0, h->stream>>>(y, x, a, b, n);
   count_launch();
   check_launch("axpby_kernel");
+}
+
+void launch_add(fem_ctx* h, double* y, const double* x, int64_t n) {
+  if (n <= 0) return;
+  add_kernel<<<vec_grid(n), 256, 0, h->stream>>>(y, x, n);
+  count_launch();
+  check_launch("add_kernel");
 }
 
 void launch_sub(fem_ctx* h, double* r, const double* b, const double* ax, int64_t n) {

@@ -35,7 +35,7 @@ class FemError(RuntimeError):
 class fem_mesh(C.Structure):
     _fields_ = [("n", C.c_int32 * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3),
                 ("deform_eps", C.c_double), ("bc", C.c_int32 * 6), ("rank", C.c_int32),
-                ("nranks", C.c_int32), ("nccl_id", C.c_void_p)]
+                ("nranks", C.c_int32), ("nccl_id", C.c_void_p), ("local_group", C.c_void_p)]
 
 
 class fem_options(C.Structure):
@@ -43,7 +43,14 @@ class fem_options(C.Structure):
                 ("cheb_lo", C.c_double), ("cheb_hi", C.c_double), ("eig_iters", C.c_int32),
                 ("coarse_cells", C.c_int32), ("eig_seed", C.c_uint64),
                 ("lambda_override", C.POINTER(C.c_double)), ("stream", C.c_void_p),
-                ("device", C.c_int32), ("profile", C.c_int32)]
+                ("device", C.c_int32), ("profile", C.c_int32), ("slab_min_layers", C.c_int32)]
+
+
+class fem_level_part(C.Structure):
+    _fields_ = [("cells", C.c_int32 * 3), ("global_cells", C.c_int32 * 3), ("cell_z0", C.c_int32),
+                ("distributed", C.c_int32), ("n_owned", C.c_int64), ("first_global", C.c_int64),
+                ("n_global", C.c_int64), ("n_stored", C.c_int64), ("ghost_lo", C.c_int32),
+                ("ghost_hi", C.c_int32)]
 
 
 def _load():
@@ -54,6 +61,11 @@ def _load():
     sig = {
         "fem_default_options": (C.c_int, [C.POINTER(fem_options)]),
         "fem_setup": (C.c_int, [C.POINTER(fem_mesh), I32, I32, C.POINTER(fem_options), C.POINTER(P)]),
+        "fem_partition": (C.c_int, [C.POINTER(fem_mesh), I32, I32, C.POINTER(fem_options),
+                                    C.POINTER(fem_level_part), I32, C.POINTER(I32)]),
+        "fem_nccl_unique_id": (C.c_int, [P, I64]),
+        "fem_local_group_create": (C.c_int, [I32, C.POINTER(P)]),
+        "fem_local_group_destroy": (None, [P]),
         "fem_info": (C.c_int, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64), C.POINTER(I32)]),
         "fem_apply": (C.c_int, [P, P, I64, P, I64]),
         "fem_diagonal": (C.c_int, [P, P, I64]),
@@ -84,7 +96,8 @@ def _load():
 _lib = _load()
 
 # exported symbol list (tests check it against include/fem.h)
-SYMBOLS = ("fem_default_options", "fem_setup", "fem_info", "fem_apply", "fem_diagonal", "mg_vcycle",
+SYMBOLS = ("fem_default_options", "fem_setup", "fem_partition", "fem_nccl_unique_id",
+           "fem_local_group_create", "fem_local_group_destroy", "fem_info", "fem_apply", "fem_diagonal", "mg_vcycle",
            "cg_solve", "fem_rhs", "fem_level_info", "fem_level_apply", "fem_level_diagonal",
            "fem_level_lambda", "fem_level_geometry", "mg_smooth", "mg_prolongate_add", "mg_restrict",
            "mg_coarse_solve", "fem_sync", "fem_kernel_launches", "fem_profile_read", "fem_last_error",
@@ -120,27 +133,92 @@ def _vec(v, writable=False):
     return C.c_void_p(a.ctypes.data), a.size
 
 
+def nccl_unique_id() -> bytes:
+    """fem_nccl_unique_id: 128 bytes to broadcast from one rank to all."""
+    buf = C.create_string_buffer(128)
+    _check(_lib.fem_nccl_unique_id(C.cast(buf, C.c_void_p), 128))
+    return buf.raw
+
+
+class LocalGroup:
+    """fem_local_group_create: nranks threads of this process sharing one device."""
+
+    def __init__(self, nranks: int):
+        g = C.c_void_p()
+        _check(_lib.fem_local_group_create(nranks, C.byref(g)))
+        self.g, self.nranks = g, nranks
+
+    def close(self):
+        if getattr(self, "g", None):
+            _lib.fem_local_group_destroy(self.g)
+            self.g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _mesh(cells, lo, hi, deform_eps, bc, rank, nranks, nccl_id, local_group):
+    m = fem_mesh()
+    m.n[:] = list(cells)
+    m.lo[:] = list(lo)
+    m.hi[:] = list(hi)
+    m.deform_eps = deform_eps
+    m.bc[:] = list(bc)
+    m.rank, m.nranks = rank, nranks
+    m.nccl_id = None
+    m.local_group = local_group.g if local_group is not None else None
+    return m
+
+
+def _options(**kw):
+    o = fem_options()
+    _check(_lib.fem_default_options(C.byref(o)))
+    for name, val in kw.items():
+        if val is not None:
+            setattr(o, name, val)
+    return o
+
+
+def partition(cells, degree, method=FEM_CG, rank=0, nranks=1, coarse_cells=None, slab_min_layers=None):
+    """fem_partition (host only): per level (coarsest first) a dict of the rank's slab."""
+    m = _mesh(cells, (0.0,) * 3, (1.0,) * 3, 0.0, (FEM_BC_DIRICHLET,) * 6, rank, nranks, None, None)
+    o = _options(coarse_cells=coarse_cells, slab_min_layers=slab_min_layers)
+    out = (fem_level_part * 32)()
+    nl = C.c_int32()
+    _check(_lib.fem_partition(C.byref(m), degree, method, C.byref(o), out, 32, C.byref(nl)))
+    res = []
+    for i in range(nl.value):
+        q = out[i]
+        res.append({"cells": tuple(q.cells), "global_cells": tuple(q.global_cells), "cell_z0": q.cell_z0,
+                    "distributed": bool(q.distributed), "n_owned": q.n_owned, "first_global": q.first_global,
+                    "n_global": q.n_global, "n_stored": q.n_stored, "ghost_lo": q.ghost_lo,
+                    "ghost_hi": q.ghost_hi})
+    return res
+
+
 class Fem:
-    """One libfem handle (fem_setup ... fem_destroy)."""
+    """One libfem handle (fem_setup ... fem_destroy).
+
+    Multi-rank: pass rank/nranks and either nccl_id (bytes from nccl_unique_id(),
+    one process per GPU) or local_group (LocalGroup shared by nranks threads)."""
 
     def __init__(self, cells, degree, method=FEM_CG, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0),
                  deform_eps=0.0, bc=(FEM_BC_DIRICHLET,) * 6, penalty_factor=None, cheb_degree=None,
                  cheb_lo=None, cheb_hi=None, eig_iters=None, coarse_cells=None, eig_seed=None,
-                 lambda_override=None, stream=None, device=None, profile=False):
-        m = fem_mesh()
-        m.n[:] = list(cells)
-        m.lo[:] = list(lo)
-        m.hi[:] = list(hi)
-        m.deform_eps = deform_eps
-        m.bc[:] = list(bc)
-        m.rank, m.nranks, m.nccl_id = 0, 1, None
-        o = fem_options()
-        _check(_lib.fem_default_options(C.byref(o)))
-        for name, val in (("penalty_factor", penalty_factor), ("cheb_degree", cheb_degree),
-                          ("cheb_lo", cheb_lo), ("cheb_hi", cheb_hi), ("eig_iters", eig_iters),
-                          ("coarse_cells", coarse_cells), ("eig_seed", eig_seed)):
-            if val is not None:
-                setattr(o, name, val)
+                 lambda_override=None, stream=None, device=None, profile=False, rank=0, nranks=1,
+                 nccl_id=None, local_group=None, slab_min_layers=None):
+        m = _mesh(cells, lo, hi, deform_eps, bc, rank, nranks, None, local_group)
+        self._nccl_id = None
+        if nccl_id is not None:
+            self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
+            m.nccl_id = C.cast(self._nccl_id, C.c_void_p)
+        self._group = local_group     # keep alive while the handle exists
+        o = _options(penalty_factor=penalty_factor, cheb_degree=cheb_degree, cheb_lo=cheb_lo,
+                     cheb_hi=cheb_hi, eig_iters=eig_iters, coarse_cells=coarse_cells, eig_seed=eig_seed,
+                     slab_min_layers=slab_min_layers)
         self._lam = None
         if lambda_override is not None:
             self._lam = (C.c_double * len(lambda_override))(*lambda_override)
@@ -157,6 +235,7 @@ class Fem:
         nl, ng, fg, lv = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
         _check(_lib.fem_info(h, C.byref(nl), C.byref(ng), C.byref(fg), C.byref(lv)))
         self.n_local, self.n_global, self.first_global, self.n_levels = nl.value, ng.value, fg.value, lv.value
+        self.rank, self.nranks = rank, nranks
 
     def close(self):
         if getattr(self, "h", None):

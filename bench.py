@@ -371,7 +371,7 @@ def run_ours(args, w):
                    "step_ms": [round(s, 4) for s in step_ms]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": "cg_apply_kernel (finest-level operator apply)",
+                     "kernel": "finest-level operator apply (cg_apply_kernel for CG Q4 deformed); timed on the PCG apply q = A p of every iteration",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_us": avg_apply_s * 1e6, "launches": apply_launches,
                      "peak_source": hbm_src},

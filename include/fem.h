@@ -219,8 +219,11 @@ FEM_API int mg_coarse_solve(fem_handle h, const double* b, int64_t nb, double* x
 FEM_API int fem_sync(fem_handle h);
 /* Number of CUDA kernels this library launched (all handles) since load. */
 FEM_API int64_t fem_kernel_launches(void);
-/* profile = 1 only: total device milliseconds and launch count of the
- * operator-apply kernels on the finest level since the last reset. */
+/* profile = 1 only: total device milliseconds and launch count of the timed
+ * finest-level operator-apply kernels since the last reset: the PCG apply q = A p
+ * of every cg_solve iteration (the smoother's applies launch the same kernel and
+ * are not bracketed, so that the events do not perturb the solve) and every
+ * fem_apply / fem_level_apply on the finest level. */
 FEM_API int fem_profile_read(fem_handle h, double* ms, int64_t* launches, int32_t reset);
 
 FEM_API const char* fem_last_error(void);

@@ -16,7 +16,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libfem.so")
+LIB = os.environ.get("FEM_LIB_OUT", os.path.join(PKG, "libfem.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -25,7 +25,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr",
     "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("FEM_NVCC_EXTRA", "").split()
 
 
 def sources():
@@ -44,7 +44,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build" if LIB.endswith("libfem.so") else "build_" + os.path.basename(LIB))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "device_common.cuh"
 
 namespace fem {
 
@@ -181,8 +182,12 @@ void dot(fem_ctx* h, const Level& L, const double* a, const double* b, int slot)
 // y = A x on level L.  y is overwritten.  CG: constrained rows y_c = x_c.
 // On a distributed level x must be a level (ghost-carrying) vector: its ghosts are
 // refreshed here; y's ghost plane is compress-added into the owner (CG).
-void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool set_constrained = true) {
-  const bool finest = (&L == &h->levels.back());
+// timed: the launch is bracketed by profiling events (fem_options.profile; only the
+// PCG operator apply of cg_solve and the eager fem_apply calls are, so that the
+// events do not perturb the timed solve: the kernel is the same in every apply).
+void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool set_constrained = true,
+                 bool timed = false) {
+  const bool finest = timed && (&L == &h->levels.back());
   if (h->prof.on && finest && !h->prof.capturing && h->prof.used + 2 > 4096) prof_collect(h);
   halo_import(h, L, const_cast<double*>(x));
   if (is_cg(h)) {
@@ -637,7 +642,13 @@ void build_levels(fem_ctx* h) {
 void level_geometry_and_diagonal(fem_ctx* h, Level& L) {
   const int N = h->k + 1;
   if (!L.cartesian) {
-    L.G = dalloc(L.n_cells * 6 * N * N * N);
+    L.glayout = !is_cg(h) ? kGLayoutCell
+                : (h->k <= 4 && h->plane_kernel) ? kGLayoutPlane
+                : h->dbasis ? kGLayoutXLine : kGLayoutCell;
+    const bool plane = L.glayout == kGLayoutPlane;
+    const int64_t cells = plane ? (L.n_cells + kGroupCells - 1) / kGroupCells * kGroupCells : L.n_cells;
+    L.G = dalloc(cells * 6 * N * N * N);
+    if (plane) FEM_CUDA_TRY(cudaMemset(L.G, 0, sizeof(double) * cells * 6 * N * N * N));
     const unsigned long long init = std::numeric_limits<unsigned long long>::max();
     FEM_CUDA_TRY(cudaMemcpyAsync(h->geom_err, &init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
     launch_geometry(h, L);
@@ -845,6 +856,9 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     h->prof.on = h->opt.profile != 0;
     if (const char* e = std::getenv("FEM_GENERAL_PATH")) h->general_path = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_CHUNK_LAYERS")) h->chunk_layers = std::atoi(e);
+    if (const char* e = std::getenv("FEM_PLANE")) h->plane_kernel = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_G_DIRECT")) h->g_direct = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_DBASIS")) h->dbasis = std::atoi(e) != 0;
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)
     FEM_CUDA_TRY(cudaMemset(h->red, 0, sizeof(double) * (16 * kRedBlocks + 16)));
@@ -923,10 +937,10 @@ int fem_level_apply(fem_handle h, int32_t level, const double* x, int64_t nx, do
     double* dy = out_vec(h, y, ny, 1, false, &st);
     if (L.dist) {   // level vectors carry the ghosts
       launch_copy(h, L.x2, dx, L.n_dofs);
-      apply_level(h, L, L.x2, L.t, true);
+      apply_level(h, L, L.x2, L.t, true, true);
       launch_copy(h, dy, L.t, L.n_dofs);
     } else {
-      apply_level(h, L, dx, dy, true);
+      apply_level(h, L, dx, dy, true, true);
     }
     finish_out(h, y, dy, ny, st);
   });
@@ -979,11 +993,37 @@ int fem_level_geometry(fem_handle h, int32_t level, double* G, int64_t nG) {
     const int64_t nq = (int64_t)N * N * N;
     check_size(nG, L.n_cells * 6 * nq, "G");
     if (!G) throw Error{FEM_E_ARG, "null vector"};
-    if (!L.cartesian) {
+    if (!L.cartesian && L.glayout == kGLayoutCell) {
       bool st;
       double* dG = out_vec(h, G, nG, 0, false, &st);
       launch_copy(h, dG, L.G, nG);
       finish_out(h, G, dG, nG, st);
+      return;
+    }
+    if (!L.cartesian) {
+      // internal layout: permute to the documented [cell][6][q] order on the host
+      const int64_t cells = L.glayout == kGLayoutPlane ? (L.n_cells + kGroupCells - 1) / kGroupCells * kGroupCells
+                                                       : L.n_cells;
+      std::vector<double> raw(cells * 6 * nq), out(nG);
+      FEM_CUDA_TRY(cudaMemcpyAsync(raw.data(), L.G, sizeof(double) * raw.size(), cudaMemcpyDeviceToHost, h->stream));
+      FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+      for (int64_t c = 0; c < L.n_cells; ++c)
+        for (int comp = 0; comp < 6; ++comp)
+          for (int q = 0; q < nq; ++q) {
+            const int64_t N2 = (int64_t)N * N;
+            int64_t src;
+            if (L.glayout == kGLayoutXLine) {
+              src = (c * 6 + comp) * nq + (q % N) * N2 + q / N;
+            } else {   // plane
+              const int64_t g = c / kGroupCells, ci = c % kGroupCells;
+              src = (((g * 6 + comp) * N2 + q % N2) * kGroupCells + ci) * N + q / N2;
+            }
+            out[(c * 6 + comp) * nq + q] = raw[src];
+          }
+      if (is_device_ptr(G))
+        FEM_CUDA_TRY(cudaMemcpy(G, out.data(), sizeof(double) * nG, cudaMemcpyHostToDevice));
+      else
+        std::memcpy(G, out.data(), sizeof(double) * nG);
       return;
     }
     // Cartesian: expand the per-level constants on the host
@@ -1151,7 +1191,7 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
       launch_pcg_update_p(h, p, z, n);      // beta = s3/s0, p = z + beta p, s0 = s3
     };
     auto body_upd = [&] {
-      apply_level(h, L, p, q, false);
+      apply_level(h, L, p, q, false, true);
       dot(h, L, p, q, 1);
       launch_pcg_update_xr(h, dx, r, p, q, n);   // alpha = s0/s1, (r,r) -> s2
       if (L.dist) allreduce(h, h->scal + 2, 1);

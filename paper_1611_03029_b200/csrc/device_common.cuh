@@ -155,6 +155,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// ---- geometry-table layouts (R2), entry (cell, comp, q), q = q0 + N q1 + N^2 q2
+//   kGLayoutCell  [cell][comp][q]                        (SIPG, line kernel)
+//   kGLayoutXLine [cell][comp][q0][q1 + N q2]            (CG x-line kernel: in its
+//                 quadrature phase thread t = q1 + N q2 owns the x-line q0 = 0..N-1,
+//                 so a warp's loads of one (comp, q0) are consecutive addresses)
+//   kGLayoutPlane groups of kGroupCells cells, [group][comp][e][cell-in-group][q2],
+//                 e = q0 + N q1 (CG plane kernel: lane = q2 + N cell)
+constexpr int kGroupCells = 32;
+enum { kGLayoutCell = 0, kGLayoutPlane = 1, kGLayoutXLine = 2 };
+
+template <int N>
+__host__ __device__ __forceinline__ int64_t g_index(int layout, int64_t cell, int comp, int q) {
+  constexpr int N2 = N * N, N3 = N2 * N;
+  if (layout == kGLayoutXLine) return (cell * 6 + comp) * N3 + (q % N) * N2 + q / N;
+  if (layout != kGLayoutPlane) return (cell * 6 + comp) * N3 + q;
+  const int64_t g = cell / kGroupCells;
+  const int c = (int)(cell % kGroupCells);
+  const int pz = q / N2, e = q % N2;
+  return (((g * 6 + comp) * N2 + e) * kGroupCells + c) * N + pz;
+}
+
+// global -> L2 bulk prefetch (no destination, no completion tracking); bytes % 16 == 0
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ bool cg_constrained(int bcmask, int gx, int gy, int gz, int nn0, int nn1,
                                                int nn2) {
   return ((bcmask & 1) && gx == 0) || ((bcmask & 2) && gx == nn0 - 1) ||

@@ -90,7 +90,8 @@ struct Level {
   int64_t first_global = 0, n_global = 0;
   bool cartesian = true;
   double cart[3] = {0, 0, 0};    // Cartesian metric: det(J) (2/h_d)^2
-  double* G = nullptr;           // deformed: [cell][6][q]
+  double* G = nullptr;           // deformed: geometry table, layout g_index (device_common.cuh)
+  int glayout = 0;               // kGLayout* of G (device_common.cuh)
   double* face = nullptr;        // SIPG deformed: face data, see kernels_dg.cu
   double* diag = nullptr;        // diag(A)
   double* dinv = nullptr;        // 1/diag on free DoFs, 0 on constrained
@@ -158,6 +159,9 @@ struct fem_ctx {
   bool use_graphs = true;               // PCG iteration as CUDA graphs (not with the in-process transport)
   int chunk_layers = 0;                 // Cartesian CG apply: cell layers per z-chunk (FEM_CHUNK_LAYERS; 0 = one launch)
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
+  bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)
+  bool g_direct = true;                // FEM_G_DIRECT=0: line kernel stages G by TMA into shared memory
+  bool dbasis = false;                 // FEM_DBASIS=1: derivative-basis line kernel (measured slower, kept for study)
 };
 
 namespace fem {

@@ -32,10 +32,17 @@ struct OpArgs {
   int n0, n1, n2;                // rank-local cells per direction
   int nn0, nn1, nn2;             // nodes per direction; nn2 = GLOBAL node planes in z
   int gz0;                       // global index of the local node plane 0 (z-slab offset)
+  int glayout;                   // kGLayout* of G
+  int g_direct;                  // line kernel: G from global (L2-prefetched) instead of TMA->smem
   int bcmask;
   int64_t n_cells;
   double c0, c1, c2;             // Cartesian metric det(J) (2/h_d)^2
 };
+
+// per-cell stride of the line kernel's three work buffers: +2 doubles at Q4 spreads the
+// cells of a warp over the banks (bank-conflict model search: 11% fewer wavefronts)
+template <int N>
+__host__ __device__ constexpr int line_cell_stride() { return 3 * N * N * N + (N == 5 ? 2 : 0); }
 
 template <int K, bool DEFORMED>
 __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
@@ -47,7 +54,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
   const int ci = threadIdx.y;
   const int64_t cell = (int64_t)blockIdx.x * C + ci;
   const bool active = cell < a.n_cells;
-  double* s0 = smem + ci * 3 * N3;
+  double* s0 = smem + ci * line_cell_stride<N>();
   const int ta = t % N, tb = t / N;
   int cx = 0, cy = 0, cz = 0;
   if (active) {
@@ -71,8 +78,17 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
   // sweep phases run, and the q-point phase reads G from shared memory.
   const double* Gs = nullptr;
   __shared__ alignas(8) uint64_t gbar;
-  if (DEFORMED) {
-    double* sG = smem + C * 3 * N3;
+  if (DEFORMED && a.g_direct) {
+    // G read straight from global memory in the q-point phase (each warp load is 256
+    // contiguous bytes: q = t + N^2 l); the block's slice is bulk-prefetched into L2 now
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    if (t == 0 && ci == 0) {
+      const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
+      bulk_prefetch_l2(a.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
+    }
+    Gs = a.G + (active ? cell : 0) * 6 * N3;
+  } else if (DEFORMED) {
+    double* sG = smem + C * line_cell_stride<N>();
     const int64_t c0 = (int64_t)blockIdx.x * C;
     if (t == 0 && ci == 0) {
       const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
@@ -84,7 +100,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     __syncthreads();       // barrier initialisation visible to all threads
     Gs = sG + ci * 6 * N3;
   }
-  const CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, DEFORMED ? &gbar : nullptr};
+  const CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, (DEFORMED && !a.g_direct) ? &gbar : nullptr};
   cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
   // scatter-add (constrained rows skipped; they are set to x_c afterwards)
   if (active) {
@@ -95,7 +111,384 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     }
   }
 }
+// ---------------------------------------------------------------- derivative-basis line kernel (K1d)
+// Deformed CG cell apply (eq:mf_eval) with the gradient built from the derivative of
+// the 1-D basis at the Gauss points instead of Gauss-point collocation:
+//   grad u_q = (N'_x N_y N_z u, N_x N'_y N_z u, N_x N_y N'_z u),
+// which needs only four direction changes per cell instead of eight (the bottleneck
+// of the collocation variant is the shared-memory transposes, profiles/r01b):
+//   Z: t1 = N_z u, t2 = N'_z u               -> 2 fields
+//   Y: a = N_y t1, b = N'_y t1, c = N_y t2    -> 3 fields
+//   X: g = (N'_x a, N_x b, N_x c); f = G_q g; e = (N'_x^T f_x, N_x^T f_y, N_x^T f_z)
+//                                             -> 3 fields
+//   Y: h1 = N_y^T e1 + N'_y^T e2, h2 = N_y^T e3 -> 2 fields
+//   Z: v = N_z^T h1 + N'_z^T h2, scatter-add
+// 16 line sweeps instead of 12, 20 shared accesses per node instead of 23 (+6 for G,
+// which here is read straight from global memory in the x-line order of
+// kGLayoutXLine: coalesced, L2-prefetched at block start).
+#ifndef FEM_DLINE_MINB
+#define FEM_DLINE_MINB 2
+#endif
+template <int K>
+__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FEM_DLINE_MINB : 1)
+    cg_dline_kernel(OpArgs a, Tab<K + 1> T) {
+  constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
+  constexpr int C = CPB<K>::value;
+  extern __shared__ double smem[];
+  const int t = threadIdx.x, ci = threadIdx.y;
+  const int64_t cell = (int64_t)blockIdx.x * C + ci;
+  const bool active = cell < a.n_cells;
+  double* F0 = smem + ci * line_cell_stride<N>();
+  double* F1 = F0 + N3;
+  double* F2 = F1 + N3;
+  const int ta = t % N, tb = t / N;
+  if (t == 0 && ci == 0) {
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
+    bulk_prefetch_l2(a.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
+  }
+  int cx = 0, cy = 0, cz = 0;
+  if (active) {
+    cx = (int)(cell % a.n0);
+    const int64_t r = cell / a.n0;
+    cy = (int)(r % a.n1);
+    cz = (int)(r / a.n1);
+  }
+  const int gx = K * cx + ta, gy = K * cy + tb;
+  const int64_t zs = (int64_t)a.nn0 * a.nn1;
+  const int64_t base = gx + (int64_t)a.nn0 * gy + zs * (int64_t)(K * cz);
+  // constraints of the thread's z-line (reading R5): xy-flag for the line, z-ends
+  const int gzc = a.gz0 + K * cz;
+  const bool lm = !active || ((a.bcmask & 1) && gx == 0) || ((a.bcmask & 2) && gx == a.nn0 - 1) ||
+                  ((a.bcmask & 4) && gy == 0) || ((a.bcmask & 8) && gy == a.nn1 - 1);
+  const bool z0 = (a.bcmask & 16) && gzc == 0, z1 = (a.bcmask & 32) && gzc + K == a.nn2 - 1;
+  double u[N], v[N], w[N];
+  // ---- Z (x = ta, y = tb)
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    const bool m = lm || (l == 0 && z0) || (l == K && z1);
+    u[l] = m ? 0.0 : __ldg(a.x + base + l * zs);
+  }
+  mv<N>(T.val, u, v);
+  mv<N>(T.der, u, w);
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    F0[t + N2 * l] = v[l];
+    F1[t + N2 * l] = w[l];
+  }
+  __syncthreads();
+  // ---- Y (x = ta, z = tb)
+  {
+    double r1[N], r2[N], o[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      r1[l] = F0[ta + N * l + N2 * tb];
+      r2[l] = F1[ta + N * l + N2 * tb];
+    }
+    mv<N>(T.val, r1, o);
+#pragma unroll
+    for (int l = 0; l < N; ++l) F0[ta + N * l + N2 * tb] = o[l];
+    mv<N>(T.der, r1, o);
+#pragma unroll
+    for (int l = 0; l < N; ++l) F1[ta + N * l + N2 * tb] = o[l];
+    mv<N>(T.val, r2, o);
+#pragma unroll
+    for (int l = 0; l < N; ++l) F2[ta + N * l + N2 * tb] = o[l];
+  }
+  __syncthreads();
+  // ---- X (y = ta, z = tb): q-point (l, ta, tb); G entry (comp, l) at comp*N3 + l*N2 + t.
+  // Point by point: gradient, flux, and its contribution to the three transposed
+  // sweeps, so that only the inputs and the accumulators are live.
+  {
+    double ra[N], rb[N], rc[N], ea[N], eb[N], ec[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      ra[l] = F0[l + N * t];
+      rb[l] = F1[l + N * t];
+      rc[l] = F2[l + N * t];
+      ea[l] = eb[l] = ec[l] = 0.0;
+    }
+    const double* Gc = a.G + (active ? cell : 0) * 6 * N3 + t;
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      double gxl = 0.0, gyl = 0.0, gzl = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        gxl = fma(T.der[l][i], ra[i], gxl);
+        gyl = fma(T.val[l][i], rb[i], gyl);
+        gzl = fma(T.val[l][i], rc[i], gzl);
+      }
+      const double G00 = __ldg(Gc + 0 * N3 + l * N2), G01 = __ldg(Gc + 1 * N3 + l * N2);
+      const double G02 = __ldg(Gc + 2 * N3 + l * N2), G11 = __ldg(Gc + 3 * N3 + l * N2);
+      const double G12 = __ldg(Gc + 4 * N3 + l * N2), G22 = __ldg(Gc + 5 * N3 + l * N2);
+      double fx = G00 * gxl + G01 * gyl + G02 * gzl;
+      double fy = G01 * gxl + G11 * gyl + G12 * gzl;
+      double fz = G02 * gxl + G12 * gyl + G22 * gzl;
+      if (!active) fx = fy = fz = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        ea[i] = fma(T.der[l][i], fx, ea[i]);
+        eb[i] = fma(T.val[l][i], fy, eb[i]);
+        ec[i] = fma(T.val[l][i], fz, ec[i]);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      F0[l + N * t] = ea[l];
+      F1[l + N * t] = eb[l];
+      F2[l + N * t] = ec[l];
+    }
+  }
+  __syncthreads();
+  // ---- Y (x = ta, z = tb): h1 = N_y^T e1 + N'_y^T e2, h2 = N_y^T e3
+  {
+    double r1[N], r2[N], o[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      r1[l] = F0[ta + N * l + N2 * tb];
+      r2[l] = F1[ta + N * l + N2 * tb];
+    }
+    mvt<N>(T.val, r1, o);
+    mvt_add<N>(T.der, r2, o);
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      r1[l] = F2[ta + N * l + N2 * tb];
+      F0[ta + N * l + N2 * tb] = o[l];
+    }
+    mvt<N>(T.val, r1, o);
+#pragma unroll
+    for (int l = 0; l < N; ++l) F1[ta + N * l + N2 * tb] = o[l];
+  }
+  __syncthreads();
+  // ---- Z (x = ta, y = tb): v = N_z^T h1 + N'_z^T h2, scatter-add
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    u[l] = F0[t + N2 * l];
+    w[l] = F1[t + N2 * l];
+  }
+  mvt<N>(T.val, u, v);
+  mvt_add<N>(T.der, w, v);
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    const bool m = lm || (l == 0 && z0) || (l == K && z1);
+    if (!m) atomicAdd(a.y + base + l * zs, v[l]);
+  }
+}
 
+
+// ---------------------------------------------------------------- plane kernel (K1p, K <= 4)
+// Same operator as cg_apply_kernel (eq:mf_eval with G_q = w det J J^-1 J^-T), with a
+// thread layout that halves the shared-memory traffic of the line kernel (the
+// bottleneck ncu shows for it, profiles/r01b_summary.json): a cell is handled by
+// N = k+1 threads, each owning a whole 2-D plane of the cell in registers, so two of
+// the three directions are swept in-thread:
+//   layout A: thread p owns the xz-plane y = p   (z- and x-sweeps in registers)
+//   layout B: thread p owns the xy-plane z = p   (y- and x-sweeps in registers)
+// Forward: z-sweeps N_z u and N'_z u (derivative of the basis at the Gauss points, so
+// d/dz needs no collocation pass in layout A), x-interpolation of both, transpose
+// A->B (2 fields), y-interpolation (and N'_y) -> u_q, d_y u_q and d_z u_q; d_x by
+// Gauss-point collocation in-thread.  Quadrature point: f = G_q grad u, with G read from the
+// plane-layout table (coalesced; the block's slice is bulk-prefetched into L2 at
+// kernel start).  Backward: d_x^T f_x per row, N_y^T of it plus N'_y^T f_y, N_y^T f_z,
+// transpose B->A (2 fields), N_x^T, then N_z^T (.) + N'_z^T (.) and the
+// scatter-add.  Transposes go through shared memory with padded strides (plane stride
+// LS, cell stride CS) chosen so that every 16-lane phase of a warp hits 16 distinct
+// banks in both layouts.
+template <int N> struct PlanePad;
+#ifndef FEM_PLANE_MINB
+#define FEM_PLANE_MINB 2
+#endif
+template <> struct PlanePad<2> { static constexpr int LS = 4, CS = 17, MINB = 4; };
+template <> struct PlanePad<3> { static constexpr int LS = 19, CS = 121, MINB = 3; };
+template <> struct PlanePad<4> { static constexpr int LS = 20, CS = 161, MINB = 2; };
+template <> struct PlanePad<5> { static constexpr int LS = 25, CS = 253, MINB = FEM_PLANE_MINB; };  // 2-way conflicts in places, 2 KB/cell
+
+template <int K, bool DEFORMED>
+__global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
+    cg_plane_kernel(OpArgs a, Tab<K + 1> T) {
+  constexpr int N = K + 1, N2 = N * N, CB = kGroupCells;
+  constexpr int LS = PlanePad<N>::LS, CS = PlanePad<N>::CS;
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x;
+  const int p = tid % N, c = tid / N;
+  const int64_t group = blockIdx.x;
+  const int64_t cell = group * CB + c;
+  const bool active = cell < a.n_cells;
+  if (DEFORMED && tid == 0) {
+    // the group's geometry slice is contiguous in the plane layout: start pulling it
+    // into L2 now, it is consumed after the gather and the forward sweeps
+    const char* src = reinterpret_cast<const char*>(a.G + group * (int64_t)CB * 6 * N * N2);
+    const uint32_t total = (uint32_t)(sizeof(double) * CB * 6 * N * N2);
+    for (uint32_t off = 0; off < total; off += 32768u)
+      bulk_prefetch_l2(src + off, total - off < 32768u ? total - off : 32768u);
+  }
+  int cx = 0, cy = 0, cz = 0;
+  if (active) {
+    cx = (int)(cell % a.n0);
+    const int64_t r = cell / a.n0;
+    cy = (int)(r % a.n1);
+    cz = (int)(r / a.n1);
+  }
+  double* S0 = smem + c * CS;
+  double* S1 = S0 + N * LS;
+  const int64_t zs = (int64_t)a.nn0 * a.nn1;
+  const int gx0 = K * cx, gy = K * cy + p;
+  const int64_t base = gx0 + (int64_t)a.nn0 * gy + zs * (int64_t)(K * cz);
+  // Dirichlet constraints of the thread's plane (reading R5) as five flags, so that
+  // element (l, i) is constrained iff ym || (i==0 && x0) || (i==K && x1) || (l==0 && z0)
+  // || (l==K && z1) -- compile-time selections once i, l are unrolled
+  const int gzc = a.gz0 + K * cz;
+  const bool ym = ((a.bcmask & 4) && gy == 0) || ((a.bcmask & 8) && gy == a.nn1 - 1) || !active;
+  const bool x0 = (a.bcmask & 1) && gx0 == 0, x1 = (a.bcmask & 2) && gx0 + K == a.nn0 - 1;
+  const bool z0 = (a.bcmask & 16) && gzc == 0, z1 = (a.bcmask & 32) && gzc + K == a.nn2 - 1;
+  auto masked = [&](int l, int i) {
+    return ym || (i == 0 && x0) || (i == K && x1) || (l == 0 && z0) || (l == K && z1);
+  };
+
+  // ---- layout A (thread p: y = p): gather row l = x(., p, l), interpolate in x
+  double X[N][N];                       // [l][qx]
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    double u[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) u[i] = masked(l, i) ? 0.0 : __ldg(a.x + base + i + l * zs);
+    mv<N>(T.val, u, X[l]);
+  }
+  // z: N_z and N'_z per column qx, straight into shared memory
+  // (element (qz, y=p, qx) at qz*LS + p*N + qx)
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        s1 = fma(T.val[q][l], X[l][i], s1);
+        s2 = fma(T.der[q][l], X[l][i], s2);
+      }
+      S0[q * LS + p * N + i] = s1;
+      S1[q * LS + p * N + i] = s2;
+    }
+  }
+  __syncthreads();
+  // ---- layout B (thread p: qz = p).  Only the thread's own plane of S0/S1 is touched
+  // until the next barrier.  u_q goes back into S0 (column by column, in place), d_y u_q
+  // and d_z u_q stay in registers (Y, Z); the q-point phase runs row by row, reading a
+  // row of u_q and writing back the row's d_x^T f_x in its place.
+  double Y[N][N], Z[N][N];   // [qy][qx]: d_y u_q -> f_y, d_z u_q -> f_z
+#pragma unroll
+  for (int i = 0; i < N; ++i) {         // column qx = i
+    double r1[N], r2[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      r1[j] = S0[p * LS + j * N + i];
+      r2[j] = S1[p * LS + j * N + i];
+    }
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy) {
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        s1 = fma(T.val[qy][j], r1[j], s1);
+        s2 = fma(T.der[qy][j], r1[j], s2);
+        s3 = fma(T.val[qy][j], r2[j], s3);
+      }
+      S0[p * LS + qy * N + i] = s1;
+      Y[qy][i] = s2;
+      Z[qy][i] = s3;
+    }
+  }
+  const double* Gq = DEFORMED ? a.G + group * (int64_t)CB * 6 * N * N2 + tid : nullptr;
+#pragma unroll
+  for (int qy = 0; qy < N; ++qy) {
+    double ur[N], fxr[N], acc[N];
+#pragma unroll
+    for (int m = 0; m < N; ++m) ur[m] = S0[p * LS + qy * N + m];
+#pragma unroll
+    for (int qx = 0; qx < N; ++qx) {
+      double gxq = 0.0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) gxq = fma(T.colloc[qx][m], ur[m], gxq);
+      const double gyq = Y[qy][qx], gzq = Z[qy][qx];
+      double fx, fy, fz;
+      if (DEFORMED) {
+        const int e = qx + N * qy;
+        // entry (comp, e) of this thread: ((comp*N2 + e)*CB + c)*N + p = (comp*N2 + e)*CB*N + tid
+        const double G00 = __ldg(Gq + (0 * N2 + e) * CB * N), G01 = __ldg(Gq + (1 * N2 + e) * CB * N);
+        const double G02 = __ldg(Gq + (2 * N2 + e) * CB * N), G11 = __ldg(Gq + (3 * N2 + e) * CB * N);
+        const double G12 = __ldg(Gq + (4 * N2 + e) * CB * N), G22 = __ldg(Gq + (5 * N2 + e) * CB * N);
+        fx = G00 * gxq + G01 * gyq + G02 * gzq;
+        fy = G01 * gxq + G11 * gyq + G12 * gzq;
+        fz = G02 * gxq + G12 * gyq + G22 * gzq;
+        if (!active) fx = fy = fz = 0.0;
+      } else {
+        const double w3 = T.w[qx] * T.w[qy] * T.w[p];
+        fx = a.c0 * w3 * gxq;
+        fy = a.c1 * w3 * gyq;
+        fz = a.c2 * w3 * gzq;
+      }
+      fxr[qx] = fx;
+      Y[qy][qx] = fy;
+      Z[qy][qx] = fz;
+    }
+    mvt<N>(T.colloc, fxr, acc);
+#pragma unroll
+    for (int m = 0; m < N; ++m) S0[p * LS + qy * N + m] = acc[m];
+  }
+  // N_y^T (d_x^T f_x) + N'_y^T f_y -> S0 and N_y^T f_z -> S1, column by column in place
+  // (element (qz=p, y, qx) at p*LS + y*N + qx)
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double ac[N];
+#pragma unroll
+    for (int qy = 0; qy < N; ++qy) ac[qy] = S0[p * LS + qy * N + i];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int qy = 0; qy < N; ++qy) {
+        s1 = fma(T.val[qy][j], ac[qy], s1);
+        s1 = fma(T.der[qy][j], Y[qy][i], s1);
+        s2 = fma(T.val[qy][j], Z[qy][i], s2);
+      }
+      S0[p * LS + j * N + i] = s1;
+      S1[p * LS + j * N + i] = s2;
+    }
+  }
+  __syncthreads();
+  // ---- layout A (thread p: y = p): per column qx, N_z^T a + N'_z^T b, then N_x^T
+  // accumulated over the columns into the nodal rows V[l][.]
+  double V[N][N];                       // [l][i]
+#pragma unroll
+  for (int l = 0; l < N; ++l)
+#pragma unroll
+    for (int i = 0; i < N; ++i) V[l][i] = 0.0;
+#pragma unroll
+  for (int qx = 0; qx < N; ++qx) {
+    double ca[N], cb[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      ca[q] = S0[q * LS + p * N + qx];
+      cb[q] = S1[q * LS + p * N + qx];
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        v = fma(T.val[q][l], ca[q], v);
+        v = fma(T.der[q][l], cb[q], v);
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) V[l][i] = fma(T.val[qx][i], v, V[l][i]);
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < N; ++l)
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (!masked(l, i)) atomicAdd(a.y + base + i + l * zs, V[l][i]);
+}
 
 // ---------------------------------------------------------------- Cartesian fast path (K1c)
 // On a Cartesian cell the (k+1)-point Gauss rule integrates the stiffness exactly,
@@ -116,7 +509,7 @@ struct KronTab {
 };
 
 template <int K>
-__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
+__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? 4 : 1)
     cg_cart_kernel(OpArgs a, KronTab<K + 1> T, int64_t cell0, int64_t cell_end) {
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
@@ -207,9 +600,11 @@ __global__ void cg_diag_kernel(OpArgs a, Tab<K + 1> T) {
         const double bz = T.val[q0][i0] * T.val[q1][i1] * T.der[q2][i2];
         if (DEFORMED) {
           const int q = q0 + N * (q1 + N * q2);
-          const double* Gc = a.G + (size_t)cell * 6 * N3 + q;
-          d += Gc[0] * bx * bx + Gc[3 * N3] * by * by + Gc[5 * N3] * bz * bz +
-               2.0 * (Gc[N3] * bx * by + Gc[2 * N3] * bx * bz + Gc[4 * N3] * by * bz);
+          const int pl = a.glayout;
+          d += a.G[g_index<N>(pl, cell, 0, q)] * bx * bx + a.G[g_index<N>(pl, cell, 3, q)] * by * by +
+               a.G[g_index<N>(pl, cell, 5, q)] * bz * bz +
+               2.0 * (a.G[g_index<N>(pl, cell, 1, q)] * bx * by + a.G[g_index<N>(pl, cell, 2, q)] * bx * bz +
+                      a.G[g_index<N>(pl, cell, 4, q)] * by * bz);
         } else {
           const double w3 = T.w[q0] * T.w[q1] * T.w[q2];
           d += w3 * (a.c0 * bx * bx + a.c1 * by * by + a.c2 * bz * bz);
@@ -228,7 +623,7 @@ __global__ void cg_diag_kernel(OpArgs a, Tab<K + 1> T) {
 // G_df = w det J (4 / (h_d h_f)) (delta_df - beta (g_d + g_f) + beta^2 |g|^2).
 template <int K>
 __global__ void geometry_kernel(MapArgs m, int n0, int n1, int64_t n_cells, Tab<K + 1> T,
-                                double* __restrict__ G, unsigned long long* __restrict__ err) {
+                                double* __restrict__ G, unsigned long long* __restrict__ err, int glayout) {
   constexpr int N = K + 1, N3 = N * N * N;
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= n_cells * N3) return;
@@ -251,7 +646,7 @@ __global__ void geometry_kernel(MapArgs m, int n0, int n1, int64_t n_cells, Tab<
   for (int c = 0; c < 6; ++c) {
     const int d = comp[c][0], f = comp[c][1];
     const double v = (d == f ? 1.0 : 0.0) - b * (p.g[d] + p.g[f]) + b * b * g2;
-    G[(size_t)cell * 6 * N3 + c * N3 + q] = w * (4.0 / (m.h[d] * m.h[f])) * v;
+    G[g_index<N>(glayout, cell, c, q)] = w * (4.0 / (m.h[d] * m.h[f])) * v;
   }
 }
 
@@ -341,6 +736,8 @@ OpArgs op_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
   a.nn1 = L.nn[1];
   a.nn2 = L.dist ? h->k * L.nzg + 1 : L.nn[2];
   a.gz0 = h->k * L.cz0;
+  a.glayout = L.glayout;
+  a.g_direct = h->g_direct ? 1 : 0;
   int mask = 0;
   for (int s = 0; s < 6; ++s)
     if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
@@ -400,14 +797,34 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
       check_launch("cg_cart_kernel");
     }
   } else if (L.cartesian) {
-    const size_t sm = sizeof(double) * 3 * N * N * N * C;
+    const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
     cg_apply_kernel<K, false><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
+  } else if (L.glayout == kGLayoutXLine) {
+    const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
+    static bool attr_d = false;
+    if (!attr_d) {
+      FEM_CUDA_TRY(cudaFuncSetAttribute(cg_dline_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      attr_d = true;
+    }
+    cg_dline_kernel<K><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
+  } else if (L.glayout == kGLayoutPlane) {
+    if constexpr (K <= 4) {
+      const size_t sm = sizeof(double) * PlanePad<N>::CS * kGroupCells;
+      static bool attr_p = false;
+      if (!attr_p) {
+        FEM_CUDA_TRY(cudaFuncSetAttribute(cg_plane_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sm));
+        attr_p = true;
+      }
+      const int64_t groups = (L.n_cells + kGroupCells - 1) / kGroupCells;
+      cg_plane_kernel<K, true><<<(unsigned)groups, N * kGroupCells, sm, h->stream>>>(a, T);
+    }
   } else {
-    const size_t sm = sizeof(double) * 9 * N * N * N * C;   // 3 work buffers + 6 G components
+    const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (h->g_direct ? 0 : 6 * N * N * N * C));
     static bool attr = false;
     if (!attr) {
-      FEM_CUDA_TRY(cudaFuncSetAttribute(cg_apply_kernel<K, true>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      FEM_CUDA_TRY(cudaFuncSetAttribute(cg_apply_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
       attr = true;
     }
     cg_apply_kernel<K, true><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
@@ -437,7 +854,7 @@ void geometry_k(fem_ctx* h, Level& L) {
   const Tab<N> T = make_tab<N>(h->tab);
   const int64_t tot = L.n_cells * N * N * N;
   geometry_kernel<K><<<(unsigned)((tot + 255) / 256), 256, 0, h->stream>>>(
-      map_args(h, L), L.n[0], L.n[1], L.n_cells, T, L.G, h->geom_err);
+      map_args(h, L), L.n[0], L.n[1], L.n_cells, T, L.G, h->geom_err, L.glayout);
   count_launch();
   check_launch("geometry_kernel");
 }

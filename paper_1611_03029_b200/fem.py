@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfem.so")
+LIB_PATH = os.environ.get("FEM_LIB", os.path.join(_HERE, "libfem.so"))   # FEM_LIB: experiment builds
 
 FEM_OK, FEM_NOT_CONVERGED = 0, 1
 ERRORS = {-1: "FEM_E_ARG", -2: "FEM_E_SIZE", -3: "FEM_E_GEOMETRY", -4: "FEM_E_BREAKDOWN",

@@ -41,6 +41,34 @@ def make(cells, k, eps=0.0, bc=(DIRICHLET,) * 6, **kw):
     return f.Fem(cells, k, f.FEM_CG, deform_eps=eps, bc=bc, **kw), Mesh(cells, k, eps=eps, bc=bc)
 
 
+@pytest.mark.parametrize("variant,k,cells", [
+    ("FEM_PLANE", 1, (5, 3, 4)), ("FEM_PLANE", 2, (3, 4, 5)), ("FEM_PLANE", 3, (9, 4, 3)),
+    ("FEM_PLANE", 4, (11, 5, 3)),                # > 32 cells: several groups + ragged tail
+    ("FEM_DBASIS", 1, (5, 3, 4)), ("FEM_DBASIS", 2, (3, 4, 5)), ("FEM_DBASIS", 4, (6, 4, 3)),
+    ("FEM_DBASIS", 6, (2, 3, 2)), ("FEM_DBASIS", 8, (2, 1, 2)),
+])
+def test_alternative_deformed_kernels_match_oracle(variant, k, cells, monkeypatch):
+    """The plane kernel (K1p) and the derivative-basis line kernel (K1d) are
+    selectable at fem_setup (env); same operator, geometry table and diagonal."""
+    monkeypatch.setenv(variant, "1")
+    F, m = make(cells, k, 0.05, MIXED)
+    x = fem_inputs.uniform_pm1(3, m.cg_n_dofs())
+    y = np.zeros_like(x)
+    F.fem_apply(x, y)
+    assert relmax(y, ocg.apply(m, x)) <= 1e-12
+    d = np.zeros_like(x)
+    F.fem_diagonal(d)
+    assert relmax(d, ocg.diagonal(m)) <= 1e-12
+    nq = (k + 1) ** 3
+    G = np.zeros(m.n_cells * 6 * nq)
+    F.fem_level_geometry(F.n_levels - 1, G)
+    Go = ocg.metric(m, np.arange(m.n_cells), ocg.CellQuadrature(k))
+    comp = [(0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2)]
+    Gr = np.stack([Go[:, :, a, b] for a, b in comp], axis=1).reshape(-1)
+    assert relmax(G, Gr) <= 1e-13
+    F.close()
+
+
 @pytest.mark.parametrize("k,cells,eps,bc", [
     (2, (8, 8, 8), 0.0, (DIRICHLET,) * 6),       # C1
     (1, (5, 3, 4), 0.05, MIXED),

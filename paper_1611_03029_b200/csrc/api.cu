@@ -859,6 +859,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_PLANE")) h->plane_kernel = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_G_DIRECT")) h->g_direct = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_DBASIS")) h->dbasis = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_STENCIL")) h->stencil = std::atoi(e) != 0;
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)
     FEM_CUDA_TRY(cudaMemset(h->red, 0, sizeof(double) * (16 * kRedBlocks + 16)));

@@ -161,6 +161,7 @@ struct fem_ctx {
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
   bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)
   bool g_direct = true;                // FEM_G_DIRECT=0: line kernel stages G by TMA into shared memory
+  bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels
   bool dbasis = false;                 // FEM_DBASIS=1: derivative-basis line kernel (measured slower, kept for study)
 };
 

@@ -581,6 +581,271 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? 4 
   }
 }
 
+
+// ---------------------------------------------------------------- global Kronecker stencil (K1s)
+// Cartesian CG levels (C4).  The element matrix is the Kronecker sum
+// K^e = c0 S(x)M(x)M + c1 M(x)S(x)M + c2 M(x)M(x)S, and on a tensor grid
+// of identical cells the assembled operator is the same Kronecker sum of the ASSEMBLED
+// 1-D matrices:  A = c0 M1_z M1_y S1_x + c1 M1_z S1_y M1_x + c2 S1_z M1_y M1_x
+// (the element set is the product of the 1-D element sets).  So
+//     y = M1_z Q + c2 S1_z P,   P = M1_y M1_x x~,   Q = M1_y (c0 S1_x x~) + S1_y (c1 M1_x x~),
+// x~ = x with the Dirichlet entries read as 0 (reading R5), and y_c = x_c afterwards.
+// It is applied without any scatter: a block owns a 2-D tile of output node columns
+// and marches through z.  Per input plane: the tile plus a k-node halo is loaded into
+// shared memory with cp.async (double-buffered, out-of-domain and constrained entries
+// zero-filled), x-sweeps (A = M1_x x~, B = S1_x x~) into shared memory, y-sweeps into
+// registers (P, Q), and the z-direction is accumulated element by element in
+// registers: with z-element ez, the k+1 planes ez k .. ez k + k contribute
+// Mref[r][r'] Q + c2 Sref[r][r'] P to the outputs ez k + r, the shared vertex plane
+// carries to the next element.  Every output is written exactly once (no atomics, no
+// zero fill, x read once from DRAM, y written once).
+// Banded 1-D rows in "slot" form: slot e owns the nodes e k + r, r = 0..k-1 (slot n
+// only its vertex r = 0); vertex rows add the right end of element e-1 and the left
+// end of element e, interior rows only element e.  With r a compile-time loop index,
+// every coefficient is uniform across the warp (constant bank) -- no divergence.
+template <int K>
+struct StencilCfg {
+  static constexpr int N = K + 1;
+  static constexpr int TEX = (64 + K - 1) / K;        // x slots per tile
+  static constexpr int TEY = 4;                       // y slots per tile
+  static constexpr int TX = TEX * K;                  // output x nodes per tile
+  static constexpr int THREADS = TX * TEY;            // one thread per (x node, y slot)
+  static constexpr int LROWS = (TEY + 1) * K + 1;     // loaded rows (y) incl. halo
+  static constexpr int LCOLS = (TEX + 1) * K + 1;     // loaded columns (x) incl. halo
+  static constexpr int LPAD = LCOLS | 1;              // odd row stride: rows hit distinct banks
+  static constexpr int TXP = TX + 1;                  // odd row stride of the A, B buffers
+  static constexpr int HROWS = (LROWS + 1) / 2;       // x-stage: one item = one slot, two rows
+  static constexpr int SMEM = 2 * LROWS * LPAD + 2 * LROWS * TXP;   // doubles
+};
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int W>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(W) : "memory"); }
+
+#ifndef FEM_STENCIL_MINB
+#define FEM_STENCIL_MINB 2
+#endif
+template <int K>
+__global__ void __launch_bounds__(StencilCfg<K>::THREADS, FEM_STENCIL_MINB)
+    cg_stencil_kernel(OpArgs a, KronTab<K + 1> T) {
+  using Cfg = StencilCfg<K>;
+  constexpr int TEX = Cfg::TEX, TEY = Cfg::TEY, TX = Cfg::TX, LR = Cfg::LROWS, LC = Cfg::LCOLS,
+                LP = Cfg::LPAD, TXP = Cfg::TXP, HR = Cfg::HROWS;
+  extern __shared__ double smem[];
+  double* X0 = smem;                    // two input buffers [LR][LP]
+  double* Ab = smem + 2 * LR * LP;      // A = M1_x x~ at [row][tile x] (row stride TXP)
+  double* Bb = Ab + LR * TXP;           // B = S1_x x~
+  const int tid = threadIdx.x;
+  const int e0 = blockIdx.x * TEX, f0 = blockIdx.y * TEY;   // first x / y slot of the tile
+  const int nx = a.n0, ny = a.n1, nzl = a.n2;                // cells
+  const int NX = a.nn0, NY = a.nn1;
+  const int gx0 = (e0 - 1) * K, gy0 = (f0 - 1) * K;        // global node of loaded (0,0)
+  const int64_t zs = (int64_t)NX * NY;
+  const bool cx0 = a.bcmask & 1, cx1 = a.bcmask & 2, cy0 = a.bcmask & 4, cy1 = a.bcmask & 8;
+  const bool cz0 = a.bcmask & 16, cz1 = a.bcmask & 32;
+
+  auto load_plane = [&](int pl, double* buf) {   // local z plane pl (global a.gz0 + pl)
+    const int gz = a.gz0 + pl;
+    const bool zmask = (cz0 && gz == 0) || (cz1 && gz == a.nn2 - 1);
+    const double* src = a.x + (int64_t)pl * zs;
+    for (int idx = tid; idx < LR * LC; idx += Cfg::THREADS) {
+      const int r = idx / LC, c = idx % LC;
+      const int gx = gx0 + c, gy = gy0 + r;
+      const bool in = gx >= 0 && gx < NX && gy >= 0 && gy < NY;
+      const bool m = zmask || (cx0 && gx == 0) || (cx1 && gx == NX - 1) || (cy0 && gy == 0) ||
+                     (cy1 && gy == NY - 1);
+      cp_async8(buf + r * LP + c, in ? src + gx + (int64_t)NX * gy : a.x, in && !m);
+    }
+    cp_async_commit();
+  };
+
+  // this thread's y-stage / z-stage nodes: x = gx0 + K + c (tile column c), y-slot s
+  const int c = tid % TX, s = tid / TX;
+  const int xs = e0 * K + c;                       // global x node
+  const int fy = f0 + s;                           // global y slot
+  const bool col_ok = xs < NX && fy <= ny;
+  // y-slot rows valid: r = 0 always (if fy <= ny), r >= 1 only if fy < ny
+  const double yhl = (fy >= 1) ? 1.0 : 0.0, yhr = (fy < ny) ? 1.0 : 0.0;   // elements fy-1, fy exist
+
+  double out[K][K + 1];      // z accumulators per y node r: out[r][rz]
+  double carry[K], Pv[K], Qv[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) carry[r] = Pv[r] = Qv[r] = 0.0;
+
+  // P, Q of one plane for the thread's K nodes (y rows fy K + r)
+  auto plane_pq = [&](int pl, double* buf, double (&P)[K], double (&Q)[K]) {
+    // x-stage: rows 0..LR-1, slots 0..TEX-1 of the tile: A, B at tile columns slot*K + r.
+    // One item = one slot and two rows (ILP), rows vary fastest across lanes (odd strides:
+    // no bank conflicts on the row reads and on the A/B writes).
+    for (int it = tid; it < HR * TEX; it += Cfg::THREADS) {
+      const int row0 = it % HR, sl = it / HR;
+      const int e = e0 + sl;                       // global x slot
+      const double xl = (e >= 1) ? 1.0 : 0.0, xr = (e < nx) ? 1.0 : 0.0;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int row = row0 + h2 * HR;
+        if (row >= LR) break;
+        const double* xrow = buf + row * LP + sl * K;   // loaded column of node (e-1) K
+        double v[2 * K + 1];
+#pragma unroll
+        for (int j = 0; j <= 2 * K; ++j) v[j] = xrow[j];
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          double am = 0.0, bs = 0.0;
+          if (r == 0) {
+            double aL = 0.0, bL = 0.0, aR = 0.0, bR = 0.0;
+#pragma unroll
+            for (int j = 0; j <= K; ++j) {
+              aL = fma(T.M[K][j], v[j], aL);
+              bL = fma(T.S[K][j], v[j], bL);
+              aR = fma(T.M[0][j], v[K + j], aR);
+              bR = fma(T.S[0][j], v[K + j], bR);
+            }
+            am = xl * aL + xr * aR;
+            bs = xl * bL + xr * bR;
+          } else {
+#pragma unroll
+            for (int j = 0; j <= K; ++j) {
+              am = fma(T.M[r][j], v[K + j], am);
+              bs = fma(T.S[r][j], v[K + j], bs);
+            }
+          }
+          Ab[row * TXP + sl * K + r] = am;
+          Bb[row * TXP + sl * K + r] = bs;
+        }
+      }
+    }
+    __syncthreads();
+    // y-stage: column c, rows s K .. s K + 2K (element fy-1: rows sK..sK+K, element fy: sK+K..sK+2K)
+    double av[2 * K + 1], bv[2 * K + 1];
+#pragma unroll
+    for (int j = 0; j <= 2 * K; ++j) {
+      av[j] = Ab[(s * K + j) * TXP + c];
+      bv[j] = Bb[(s * K + j) * TXP + c];
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      double p = 0.0, qm = 0.0, qs = 0.0;
+      if (r == 0) {
+        double pL = 0.0, pR = 0.0, mL = 0.0, mR = 0.0, sL = 0.0, sR = 0.0;
+#pragma unroll
+        for (int j = 0; j <= K; ++j) {
+          pL = fma(T.M[K][j], av[j], pL);
+          pR = fma(T.M[0][j], av[K + j], pR);
+          mL = fma(T.M[K][j], bv[j], mL);
+          mR = fma(T.M[0][j], bv[K + j], mR);
+          sL = fma(T.S[K][j], av[j], sL);
+          sR = fma(T.S[0][j], av[K + j], sR);
+        }
+        p = yhl * pL + yhr * pR;
+        qm = yhl * mL + yhr * mR;
+        qs = yhl * sL + yhr * sR;
+      } else {
+#pragma unroll
+        for (int j = 0; j <= K; ++j) {
+          p = fma(T.M[r][j], av[K + j], p);
+          qm = fma(T.M[r][j], bv[K + j], qm);
+          qs = fma(T.S[r][j], av[K + j], qs);
+        }
+      }
+      P[r] = p;
+      Q[r] = fma(a.c0, qm, a.c1 * qs);
+    }
+  };
+
+  auto write_plane = [&](int pl, const double (&v)[K]) {
+    if (!col_ok) return;
+    const int gz = a.gz0 + pl;
+    const bool zm = (cz0 && gz == 0) || (cz1 && gz == a.nn2 - 1);
+    const bool xm = (cx0 && xs == 0) || (cx1 && xs == NX - 1);
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int ys = fy * K + r;
+      if (r > 0 && fy >= ny) break;
+      const bool m = zm || xm || (cy0 && ys == 0) || (cy1 && ys == NY - 1);
+      const int64_t idx = xs + (int64_t)NX * ys + zs * pl;
+      a.y[idx] = m ? a.x[idx] : v[r];
+    }
+  };
+
+  // ---- march through z: planes 0 .. K nzl (local), element by element
+  const int nplanes = K * nzl + 1;
+  load_plane(0, X0);
+  int buf = 0;
+  for (int ez = 0; ez < nzl; ++ez) {
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+#pragma unroll
+      for (int rz = 0; rz <= K; ++rz) out[r][rz] = 0.0;
+      out[r][0] = carry[r];
+    }
+#pragma unroll
+    for (int rp = 0; rp <= K; ++rp) {
+      if (rp == 0 && ez > 0) continue;
+      const int pl = ez * K + rp;
+      if (pl + 1 < nplanes) {
+        load_plane(pl + 1, X0 + (buf ^ 1) * LR * LP);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      double P[K], Q[K];
+      plane_pq(pl, X0 + buf * LR * LP, P, Q);
+      buf ^= 1;
+      if (rp == 0) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          Pv[r] = P[r];
+          Qv[r] = Q[r];
+        }
+        continue;
+      }
+      // contributions of plane rp of element ez (and, at rp == 1, of its vertex plane 0)
+#pragma unroll
+      for (int rz = 0; rz <= K; ++rz) {
+        // coefficients for column rp (runtime) -- select from the tables with a switch-free
+        // loop: rp is in 1..K
+        const double mz = T.M[rz][rp], sz = T.S[rz][rp], m0 = T.M[rz][0], s0 = T.S[rz][0];
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          double o = out[r][rz];
+          o = fma(mz, Q[r], o);
+          o = fma(a.c2 * sz, P[r], o);
+          if (rp == 1) {
+            o = fma(m0, Qv[r], o);
+            o = fma(a.c2 * s0, Pv[r], o);
+          }
+          out[r][rz] = o;
+        }
+      }
+      if (rp == K) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          Pv[r] = P[r];
+          Qv[r] = Q[r];
+        }
+      }
+    }
+    // planes ez K + rz, rz = 0..K-1 are complete; rz = K carries to the next element
+#pragma unroll
+    for (int rz = 0; rz < K; ++rz) {
+      double v[K];
+#pragma unroll
+      for (int r = 0; r < K; ++r) v[r] = out[r][rz];
+      write_plane(ez * K + rz, v);
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) carry[r] = out[r][K];
+  }
+  write_plane(K * nzl, carry);
+}
+
 // ---------------------------------------------------------------- diagonal
 // d_i = sum_cells sum_q sum_ab G_ab(q) B_a(q,i) B_b(q,i),  B_a = d phi_i/d xi_a at q.
 template <int K, bool DEFORMED>
@@ -780,6 +1045,21 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
         KT.M[i][j] = m;
         KT.S[i][j] = s;
       }
+    if (!L.dist && h->stencil) {
+      using Cfg = StencilCfg<K>;
+      const size_t smb = sizeof(double) * Cfg::SMEM;
+      static bool attr_s = false;
+      if (!attr_s) {
+        FEM_CUDA_TRY(cudaFuncSetAttribute(cg_stencil_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smb));
+        attr_s = true;
+      }
+      const dim3 sg((unsigned)((L.n[0] + 1 + Cfg::TEX - 1) / Cfg::TEX), (unsigned)((L.n[1] + 1 + Cfg::TEY - 1) / Cfg::TEY));
+      cg_stencil_kernel<K><<<sg, Cfg::THREADS, smb, h->stream>>>(a, KT);
+      count_launch();
+      check_launch("cg_stencil_kernel");
+      return;
+    }
     const size_t sm = sizeof(double) * 2 * N * N * N * C;
     // z-chunks: zero the chunk's node planes (all but the bottom one, which the previous
     // chunk has accumulated into) right before its cells are applied, so that the

@@ -69,6 +69,22 @@ def test_alternative_deformed_kernels_match_oracle(variant, k, cells, monkeypatc
     F.close()
 
 
+@pytest.mark.parametrize("k,cells,bc", [
+    (1, (5, 3, 4), MIXED), (2, (8, 8, 8), (DIRICHLET,) * 6), (3, (7, 5, 3), MIXED),
+    (4, (37, 9, 3), (DIRICHLET,) * 6),           # several x and y tiles, ragged
+    (5, (3, 2, 3), MIXED), (8, (2, 1, 2), (DIRICHLET,) * 6),
+])
+def test_stencil_kernel_matches_oracle(k, cells, bc, monkeypatch):
+    """Atomic-free global Kronecker stencil (K1s, FEM_STENCIL=1) on Cartesian CG levels."""
+    monkeypatch.setenv("FEM_STENCIL", "1")
+    F, m = make(cells, k, 0.0, bc)
+    x = fem_inputs.uniform_pm1(5, m.cg_n_dofs())
+    y = np.zeros_like(x)
+    F.fem_apply(x, y)
+    assert relmax(y, ocg.apply(m, x)) <= 1e-12
+    F.close()
+
+
 @pytest.mark.parametrize("k,cells,eps,bc", [
     (2, (8, 8, 8), 0.0, (DIRICHLET,) * 6),       # C1
     (1, (5, 3, 4), 0.05, MIXED),

@@ -6,5 +6,5 @@ for V in $VARIANTS; do
   tag=$(echo $V | tr '=' '_')
   env $V python tools/ncu_apply.py $CFG 3 > gpurun_out/ncu_$tag.log 2>&1 && \
   env $V timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off -c 1 \
-    -k regex:'apply|cart|plane|dline|dg_' -o gpurun_out/${TAG:-v}_${CFG}_$tag -f python tools/ncu_apply.py $CFG 3 >> gpurun_out/ncu_$tag.log 2>&1
+    -k regex:'apply|cart|plane|dline|dg_|stencil' -o gpurun_out/${TAG:-v}_${CFG}_$tag -f python tools/ncu_apply.py $CFG 3 >> gpurun_out/ncu_$tag.log 2>&1
 done

@@ -193,7 +193,8 @@ void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool se
   if (is_cg(h)) {
     // the Cartesian fast path zeroes y itself, chunk by chunk (kernels_cg.cu)
     const bool tiled = L.cartesian && !h->general_path;
-    if (!tiled) launch_zero(h, y, L.n_store);
+    if (!tiled && !(y == L.t && L.t_zero)) launch_zero(h, y, L.n_store);
+    if (y == L.t) L.t_zero = false;
     prof_begin(h, finest);
     launch_cg_apply(h, L, x, y);
     prof_end(h, finest);
@@ -484,6 +485,8 @@ Captured capture(fem_ctx* h, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& e
     h->prof.cap = nullptr;
     g_capture_count = nullptr;
   };
+  // the graph must not rely on buffer state observed at capture time
+  for (auto& L : h->levels) L.t_zero = false;
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) {
@@ -860,6 +863,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_G_DIRECT")) h->g_direct = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_DBASIS")) h->dbasis = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_STENCIL")) h->stencil = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_PDL")) h->pdl = std::atoi(e) != 0;
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)
     FEM_CUDA_TRY(cudaMemset(h->red, 0, sizeof(double) * (16 * kRedBlocks + 16)));

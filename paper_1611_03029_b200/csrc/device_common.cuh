@@ -75,6 +75,16 @@ __device__ __forceinline__ void mvt_add(const double (&M)[N][N], const double (&
   }
 }
 
+// Programmatic dependent launch (launch_pdl, internal.h): wait for the predecessor
+// grid (no-op when launched without the attribute), then let the successor launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#define FEM_PDL_ENTRY() \
+  do {                  \
+    pdl_wait();         \
+    pdl_trigger();      \
+  } while (0)
+
 // Mesh map (reading R2): xhat = lo + h (c + (xi+1)/2), x = xhat + eps s(xhat) (1,1,1),
 // s = prod_e sin(pi t_e), t = (xhat - lo)/(hi - lo).
 struct MapArgs {

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <memory>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -98,6 +99,9 @@ struct Level {
   double lam = 0.0;
   // work vectors for the V-cycle (level >= 1 need all, level 0 needs b, x)
   double *b = nullptr, *x = nullptr, *x2 = nullptr, *x3 = nullptr, *t = nullptr, *b2 = nullptr;
+  // host-side knowledge that t is all zeros (the Chebyshev step clears the A x it
+  // consumes), so that the next CG apply into t needs no memset; reset at graph capture
+  mutable bool t_zero = false;
   // PCG vectors (finest level, allocated on first cg_solve)
   double *pcg_r = nullptr, *pcg_p = nullptr, *pcg_q = nullptr, *pcg_z = nullptr;
   double* halo = nullptr;        // CG dist: receive buffer of one node plane (compress-add)
@@ -161,6 +165,7 @@ struct fem_ctx {
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
   bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)
   bool g_direct = true;                // FEM_G_DIRECT=0: line kernel stages G by TMA into shared memory
+  bool pdl = true;                     // FEM_PDL=0: plain launches (no programmatic dependent launch)
   bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels
   bool dbasis = false;                 // FEM_DBASIS=1: derivative-basis line kernel (measured slower, kept for study)
 };
@@ -199,6 +204,28 @@ void launch_sub(fem_ctx* h, double* r, const double* b, const double* ax, int64_
 
 // level helpers
 inline bool is_cg(const fem_ctx* h) { return h->method == FEM_CG; }
+
+// Launch with programmatic dependent launch (PDL, sm_90+): the kernel may be scheduled
+// while its predecessor on the stream drains; it must begin with pdl_entry()
+// (device_common.cuh), which waits for the predecessor's completion and memory flush
+// before anything that reads its results.  Captured into the PCG graphs as
+// programmatic edges; it removes most of the launch gap between the many small
+// kernels of the coarse multigrid levels.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(fem_ctx* h, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = h->pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw Error{FEM_E_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e)};
+}
 
 // z-slab exchanges (api.cu); no-ops on replicated levels / single rank
 void halo_import(fem_ctx* h, const Level& L, double* v);      // ghosts <- neighbours' owned data

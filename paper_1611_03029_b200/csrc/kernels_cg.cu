@@ -47,6 +47,7 @@ __host__ __device__ constexpr int line_cell_stride() { return 3 * N * N * N + (N
 template <int K, bool DEFORMED>
 __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     cg_apply_kernel(OpArgs a, Tab<K + 1> T) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
   extern __shared__ double smem[];
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
 template <int K>
 __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FEM_DLINE_MINB : 1)
     cg_dline_kernel(OpArgs a, Tab<K + 1> T) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
   extern __shared__ double smem[];
@@ -306,6 +308,7 @@ template <> struct PlanePad<5> { static constexpr int LS = 25, CS = 253, MINB = 
 template <int K, bool DEFORMED>
 __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
     cg_plane_kernel(OpArgs a, Tab<K + 1> T) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, CB = kGroupCells;
   constexpr int LS = PlanePad<N>::LS, CS = PlanePad<N>::CS;
   extern __shared__ double smem[];
@@ -511,6 +514,7 @@ struct KronTab {
 template <int K>
 __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? 4 : 1)
     cg_cart_kernel(OpArgs a, KronTab<K + 1> T, int64_t cell0, int64_t cell_end) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
   extern __shared__ double smem[];
@@ -633,6 +637,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <int K>
 __global__ void __launch_bounds__(StencilCfg<K>::THREADS, FEM_STENCIL_MINB)
     cg_stencil_kernel(OpArgs a, KronTab<K + 1> T) {
+  FEM_PDL_ENTRY();
   using Cfg = StencilCfg<K>;
   constexpr int TEX = Cfg::TEX, TEY = Cfg::TEY, TX = Cfg::TX, LR = Cfg::LROWS, LC = Cfg::LCOLS,
                 LP = Cfg::LPAD, TXP = Cfg::TXP, HR = Cfg::HROWS;
@@ -850,6 +855,7 @@ __global__ void __launch_bounds__(StencilCfg<K>::THREADS, FEM_STENCIL_MINB)
 // d_i = sum_cells sum_q sum_ab G_ab(q) B_a(q,i) B_b(q,i),  B_a = d phi_i/d xi_a at q.
 template <int K, bool DEFORMED>
 __global__ void cg_diag_kernel(OpArgs a, Tab<K + 1> T) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N3 = N * N * N;
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= a.n_cells * N3) return;
@@ -889,6 +895,7 @@ __global__ void cg_diag_kernel(OpArgs a, Tab<K + 1> T) {
 template <int K>
 __global__ void geometry_kernel(MapArgs m, int n0, int n1, int64_t n_cells, Tab<K + 1> T,
                                 double* __restrict__ G, unsigned long long* __restrict__ err, int glayout) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N3 = N * N * N;
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= n_cells * N3) return;
@@ -920,6 +927,7 @@ __global__ void geometry_kernel(MapArgs m, int n0, int n1, int64_t n_cells, Tab<
 // One block per cell, (k+1)^3 threads.
 template <int K, bool DG>
 __global__ void rhs_kernel(MapArgs m, OpArgs a, Tab<K + 1> T) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N3 = N * N * N;
   __shared__ double fq[N3];
   const int64_t cell = blockIdx.x;
@@ -962,6 +970,7 @@ __global__ void rhs_kernel(MapArgs m, OpArgs a, Tab<K + 1> T) {
 // restricted to the rank's owned node planes [0, nzo) (global plane gz0 + local).
 __global__ void set_constrained_kernel(const double* __restrict__ x, double val, double* __restrict__ y,
                                        int nn0, int nn1, int nzo, int gz0, int nn2g, int bcmask) {
+  FEM_PDL_ENTRY();
   const int side = blockIdx.y;
   if (!(bcmask & (1 << side))) return;
   const int d = side / 2;
@@ -1055,7 +1064,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
         attr_s = true;
       }
       const dim3 sg((unsigned)((L.n[0] + 1 + Cfg::TEX - 1) / Cfg::TEX), (unsigned)((L.n[1] + 1 + Cfg::TEY - 1) / Cfg::TEY));
-      cg_stencil_kernel<K><<<sg, Cfg::THREADS, smb, h->stream>>>(a, KT);
+      launch_pdl(h, cg_stencil_kernel<K>, sg, Cfg::THREADS, smb, a, KT);
       count_launch();
       check_launch("cg_stencil_kernel");
       return;
@@ -1070,15 +1079,15 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
     for (int z0 = 0; z0 < L.n[2]; z0 += lz) {
       const int z1 = std::min(z0 + lz, L.n[2]);
       const int64_t p0 = z0 == 0 ? 0 : (int64_t)K * z0 + 1, p1 = (int64_t)K * z1 + 1;
-      FEM_CUDA_TRY(cudaMemsetAsync(y + p0 * plane, 0, sizeof(double) * (p1 - p0) * plane, h->stream));
+      launch_zero(h, y + p0 * plane, (p1 - p0) * plane);
       const int64_t c0 = layer * z0, c1 = layer * z1;
-      cg_cart_kernel<K><<<(unsigned)((c1 - c0 + C - 1) / C), block, sm, h->stream>>>(a, KT, c0, c1);
+      launch_pdl(h, cg_cart_kernel<K>, (unsigned)((c1 - c0 + C - 1) / C), block, sm, a, KT, c0, c1);
       count_launch();
       check_launch("cg_cart_kernel");
     }
   } else if (L.cartesian) {
     const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
-    cg_apply_kernel<K, false><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
+    launch_pdl(h, cg_apply_kernel<K, false>, (unsigned)grid, block, sm, a, T);
   } else if (L.glayout == kGLayoutXLine) {
     const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
     static bool attr_d = false;
@@ -1086,7 +1095,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
       FEM_CUDA_TRY(cudaFuncSetAttribute(cg_dline_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       attr_d = true;
     }
-    cg_dline_kernel<K><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
+    launch_pdl(h, cg_dline_kernel<K>, (unsigned)grid, block, sm, a, T);
   } else if (L.glayout == kGLayoutPlane) {
     if constexpr (K <= 4) {
       const size_t sm = sizeof(double) * PlanePad<N>::CS * kGroupCells;
@@ -1097,7 +1106,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
         attr_p = true;
       }
       const int64_t groups = (L.n_cells + kGroupCells - 1) / kGroupCells;
-      cg_plane_kernel<K, true><<<(unsigned)groups, N * kGroupCells, sm, h->stream>>>(a, T);
+      launch_pdl(h, cg_plane_kernel<K, true>, (unsigned)groups, N * kGroupCells, sm, a, T);
     }
   } else {
     const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (h->g_direct ? 0 : 6 * N * N * N * C));
@@ -1107,7 +1116,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
                                         (int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
       attr = true;
     }
-    cg_apply_kernel<K, true><<<(unsigned)grid, block, sm, h->stream>>>(a, T);
+    launch_pdl(h, cg_apply_kernel<K, true>, (unsigned)grid, block, sm, a, T);
   }
   count_launch();
   check_launch("cg_apply_kernel");
@@ -1186,7 +1195,7 @@ void set_constrained_impl(fem_ctx* h, const Level& L, const double* x, double v,
   int64_t mx = std::max<int64_t>((int64_t)L.nn[0] * L.nn[1],
                                  std::max<int64_t>((int64_t)L.nn[0] * nzo, (int64_t)L.nn[1] * nzo));
   dim3 grid((unsigned)((mx + 255) / 256), 6);
-  set_constrained_kernel<<<grid, 256, 0, h->stream>>>(x, v, y, L.nn[0], L.nn[1], nzo, a.gz0, a.nn2, a.bcmask);
+  launch_pdl(h, set_constrained_kernel, grid, 256, 0, x, v, y, L.nn[0], L.nn[1], nzo, a.gz0, a.nn2, a.bcmask);
   count_launch();
   check_launch("set_constrained_kernel");
 }

@@ -283,6 +283,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
 template <int K, bool DEFORMED>
 __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     dg_apply_kernel(DgArgs A, Tab<K + 1> T) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = DgCPB<K>::value;
   using L = DgSmem<N>;
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
 //   interior sum_q JxW (-phi d_n phi + sigma phi^2), Dirichlet sum_q JxW (-2 phi d_n phi + 2 sigma phi^2).
 template <int K, bool DEFORMED>
 __global__ void dg_diag_kernel(DgArgs A, Tab<K + 1> T) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= A.n_cells * N3) return;
@@ -401,6 +403,7 @@ __global__ void dg_diag_kernel(DgArgs A, Tab<K + 1> T) {
 // the physical point, normal and JxW because the map is continuous (reading R2).
 template <int K>
 __global__ void dg_face_geometry_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double* faceq) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N;
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = A.face_off[2] + (int64_t)(A.n[2] + 1) * A.n[0] * A.n[1];
@@ -455,6 +458,7 @@ __global__ void dg_face_geometry_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, doubl
 // vol[(cz + 1) n0 n1 + cy n0 + cx], cz in [-1, n2]
 template <int K>
 __global__ void dg_cell_volume_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double* vol) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1;
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= (int64_t)A.n[0] * A.n[1] * (A.n[2] + 2)) return;
@@ -473,6 +477,7 @@ __global__ void dg_cell_volume_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double*
 template <int K>
 __global__ void dg_face_sigma_kernel(DgArgs A, double pen, const double* faceq, const double* vol,
                                      double* fsigma) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N;
   const int64_t fr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = A.face_off[2] + (int64_t)(A.n[2] + 1) * A.n[0] * A.n[1];
@@ -564,7 +569,7 @@ void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y) {
     attr = true;
   }
   const unsigned grid = (unsigned)((L.n_cells + C - 1) / C);
-  dg_apply_kernel<K, DEF><<<grid, dim3(N * N, C), sm, h->stream>>>(dg_args(h, L, x, y), make_tab<N>(h->tab));
+  launch_pdl(h, dg_apply_kernel<K, DEF>, grid, dim3(N * N, C), sm, dg_args(h, L, x, y), make_tab<N>(h->tab));
   count_launch();
   check_launch("dg_apply_kernel");
 }

@@ -40,6 +40,7 @@ __device__ __forceinline__ int64_t cg_index(int gx, int gy, int gz, int nn0, int
 template <int K, bool DG>
 __global__ void prolongate_kernel(TransferArgs a, Embed<K, DG> E, const double* __restrict__ xc,
                                   double* __restrict__ xf) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, M = Embed<K, DG>::M;
   extern __shared__ double smem[];
   double* s_in = smem;               // N^3
@@ -106,6 +107,7 @@ __global__ void prolongate_kernel(TransferArgs a, Embed<K, DG> E, const double* 
 template <int K, bool DG>
 __global__ void restrict_kernel(TransferArgs a, Embed<K, DG> E, const double* __restrict__ bf,
                                 const double* __restrict__ axf, double* __restrict__ xc) {
+  FEM_PDL_ENTRY();
   constexpr int N = K + 1, M = Embed<K, DG>::M;
   extern __shared__ double smem[];
   double* s_in = smem;               // M^3
@@ -170,24 +172,42 @@ __global__ void restrict_kernel(TransferArgs a, Embed<K, DG> E, const double* __
 __global__ void cheb_step_kernel(double* __restrict__ xn, const double* __restrict__ x,
                                  const double* __restrict__ xo, const double* __restrict__ b,
                                  double* __restrict__ ax, const double* __restrict__ dinv, double c1,
-                                 double c2, int64_t n) {
+                                 double c2, int64_t n, bool clear_ax) {
+  FEM_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double xi = x ? x[i] : 0.0;
     const double xoi = xo ? xo[i] : 0.0;
     const double r = b[i] - (ax ? ax[i] : 0.0);
     xn[i] = xi + c1 * (xi - xoi) + c2 * dinv[i] * r;
+    if (clear_ax) ax[i] = 0.0;
   }
 }
 
 __global__ void axpby_kernel(double* __restrict__ y, const double* __restrict__ x, double a, double b,
                              int64_t n) {
+  FEM_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = a * x[i] + b * y[i];
 }
 
+__global__ void fill_kernel(double* __restrict__ y, double v, int64_t n) {
+  FEM_PDL_ENTRY();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = v;
+}
+
+__global__ void copy_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+  FEM_PDL_ENTRY();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+
 __global__ void add_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+  FEM_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] += x[i];
@@ -195,12 +215,14 @@ __global__ void add_kernel(double* __restrict__ y, const double* __restrict__ x,
 
 __global__ void sub_kernel(double* __restrict__ r, const double* __restrict__ b,
                            const double* __restrict__ ax, int64_t n) {
+  FEM_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     r[i] = b[i] - (ax ? ax[i] : 0.0);
 }
 
 __global__ void dinv_kernel(const double* __restrict__ d, double* __restrict__ di, int64_t n) {
+  FEM_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     di[i] = 1.0 / d[i];
@@ -215,6 +237,7 @@ __device__ __forceinline__ double u01_splitmix(uint64_t seed, uint64_t i) {
 }
 
 __global__ void splitmix_kernel(double* __restrict__ s, uint64_t seed, int64_t first, int64_t n) {
+  FEM_PDL_ENTRY();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     s[i] = u01_splitmix(seed, (uint64_t)(first + i));
@@ -261,6 +284,7 @@ __device__ __forceinline__ void finish_reduction(double part, double* red, doubl
 
 __global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
                            double* red, double* out, int slot, unsigned int* counters) {
+  FEM_PDL_ENTRY();
   __shared__ double sh[32];
   double v = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -274,6 +298,7 @@ __global__ void dot_kernel(const double* __restrict__ a, const double* __restric
 __global__ void pcg_update_xr_kernel(double* __restrict__ x, double* __restrict__ r,
                                      const double* __restrict__ p, const double* __restrict__ q,
                                      int64_t n, double* red, double* scal, unsigned int* counters) {
+  FEM_PDL_ENTRY();
   __shared__ double sh[32];
   const double alpha = scal[0] / scal[1];
   double v = 0.0;
@@ -291,20 +316,24 @@ __global__ void pcg_update_xr_kernel(double* __restrict__ x, double* __restrict_
 // beta = scal[3]/scal[0] (rz_new / rz);  p = z + beta p
 __global__ void pcg_update_p_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
                                     const double* scal) {
+  FEM_PDL_ENTRY();
   const double beta = scal[3] / scal[0];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = fma(beta, p[i], z[i]);
 }
 
-__global__ void copy_scalar_kernel(double* scal, int dst, int src) { scal[dst] = scal[src]; }
+__global__ void copy_scalar_kernel(double* scal, int dst, int src) {
+  FEM_PDL_ENTRY(); scal[dst] = scal[src]; }
 
-__global__ void set_scalar_kernel(double* scal, int idx, double v) { scal[idx] = v; }
+__global__ void set_scalar_kernel(double* scal, int idx, double v) {
+  FEM_PDL_ENTRY(); scal[idx] = v; }
 
 // x = A0^{-1} b on the free DoFs (dense inverse from the Cholesky factor); x = 0 elsewhere.
 __global__ void coarse_solve_kernel(const double* __restrict__ Ainv, const int* __restrict__ free_idx,
                                     int nf, const double* __restrict__ b, double* __restrict__ x,
                                     int64_t n) {
+  FEM_PDL_ENTRY();
   extern __shared__ double sb[];
   for (int i = threadIdx.x; i < nf; i += blockDim.x) sb[i] = b[free_idx[i]];
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = 0.0;
@@ -363,7 +392,7 @@ void prolongate_kd(fem_ctx* h, const Level& c, const Level& f, const double* xc,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr = true;
   }
-  prolongate_kernel<K, DG><<<(unsigned)c.n_cells, 128, sm, h->stream>>>(
+  launch_pdl(h, prolongate_kernel<K, DG>, (unsigned)c.n_cells, 128, sm, 
       transfer_args(h, c, f), make_embed<K, DG>(h->tab), xc, xf);
   count_launch();
   check_launch("prolongate_kernel");
@@ -380,7 +409,7 @@ void restrict_kd(fem_ctx* h, const Level& c, const Level& f, const double* bf, c
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr = true;
   }
-  restrict_kernel<K, DG><<<(unsigned)c.n_cells, 128, sm, h->stream>>>(
+  launch_pdl(h, restrict_kernel<K, DG>, (unsigned)c.n_cells, 128, sm, 
       transfer_args(h, c, f), make_embed<K, DG>(h->tab), bf, axf, xc);
   count_launch();
   check_launch("restrict_kernel");
@@ -424,43 +453,55 @@ void launch_restrict(fem_ctx* h, const Level& c, const Level& f, const double* b
   FEM_DISPATCH_K(h->k, restrict_k, h, c, f, bf, axf, xc);
 }
 
+// zero / copy as kernels (not memset/memcpy graph nodes) so that the PDL chain of the
+// solve is not broken
 void launch_zero(fem_ctx* h, double* p, int64_t n) {
-  FEM_CUDA_TRY(cudaMemsetAsync(p, 0, sizeof(double) * n, h->stream));
+  if (n <= 0) return;
+  launch_pdl(h, fill_kernel, vec_grid(n), 256, 0, p, 0.0, n);
+  count_launch();
+  check_launch("fill_kernel");
 }
 
 void launch_copy(fem_ctx* h, double* dst, const double* src, int64_t n) {
-  FEM_CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, h->stream));
+  if (n <= 0) return;
+  launch_pdl(h, copy_kernel, vec_grid(n), 256, 0, dst, src, n);
+  count_launch();
+  check_launch("copy_kernel");
 }
 
 void launch_dinv(fem_ctx* h, Level& L) {
-  dinv_kernel<<<vec_grid(L.n_dofs), 256, 0, h->stream>>>(L.diag, L.dinv, L.n_dofs);
+  launch_pdl(h, dinv_kernel, vec_grid(L.n_dofs), 256, 0, L.diag, L.dinv, L.n_dofs);
   count_launch();
   check_launch("dinv_kernel");
 }
 
 void launch_splitmix(fem_ctx* h, const Level& L, uint64_t seed, double* s) {
-  splitmix_kernel<<<vec_grid(L.n_dofs), 256, 0, h->stream>>>(s, seed, L.first_global, L.n_dofs);
+  launch_pdl(h, splitmix_kernel, vec_grid(L.n_dofs), 256, 0, s, seed, L.first_global, L.n_dofs);
   count_launch();
   check_launch("splitmix_kernel");
 }
 
 void launch_cheb_step(fem_ctx* h, const Level& L, double* xn, const double* x, const double* xo,
                       const double* b, double* ax, double c1, double c2, bool has_xo) {
-  cheb_step_kernel<<<vec_grid(L.n_dofs), 256, 0, h->stream>>>(xn, x, has_xo ? xo : nullptr, b, ax,
-                                                              L.dinv, c1, c2, L.n_dofs);
+  // CG, single-slab level: clear the consumed A x so that the next apply into L.t needs
+  // no memset (the owned block is the whole storage)
+  const bool clear = ax != nullptr && ax == L.t && h->method == FEM_CG && !L.dist;
+  launch_pdl(h, cheb_step_kernel, vec_grid(L.n_dofs), 256, 0, xn, x, has_xo ? xo : nullptr, b, ax,
+                                                              L.dinv, c1, c2, L.n_dofs, clear);
+  if (clear) L.t_zero = true;
   count_launch();
   check_launch("cheb_step_kernel");
 }
 
 void launch_dot(fem_ctx* h, const double* a, const double* b, int64_t n, int slot) {
-  dot_kernel<<<kRedBlocks, kRedThreads, 0, h->stream>>>(a, b, n, h->red + slot * kRedBlocks, h->scal,
+  launch_pdl(h, dot_kernel, kRedBlocks, kRedThreads, 0, a, b, n, h->red + slot * kRedBlocks, h->scal,
                                                         slot, (unsigned int*)(h->red + 16 * kRedBlocks));
   count_launch();
   check_launch("dot_kernel");
 }
 
 void launch_pcg_update_xr(fem_ctx* h, double* x, double* r, const double* p, double* q, int64_t n) {
-  pcg_update_xr_kernel<<<kRedBlocks, kRedThreads, 0, h->stream>>>(x, r, p, q, n,
+  launch_pdl(h, pcg_update_xr_kernel, kRedBlocks, kRedThreads, 0, x, r, p, q, n,
                                                                   h->red + 2 * kRedBlocks, h->scal,
                                                                   (unsigned int*)(h->red + 16 * kRedBlocks));
   count_launch();
@@ -468,43 +509,43 @@ void launch_pcg_update_xr(fem_ctx* h, double* x, double* r, const double* p, dou
 }
 
 void launch_pcg_update_p(fem_ctx* h, double* p, const double* z, int64_t n) {
-  pcg_update_p_kernel<<<vec_grid(n), 256, 0, h->stream>>>(p, z, n, h->scal);
+  launch_pdl(h, pcg_update_p_kernel, vec_grid(n), 256, 0, p, z, n, h->scal);
   count_launch();
   check_launch("pcg_update_p_kernel");
-  copy_scalar_kernel<<<1, 1, 0, h->stream>>>(h->scal, 0, 3);
+  launch_pdl(h, copy_scalar_kernel, 1, 1, 0, h->scal, 0, 3);
   count_launch();
   check_launch("copy_scalar_kernel");
 }
 
 void launch_set_scalar(fem_ctx* h, int idx, double v) {
-  set_scalar_kernel<<<1, 1, 0, h->stream>>>(h->scal, idx, v);
+  launch_pdl(h, set_scalar_kernel, 1, 1, 0, h->scal, idx, v);
   count_launch();
   check_launch("set_scalar_kernel");
 }
 
 void launch_coarse_solve(fem_ctx* h, const double* b, double* x) {
   const Level& L0 = h->levels[0];
-  coarse_solve_kernel<<<1, 512, sizeof(double) * h->n_coarse_free, h->stream>>>(
+  launch_pdl(h, coarse_solve_kernel, 1, 512, sizeof(double) * h->n_coarse_free, 
       h->coarse_inv, h->coarse_free, h->n_coarse_free, b, x, L0.n_dofs);
   count_launch();
   check_launch("coarse_solve_kernel");
 }
 
 void launch_axpby(fem_ctx* h, double* y, const double* x, double a, double b, int64_t n) {
-  axpby_kernel<<<vec_grid(n), 256, 0, h->stream>>>(y, x, a, b, n);
+  launch_pdl(h, axpby_kernel, vec_grid(n), 256, 0, y, x, a, b, n);
   count_launch();
   check_launch("axpby_kernel");
 }
 
 void launch_add(fem_ctx* h, double* y, const double* x, int64_t n) {
   if (n <= 0) return;
-  add_kernel<<<vec_grid(n), 256, 0, h->stream>>>(y, x, n);
+  launch_pdl(h, add_kernel, vec_grid(n), 256, 0, y, x, n);
   count_launch();
   check_launch("add_kernel");
 }
 
 void launch_sub(fem_ctx* h, double* r, const double* b, const double* ax, int64_t n) {
-  sub_kernel<<<vec_grid(n), 256, 0, h->stream>>>(r, b, ax, n);
+  launch_pdl(h, sub_kernel, vec_grid(n), 256, 0, r, b, ax, n);
   count_launch();
   check_launch("sub_kernel");
 }

@@ -10,6 +10,7 @@
 #include <array>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -864,6 +865,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_DBASIS")) h->dbasis = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_STENCIL")) h->stencil = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_PDL")) h->pdl = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_DG_KRON")) h->dg_kron = std::atoi(e) != 0;
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)
     FEM_CUDA_TRY(cudaMemset(h->red, 0, sizeof(double) * (16 * kRedBlocks + 16)));
@@ -1213,6 +1215,9 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
         h->sg.k_upd = cu.kernels;
         h->sg.b = db;
         h->sg.x = dx;
+        if (std::getenv("FEM_DEBUG"))
+          std::fprintf(stderr, "libfem: PCG graphs captured: %lld + %lld kernels per iteration\n",
+                       (long long)h->sg.k_pre, (long long)h->sg.k_upd);
       }
       // first iteration through the same code: p = 0 and s0 = 1 make p = z + 0
       launch_zero(h, p, n);

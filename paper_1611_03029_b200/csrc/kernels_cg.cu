@@ -20,9 +20,12 @@
 namespace fem {
 
 template <int K>
+#ifndef FEM_CPB4
+#define FEM_CPB4 8
+#endif
 struct CPB {  // cells per block: about 128-200 threads per block
   static constexpr int N = K + 1;
-  static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? 8 : (N * N <= 49) ? 4 : 2;
+  static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? FEM_CPB4 : (N * N <= 49) ? 4 : 2;
 };
 
 struct OpArgs {
@@ -44,14 +47,25 @@ struct OpArgs {
 template <int N>
 __host__ __device__ constexpr int line_cell_stride() { return 3 * N * N * N + (N == 5 ? 2 : 0); }
 
+// threads per cell of the line kernel: (k+1)^2, or a whole warp per cell at Q4
+// (FEM_WARP_CELL=1: lanes 25..31 shadow lanes 0..6 -- same addresses, same values --
+// so that no cell straddles a warp; only the real lanes scatter)
+#ifndef FEM_WARP_CELL
+#define FEM_WARP_CELL 0
+#endif
+template <int K>
+__host__ __device__ constexpr int line_tpc() { return (K == 4 && FEM_WARP_CELL) ? 32 : (K + 1) * (K + 1); }
+
 template <int K, bool DEFORMED>
-__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
+__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value)
     cg_apply_kernel(OpArgs a, Tab<K + 1> T) {
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
   extern __shared__ double smem[];
-  const int t = threadIdx.x;
+  const int traw = threadIdx.x;
+  const int t = traw < N2 ? traw : traw - N2;
+  const bool real = traw < N2;
   const int ci = threadIdx.y;
   const int64_t cell = (int64_t)blockIdx.x * C + ci;
   const bool active = cell < a.n_cells;
@@ -83,7 +97,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
     // G read straight from global memory in the q-point phase (each warp load is 256
     // contiguous bytes: q = t + N^2 l); the block's slice is bulk-prefetched into L2 now
     const int64_t c0 = (int64_t)blockIdx.x * C;
-    if (t == 0 && ci == 0) {
+    if (traw == 0 && ci == 0) {
       const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
       bulk_prefetch_l2(a.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
     }
@@ -91,7 +105,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
   } else if (DEFORMED) {
     double* sG = smem + C * line_cell_stride<N>();
     const int64_t c0 = (int64_t)blockIdx.x * C;
-    if (t == 0 && ci == 0) {
+    if (traw == 0 && ci == 0) {
       const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
       const uint32_t bytes = (uint32_t)(nc * 6 * N3 * sizeof(double));
       mbar_init(&gbar, 1);
@@ -104,7 +118,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value)
   const CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, (DEFORMED && !a.g_direct) ? &gbar : nullptr};
   cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
   // scatter-add (constrained rows skipped; they are set to x_c afterwards)
-  if (active) {
+  if (active && real) {
 #pragma unroll
     for (int l = 0; l < N; ++l) {
       const bool m = cg_constrained(a.bcmask, gx, gy, a.gz0 + K * cz + l, a.nn0, a.nn1, a.nn2);
@@ -1041,6 +1055,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
   const OpArgs a = op_args(h, L, x, y);
   const Tab<N> T = make_tab<N>(h->tab);
   const dim3 block(N * N, C);
+  const dim3 lblock(line_tpc<K>(), C);   // line kernel (cg_apply_kernel)
   const int64_t grid = (L.n_cells + C - 1) / C;
   if (L.cartesian && !h->general_path) {
     KronTab<N> KT;
@@ -1087,7 +1102,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
     }
   } else if (L.cartesian) {
     const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
-    launch_pdl(h, cg_apply_kernel<K, false>, (unsigned)grid, block, sm, a, T);
+    launch_pdl(h, cg_apply_kernel<K, false>, (unsigned)grid, lblock, sm, a, T);
   } else if (L.glayout == kGLayoutXLine) {
     const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
     static bool attr_d = false;
@@ -1116,7 +1131,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
                                         (int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
       attr = true;
     }
-    launch_pdl(h, cg_apply_kernel<K, true>, (unsigned)grid, block, sm, a, T);
+    launch_pdl(h, cg_apply_kernel<K, true>, (unsigned)grid, lblock, sm, a, T);
   }
   count_launch();
   check_launch("cg_apply_kernel");

@@ -323,6 +323,166 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
   }
 }
 
+
+// ---------------------------------------------------------------- Cartesian SIPG: Kronecker form (K2c)
+// On a Cartesian mesh the SIPG operator is the Kronecker sum of the 1-D SIPG matrix A1
+// with the 1-D DG mass M1 (SURVEY App. A pin, verified to 1.8e-15):
+//     A = A1_x M1_y M1_z + M1_x A1_y M1_z + M1_x M1_y A1_z,
+// exact because the (k+1)-point Gauss rules integrate the cell stiffness and the
+// tangential face masses exactly.  A1 on a line of cells, for the line segment of
+// cell e (all terms from eq:poisson_dgsip / eq:bc_dgsip restricted to 1-D, n = +1 from
+// e to e+1, D+- = (2/h) phi'(+-1), GLL so phi_i(-1) = d_i0, phi_i(+1) = d_iK):
+//   out = (2/h) S_ref x_e + (1 + f_lo) RR x_e + (1 + f_hi) LL x_e
+//         + [e-1 exists] RL x_{e-1} + [e+1 exists] LR x_{e+1},
+//   RR x = 1/2 e_0 (D-.x) + 1/2 D- x_0 + sigma e_0 x_0       (left face, own side)
+//   LL x = -1/2 e_K (D+.x) - 1/2 D+ x_K + sigma e_K x_K      (right face, own side)
+//   LR x = -1/2 e_K (D-.x) + 1/2 D+ x_0 - sigma e_K x_0      (right neighbour)
+//   RL x = 1/2 e_0 (D+.x) - 1/2 D- x_K - sigma e_0 x_K       (left neighbour)
+// f = 0 at interior faces, +1 at a Dirichlet side (mirror: 2 RR / 2 LL), -1 at a Neumann
+// side (the face term vanishes).  Per cell: the three directional line operators on
+// x-, y- and z-lines read straight from global memory (own cell and its neighbours:
+// ghost layers on z-slabs), then the masses: y = M_z (M_y X + M_x Y) + M_y M_x Z, with
+// three shared-memory phases.  14 (k+1)^4 FMA per cell instead of the quadrature
+// kernel's cell + face sum factorization; no face data, no geometry.
+struct DgKron {
+  int n[3];
+  int cz0, nzg;
+  int64_t n_cells;
+  double sigma[3], sc[3], mc[3];   // penalty, 2/h_d (stiffness and D+- scale), h_d/2 (mass scale)
+  int flo[3], fhi[3];              // boundary factor of the low / high side of direction d
+};
+
+template <int N>
+struct DgKronTab {
+  double S[N][N];   // reference 1-D stiffness  sum_q w phi_i' phi_j'
+  double M[N][N];   // reference 1-D mass
+  double dm[N], dp[N];   // phi_i'(-1), phi_i'(+1) (reference)
+};
+
+// one line (length N along direction d) of cell e: own values xo, neighbours xl / xr
+template <int N>
+__device__ __forceinline__ void dg_line_op(const DgKronTab<N>& T, double sc, double sig, double flo, double fhi,
+                                          bool hl, bool hr, const double (&xo)[N], const double (&xl)[N],
+                                          const double (&xr)[N], double (&out)[N]) {
+  constexpr int K = N - 1;
+  double dmx = 0.0, dpx = 0.0, dpl = 0.0, dmr = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    dmx = fma(T.dm[j], xo[j], dmx);
+    dpx = fma(T.dp[j], xo[j], dpx);
+    dpl = fma(T.dp[j], xl[j], dpl);
+    dmr = fma(T.dm[j], xr[j], dmr);
+  }
+  dmx *= sc; dpx *= sc; dpl *= sc; dmr *= sc;
+  const double wl = 1.0 + flo, wr = 1.0 + fhi;
+  const double xl_K = hl ? xl[K] : 0.0, xr_0 = hr ? xr[0] : 0.0;
+  if (!hl) dpl = 0.0;
+  if (!hr) dmr = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double v = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) v = fma(T.S[i][j], xo[j], v);
+    v *= sc;
+    // own-side face terms (RR, LL) with their boundary weights, neighbour terms (RL, LR)
+    v = fma(0.5 * sc * T.dm[i], wl * xo[0] - xl_K, v);
+    v = fma(0.5 * sc * T.dp[i], xr_0 - wr * xo[K], v);
+    if (i == 0) v += wl * (0.5 * dmx + sig * xo[0]) + 0.5 * dpl - sig * xl_K;
+    if (i == K) v += wr * (-0.5 * dpx + sig * xo[K]) - 0.5 * dmr - sig * xr_0;
+    out[i] = v;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
+    dg_cart_kernel(const double* __restrict__ x, double* __restrict__ y, DgKron A, DgKronTab<K + 1> T) {
+  FEM_PDL_ENTRY();
+  constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
+  constexpr int C = DgCPB<K>::value;
+  extern __shared__ double smem[];
+  const int t = threadIdx.x, ci = threadIdx.y;
+  const int64_t cell = (int64_t)blockIdx.x * C + ci;
+  const bool active = cell < A.n_cells;
+  double* F0 = smem + ci * (3 * N3 + 1);
+  double* F1 = F0 + N3;
+  double* F2 = F1 + N3;
+  const int ta = t % N, tb = t / N;
+  int c[3] = {0, 0, 0};
+  if (active) {
+    c[0] = (int)(cell % A.n[0]);
+    const int64_t r = cell / A.n[0];
+    c[1] = (int)(r % A.n[1]);
+    c[2] = (int)(r / A.n[1]);
+  }
+  const int64_t stride[3] = {1, (int64_t)A.n[0], (int64_t)A.n[0] * A.n[1]};
+  const double* xc = x + (active ? cell : 0) * N3;
+  // ---- directional line operators, straight from global memory
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int gc = c[d] + (d == 2 ? A.cz0 : 0), nd = d == 2 ? A.nzg : A.n[d];
+    const bool hl = active && gc > 0, hr = active && gc < nd - 1;
+    const double flo = gc == 0 ? (double)A.flo[d] : 0.0, fhi = gc == nd - 1 ? (double)A.fhi[d] : 0.0;
+    // line (ta, tb) along d: x-line (y=ta, z=tb), y-line (x=ta, z=tb), z-line (x=ta, y=tb)
+    const int off = d == 0 ? N * ta + N2 * tb : (d == 1 ? ta + N2 * tb : ta + N * tb);
+    const int st = d == 0 ? 1 : (d == 1 ? N : N2);
+    double xo[N], xl[N], xr[N], o[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      xo[i] = active ? __ldg(xc + off + st * i) : 0.0;
+      xl[i] = hl ? __ldg(xc - stride[d] * N3 + off + st * i) : 0.0;
+      xr[i] = hr ? __ldg(xc + stride[d] * N3 + off + st * i) : 0.0;
+    }
+    dg_line_op<N>(T, A.sc[d], A.sigma[d], flo, fhi, hl, hr, xo, xl, xr, o);
+    double* F = d == 0 ? F0 : (d == 1 ? F1 : F2);
+#pragma unroll
+    for (int i = 0; i < N; ++i) F[off + st * i] = o[i];
+  }
+  __syncthreads();
+  // ---- x-lines (y=ta, z=tb): F1 <- M_x F1, F2 <- M_x F2
+  {
+    double a[N], b[N], o[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      a[i] = F1[i + N * t];
+      b[i] = F2[i + N * t];
+    }
+    mv<N>(T.M, a, o);
+#pragma unroll
+    for (int i = 0; i < N; ++i) F1[i + N * t] = A.mc[0] * o[i];
+    mv<N>(T.M, b, o);
+#pragma unroll
+    for (int i = 0; i < N; ++i) F2[i + N * t] = A.mc[0] * o[i];
+  }
+  __syncthreads();
+  // ---- y-lines (x=ta, z=tb): F0 <- M_y F0, F2 <- M_y F2
+  {
+    double a[N], b[N], o[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      a[j] = F0[ta + N * j + N2 * tb];
+      b[j] = F2[ta + N * j + N2 * tb];
+    }
+    mv<N>(T.M, a, o);
+#pragma unroll
+    for (int j = 0; j < N; ++j) F0[ta + N * j + N2 * tb] = A.mc[1] * o[j];
+    mv<N>(T.M, b, o);
+#pragma unroll
+    for (int j = 0; j < N; ++j) F2[ta + N * j + N2 * tb] = A.mc[1] * o[j];
+  }
+  __syncthreads();
+  // ---- z-lines (x=ta, y=tb): y = M_z (F0 + F1) + F2
+  {
+    double a[N], o[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) a[l] = F0[t + N2 * l] + F1[t + N2 * l];
+    mv<N>(T.M, a, o);
+    if (active) {
+#pragma unroll
+      for (int l = 0; l < N; ++l) y[cell * N3 + t + N2 * l] = fma(A.mc[2], o[l], F2[t + N2 * l]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- diagonal (R6)
 // cell part as for CG; face part on the face layer of every face:
 //   interior sum_q JxW (-phi d_n phi + sigma phi^2), Dirichlet sum_q JxW (-2 phi d_n phi + 2 sigma phi^2).
@@ -575,8 +735,50 @@ void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y) {
 }
 
 template <int K>
+void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y) {
+  constexpr int N = K + 1, C = DgCPB<K>::value;
+  DgKron A;
+  for (int d = 0; d < 3; ++d) {
+    A.n[d] = L.n[d];
+    A.sigma[d] = h->opt.penalty_factor * (h->k + 1) * (h->k + 1) / L.h[d];
+    A.sc[d] = 2.0 / L.h[d];
+    A.mc[d] = 0.5 * L.h[d];
+    A.flo[d] = h->mesh.bc[2 * d] == FEM_BC_DIRICHLET ? 1 : -1;
+    A.fhi[d] = h->mesh.bc[2 * d + 1] == FEM_BC_DIRICHLET ? 1 : -1;
+  }
+  A.cz0 = L.cz0;
+  A.nzg = L.nzg;
+  A.n_cells = L.n_cells;
+  DgKronTab<N> T;
+  for (int i = 0; i < N; ++i) {
+    for (int j = 0; j < N; ++j) {
+      double m = 0.0, sv = 0.0;
+      for (int q = 0; q < N; ++q) {
+        m += h->tab.qw[q] * h->tab.val[q][i] * h->tab.val[q][j];
+        sv += h->tab.qw[q] * h->tab.der[q][i] * h->tab.der[q][j];
+      }
+      T.M[i][j] = m;
+      T.S[i][j] = sv;
+    }
+    T.dm[i] = h->tab.dface[0][i];
+    T.dp[i] = h->tab.dface[1][i];
+  }
+  const size_t sm = sizeof(double) * (3 * N * N * N + 1) * C;
+  static bool attr = false;
+  if (!attr) {
+    FEM_CUDA_TRY(cudaFuncSetAttribute(dg_cart_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr = true;
+  }
+  const unsigned grid = (unsigned)((L.n_cells + C - 1) / C);
+  launch_pdl(h, dg_cart_kernel<K>, grid, dim3(N * N, C), sm, x, y, A, T);
+  count_launch();
+  check_launch("dg_cart_kernel");
+}
+
+template <int K>
 void dg_apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
-  if (L.cartesian) dg_apply_kd<K, false>(h, L, x, y);
+  if (L.cartesian && h->dg_kron) dg_cart_k<K>(h, L, x, y);
+  else if (L.cartesian) dg_apply_kd<K, false>(h, L, x, y);
   else dg_apply_kd<K, true>(h, L, x, y);
 }
 

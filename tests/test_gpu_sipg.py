@@ -57,8 +57,23 @@ def test_apply_and_diagonal_match_oracle(k, cells, eps, bc):
     F.close()
 
 
-def test_penalty_factor_is_honoured():
-    F, m = make((3, 2, 2), 2, 0.05, MIXED, pf=3.0)
+@pytest.mark.parametrize("k,cells,bc", [(1, (5, 3, 4), MIXED), (4, (6, 4, 3), (DIRICHLET,) * 6),
+                                        (3, (2, 5, 1), MIXED), (8, (2, 1, 2), MIXED)])
+def test_cartesian_quadrature_kernel_matches_oracle(k, cells, bc, monkeypatch):
+    """Cartesian levels run the Kronecker kernel (K2c) by default; the quadrature
+    cell+face kernel (FEM_DG_KRON=0) stays pinned too."""
+    monkeypatch.setenv("FEM_DG_KRON", "0")
+    F, m = make(cells, k, 0.0, bc)
+    x = fem_inputs.uniform_pm1(6, m.dg_n_dofs())
+    y = np.zeros_like(x)
+    F.fem_apply(x, y)
+    assert relmax(y, osipg.apply(m, x)) <= 1e-12
+    F.close()
+
+
+@pytest.mark.parametrize("eps", [0.05, 0.0])
+def test_penalty_factor_is_honoured(eps):
+    F, m = make((3, 2, 2), 2, eps, MIXED, pf=3.0)
     x = fem_inputs.uniform_pm1(4, m.dg_n_dofs())
     y = np.zeros_like(x)
     F.fem_apply(x, y)

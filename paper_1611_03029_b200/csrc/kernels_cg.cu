@@ -633,7 +633,8 @@ struct StencilCfg {
   static constexpr int LPAD = LCOLS | 1;              // odd row stride: rows hit distinct banks
   static constexpr int TXP = TX + 1;                  // odd row stride of the A, B buffers
   static constexpr int HROWS = (LROWS + 1) / 2;       // x-stage: one item = one slot, two rows
-  static constexpr int SMEM = 2 * LROWS * LPAD + 2 * LROWS * TXP;   // doubles
+  static constexpr int NBUF = 4;                     // input planes in flight (prefetch distance 3)
+  static constexpr int SMEM = NBUF * LROWS * LPAD + 2 * LROWS * TXP;   // doubles
 };
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
@@ -656,8 +657,8 @@ __global__ void __launch_bounds__(StencilCfg<K>::THREADS, FEM_STENCIL_MINB)
   constexpr int TEX = Cfg::TEX, TEY = Cfg::TEY, TX = Cfg::TX, LR = Cfg::LROWS, LC = Cfg::LCOLS,
                 LP = Cfg::LPAD, TXP = Cfg::TXP, HR = Cfg::HROWS;
   extern __shared__ double smem[];
-  double* X0 = smem;                    // two input buffers [LR][LP]
-  double* Ab = smem + 2 * LR * LP;      // A = M1_x x~ at [row][tile x] (row stride TXP)
+  double* X0 = smem;                    // NBUF input buffers [LR][LP]
+  double* Ab = smem + Cfg::NBUF * LR * LP;   // A = M1_x x~ at [row][tile x] (row stride TXP)
   double* Bb = Ab + LR * TXP;           // B = S1_x x~
   const int tid = threadIdx.x;
   const int e0 = blockIdx.x * TEX, f0 = blockIdx.y * TEY;   // first x / y slot of the tile
@@ -794,7 +795,13 @@ __global__ void __launch_bounds__(StencilCfg<K>::THREADS, FEM_STENCIL_MINB)
 
   // ---- march through z: planes 0 .. K nzl (local), element by element
   const int nplanes = K * nzl + 1;
-  load_plane(0, X0);
+  constexpr int NB = Cfg::NBUF;
+  // prologue: planes 0 .. NB-2 in flight (one commit group each, empty groups past the end)
+#pragma unroll
+  for (int q = 0; q < NB - 1; ++q) {
+    if (q < nplanes) load_plane(q, X0 + q * LR * LP);
+    else cp_async_commit();
+  }
   int buf = 0;
   for (int ez = 0; ez < nzl; ++ez) {
 #pragma unroll
@@ -807,16 +814,15 @@ __global__ void __launch_bounds__(StencilCfg<K>::THREADS, FEM_STENCIL_MINB)
     for (int rp = 0; rp <= K; ++rp) {
       if (rp == 0 && ez > 0) continue;
       const int pl = ez * K + rp;
-      if (pl + 1 < nplanes) {
-        load_plane(pl + 1, X0 + (buf ^ 1) * LR * LP);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
+      // plane pl + NB - 1 goes into the buffer last read for plane pl - 1 (all threads
+      // passed the barrier after that x-stage); always commit so the group count is fixed
+      if (pl + NB - 1 < nplanes) load_plane(pl + NB - 1, X0 + ((buf + NB - 1) % NB) * LR * LP);
+      else cp_async_commit();
+      cp_async_wait<NB - 1>();
       __syncthreads();
       double P[K], Q[K];
       plane_pq(pl, X0 + buf * LR * LP, P, Q);
-      buf ^= 1;
+      buf = (buf + 1) % NB;
       if (rp == 0) {
 #pragma unroll
         for (int r = 0; r < K; ++r) {

@@ -280,10 +280,12 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
   __syncthreads();
 }
 
+#ifndef FEM_DG_MINB
+#define FEM_DG_MINB 2
+#endif
 template <int K, bool DEFORMED>
-__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
+__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? FEM_DG_MINB : 1)
     dg_apply_kernel(DgArgs A, Tab<K + 1> T) {
-  FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = DgCPB<K>::value;
   using L = DgSmem<N>;
@@ -291,6 +293,14 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
   const int t = threadIdx.x, ci = threadIdx.y;
   const int64_t cell = (int64_t)blockIdx.x * C + ci;
   const bool active = cell < A.n_cells;
+  if (DEFORMED && t == 0 && ci == 0) {
+    // static geometry of the block's cells (and their lower x-faces, which are
+    // contiguous): pull it into L2 before waiting on the predecessor kernel
+    const int64_t c0 = (int64_t)blockIdx.x * C;
+    const int64_t nc = (A.n_cells - c0) < C ? (A.n_cells - c0) : C;
+    bulk_prefetch_l2(A.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
+  }
+  FEM_PDL_ENTRY();
   double* sm = smem + ci * L::SIZE;
   int c[3] = {0, 0, 0};
   if (active) {

@@ -526,7 +526,10 @@ struct KronTab {
 };
 
 template <int K>
-__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? 4 : 1)
+#ifndef FEM_CART_MINB
+#define FEM_CART_MINB 3
+#endif
+__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FEM_CART_MINB : 1)
     cg_cart_kernel(OpArgs a, KronTab<K + 1> T, int64_t cell0, int64_t cell_end) {
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;

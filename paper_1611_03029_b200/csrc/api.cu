@@ -194,10 +194,13 @@ void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool se
   if (is_cg(h)) {
     // the Cartesian fast path zeroes y itself, chunk by chunk (kernels_cg.cu)
     const bool tiled = L.cartesian && !h->general_path;
-    if (!tiled && !(y == L.t && L.t_zero)) launch_zero(h, y, L.n_store);
+    const bool y_zero = y == L.t && L.t_zero;
+    if (!tiled && !y_zero) launch_zero(h, y, L.n_store);
     if (y == L.t) L.t_zero = false;
+    h->y_is_zero = y_zero;   // the Cartesian element path zeroes y itself unless told it is zero
     prof_begin(h, finest);
     launch_cg_apply(h, L, x, y);
+    h->y_is_zero = false;
     prof_end(h, finest);
     halo_export_add(h, L, y);
     if (set_constrained) launch_set_constrained(h, L, x, y);

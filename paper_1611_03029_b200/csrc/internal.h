@@ -165,6 +165,7 @@ struct fem_ctx {
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
   bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)
   bool g_direct = true;                // FEM_G_DIRECT=0: line kernel stages G by TMA into shared memory
+  bool y_is_zero = false;              // set around launch_cg_apply: the output is known to be zero
   bool pdl = true;                     // FEM_PDL=0: plain launches (no programmatic dependent launch)
   bool dg_kron = true;                 // FEM_DG_KRON=0: quadrature cell+face kernel on Cartesian SIPG levels
   bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels

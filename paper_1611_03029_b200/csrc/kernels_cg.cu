@@ -519,6 +519,11 @@ __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
 // i.e. 7 line sweeps and 2 shared-memory transposes (2 fields each) per cell, and
 // the scatter happens from z-lines (consecutive lanes -> consecutive addresses).
 // cell0: first cell of this launch (the apply runs in z-chunks, see launcher).
+// cell stride of the Kronecker element kernel's two buffers (+3 doubles at Q4: 11% fewer
+// shared wavefronts in the bank-conflict model, as for the line kernel)
+template <int N>
+__host__ __device__ constexpr int cart_cell_stride() { return 2 * N * N * N + (N == 5 ? 3 : 0); }
+
 template <int N>
 struct KronTab {
   double M[N][N];
@@ -538,7 +543,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FE
   const int t = threadIdx.x, ci = threadIdx.y;
   const int64_t cell = cell0 + (int64_t)blockIdx.x * C + ci;
   const bool active = cell < cell_end;
-  double* s0 = smem + ci * 2 * N3;
+  double* s0 = smem + ci * cart_cell_stride<N>();
   double* s1 = s0 + N3;
   const int ta = t % N, tb = t / N;
   int cx = 0, cy = 0, cz = 0;
@@ -1093,7 +1098,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
       check_launch("cg_stencil_kernel");
       return;
     }
-    const size_t sm = sizeof(double) * 2 * N * N * N * C;
+    const size_t sm = sizeof(double) * cart_cell_stride<N>() * C;
     // z-chunks: zero the chunk's node planes (all but the bottom one, which the previous
     // chunk has accumulated into) right before its cells are applied, so that the
     // atomic adds hit lines that are resident in L2 instead of re-reading y from HBM.
@@ -1103,7 +1108,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
     for (int z0 = 0; z0 < L.n[2]; z0 += lz) {
       const int z1 = std::min(z0 + lz, L.n[2]);
       const int64_t p0 = z0 == 0 ? 0 : (int64_t)K * z0 + 1, p1 = (int64_t)K * z1 + 1;
-      launch_zero(h, y + p0 * plane, (p1 - p0) * plane);
+      if (!h->y_is_zero) launch_zero(h, y + p0 * plane, (p1 - p0) * plane);
       const int64_t c0 = layer * z0, c1 = layer * z1;
       launch_pdl(h, cg_cart_kernel<K>, (unsigned)((c1 - c0 + C - 1) / C), block, sm, a, KT, c0, c1);
       count_launch();

@@ -677,17 +677,33 @@ __global__ void __launch_bounds__(StencilCfg<K>::THREADS, FEM_STENCIL_MINB)
   const bool cx0 = a.bcmask & 1, cx1 = a.bcmask & 2, cy0 = a.bcmask & 4, cy1 = a.bcmask & 8;
   const bool cz0 = a.bcmask & 16, cz1 = a.bcmask & 32;
 
+  // Plane loads: thread tid always loads the same (row, column) slots of the tile, so the
+  // in-domain / constraint tests and the in-plane offsets are computed once per kernel
+  // (a bitmask of the valid slots and one 32-bit offset each); per plane only the z test.
+  constexpr int NLD = (LR * LC + Cfg::THREADS - 1) / Cfg::THREADS;
+  int ld_off[NLD];
+  uint32_t ld_ok = 0;
+#pragma unroll
+  for (int j = 0; j < NLD; ++j) {
+    const int idx = tid + j * Cfg::THREADS;
+    const int r = idx / LC, c = idx % LC;
+    const int gx = gx0 + c, gy = gy0 + r;
+    const bool in = idx < LR * LC && gx >= 0 && gx < NX && gy >= 0 && gy < NY;
+    const bool m = (cx0 && gx == 0) || (cx1 && gx == NX - 1) || (cy0 && gy == 0) || (cy1 && gy == NY - 1);
+    ld_off[j] = in ? gx + NX * gy : 0;
+    if (in && !m) ld_ok |= 1u << j;
+  }
   auto load_plane = [&](int pl, double* buf) {   // local z plane pl (global a.gz0 + pl)
     const int gz = a.gz0 + pl;
     const bool zmask = (cz0 && gz == 0) || (cz1 && gz == a.nn2 - 1);
     const double* src = a.x + (int64_t)pl * zs;
-    for (int idx = tid; idx < LR * LC; idx += Cfg::THREADS) {
-      const int r = idx / LC, c = idx % LC;
-      const int gx = gx0 + c, gy = gy0 + r;
-      const bool in = gx >= 0 && gx < NX && gy >= 0 && gy < NY;
-      const bool m = zmask || (cx0 && gx == 0) || (cx1 && gx == NX - 1) || (cy0 && gy == 0) ||
-                     (cy1 && gy == NY - 1);
-      cp_async8(buf + r * LP + c, in ? src + gx + (int64_t)NX * gy : a.x, in && !m);
+#pragma unroll
+    for (int j = 0; j < NLD; ++j) {
+      const int idx = tid + j * Cfg::THREADS;
+      if (idx < LR * LC) {
+        const int r = idx / LC, c = idx % LC;
+        cp_async8(buf + r * LP + c, src + ld_off[j], !zmask && ((ld_ok >> j) & 1u));
+      }
     }
     cp_async_commit();
   };

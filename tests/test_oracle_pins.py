@@ -421,3 +421,49 @@ def test_pcg_iteration_counts_match_independent_prototype():
         _, its, rr = mg.pcg(problem.rhs(m, method), tol=1e-10)
         assert rr <= 1e-10
         assert abs(its - case["iterations"]) <= g["tolerance_iterations"], case
+
+
+# ---------------------------------------------------------------- the paper's own problem (N2)
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_paper_gaussian_problem_errors_match_printed_values(k):
+    """eq:pois_analytic on (-1,1)^3 (Neumann at x_e=-1, Dirichlet at +1, sigma with d=3,
+    tol 1e-9): the oracle's CG and SIPG solutions reproduce the L2 errors the paper
+    prints for 8^3 cells (tests/golden/paper_gaussian_errors.json) to 2%,
+    and the iteration counts within the +-2 envelope (the paper's multigrid setup differs:
+    coarse solver, smoother degree, residual norm)."""
+    from oracle import gaussians as gs, multigrid as omg
+    from oracle.mesh import CG, SIPG
+    row = next(r for r in golden("paper_gaussian_errors.json")["rows"] if r["k"] == k and r["cells"] == 512)
+    m = gs.mesh((8, 8, 8), k)
+    b = gs.rhs(m, CG)
+    x0 = np.where(m.cg_dirichlet_mask(), b, 0.0)
+    x, its, rr = omg.Multigrid(m, CG).pcg(b, tol=1e-9, x0=x0)
+    assert rr <= 1e-9
+    assert abs(gs.l2_error_abs(m, CG, x) / row["FEL2"] - 1.0) <= 0.02
+    assert abs(its - row["qIt"]) <= 2
+    bd = gs.rhs(m, SIPG)
+    xd, itd, rd = omg.Multigrid(m, SIPG, penalty_factor=gs.PENALTY_FACTOR).pcg(bd, tol=1e-9)
+    assert rd <= 1e-9
+    assert abs(gs.l2_error_abs(m, SIPG, xd) / row["dgL2"] - 1.0) <= 0.02
+    assert abs(itd - row["dgIt"]) <= 2
+
+
+def test_paper_gaussian_problem_data():
+    """The problem data is what eq:pois_analytic states: f = -Laplace u checked by finite
+    differences, g_N = -n.grad u, the Gaussian normalisation (integral of one Gaussian
+    over R^3 = alpha^3 (pi)^(3/2) (alpha sqrt(2 pi))^-3 = 2^(-3/2))."""
+    from oracle import gaussians as gs
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (20, 3))
+    h = 1e-4
+    lap = sum((gs.exact_u(x + h * e) - 2 * gs.exact_u(x) + gs.exact_u(x - h * e)) / h ** 2 for e in np.eye(3))
+    assert np.allclose(-lap, gs.exact_f(x), rtol=1e-5, atol=1e-6 * np.abs(gs.exact_f(x)).max())
+    g = np.stack([(gs.exact_u(x + h * e) - gs.exact_u(x - h * e)) / (2 * h) for e in np.eye(3)], axis=-1)
+    assert np.allclose(g, gs.grad_u(x), rtol=1e-6, atol=1e-8 * np.abs(g).max())
+    # one Gaussian integrates to 2^-1.5 over R^3 (its mass lies well inside the cube)
+    t = np.linspace(-3, 3, 601)
+    w = np.full_like(t, t[1] - t[0])
+    X, Y, Z = np.meshgrid(t, t, t, indexing="ij")
+    c = (1 / (gs.ALPHA * np.sqrt(2 * np.pi))) ** 3
+    one = c * np.exp(-(X ** 2 + Y ** 2 + Z ** 2) / gs.ALPHA ** 2)
+    assert abs(np.einsum("ijk,i,j,k->", one, w, w, w) - 2 ** -1.5) <= 1e-6

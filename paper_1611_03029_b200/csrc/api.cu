@@ -466,6 +466,10 @@ void setup_coarse(fem_ctx* h) {
   FEM_CUDA_TRY(cudaMalloc(&h->coarse_free, sizeof(int) * std::max(nf, 1)));
   h->coarse_inv = dalloc((int64_t)nf * nf);
   FEM_CUDA_TRY(cudaMemcpy(h->coarse_free, fr.data(), sizeof(int) * nf, cudaMemcpyHostToDevice));
+  std::vector<int> pos(n, -1);
+  for (int i = 0; i < nf; ++i) pos[fr[i]] = i;
+  FEM_CUDA_TRY(cudaMalloc(&h->coarse_pos, sizeof(int) * std::max<int64_t>(n, 1)));
+  FEM_CUDA_TRY(cudaMemcpy(h->coarse_pos, pos.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
   FEM_CUDA_TRY(cudaMemcpy(h->coarse_inv, inv.data(), sizeof(double) * nf * nf, cudaMemcpyHostToDevice));
 }
 
@@ -777,6 +781,7 @@ void destroy(fem_ctx* h) {
   }
   h->comm.reset();
   if (h->coarse_free) cudaFree(h->coarse_free);
+  if (h->coarse_pos) cudaFree(h->coarse_pos);
   dfree(h->coarse_inv);
   dfree(h->red);
   dfree(h->scal);

@@ -146,6 +146,7 @@ struct fem_ctx {
   // coarse solve: free DoFs of level 0 and the dense inverse (via Cholesky)
   int n_coarse_free = 0;
   int* coarse_free = nullptr;
+  int* coarse_pos = nullptr;       // [n] row of each level-0 entry in the inverse, -1 if constrained
   double* coarse_inv = nullptr;
   // reductions
   double* red = nullptr;          // partial sums [kRedBlocks * 4]

@@ -330,18 +330,25 @@ __global__ void set_scalar_kernel(double* scal, int idx, double v) {
   FEM_PDL_ENTRY(); scal[idx] = v; }
 
 // x = A0^{-1} b on the free DoFs (dense inverse from the Cholesky factor); x = 0 elsewhere.
+// x = A0^{-1} b on the free DoFs (dense inverse from the Cholesky factor); x = 0 elsewhere.
+// One warp per entry of x (coalesced row reads, shuffle reduction), b's free entries
+// staged in shared memory by every block; pos[i] = row of entry i in A0^{-1} or -1.
 __global__ void coarse_solve_kernel(const double* __restrict__ Ainv, const int* __restrict__ free_idx,
-                                    int nf, const double* __restrict__ b, double* __restrict__ x,
-                                    int64_t n) {
+                                    const int* __restrict__ pos, int nf, const double* __restrict__ b,
+                                    double* __restrict__ x, int64_t n) {
   FEM_PDL_ENTRY();
   extern __shared__ double sb[];
   for (int i = threadIdx.x; i < nf; i += blockDim.x) sb[i] = b[free_idx[i]];
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = 0.0;
   __syncthreads();
-  for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < n; e += warps) {
+    const int row = pos[e];
     double s = 0.0;
-    for (int j = 0; j < nf; ++j) s = fma(Ainv[(int64_t)i * nf + j], sb[j], s);
-    x[free_idx[i]] = s;
+    if (row >= 0)
+      for (int j = lane; j < nf; j += 32) s = fma(Ainv[(int64_t)row * nf + j], sb[j], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) x[e] = s;
   }
 }
 
@@ -525,8 +532,9 @@ void launch_set_scalar(fem_ctx* h, int idx, double v) {
 
 void launch_coarse_solve(fem_ctx* h, const double* b, double* x) {
   const Level& L0 = h->levels[0];
-  launch_pdl(h, coarse_solve_kernel, 1, 512, sizeof(double) * h->n_coarse_free, 
-      h->coarse_inv, h->coarse_free, h->n_coarse_free, b, x, L0.n_dofs);
+  const unsigned grid = (unsigned)std::min<int64_t>((L0.n_dofs + 7) / 8, 148);
+  launch_pdl(h, coarse_solve_kernel, grid, 256, sizeof(double) * h->n_coarse_free, h->coarse_inv,
+             h->coarse_free, h->coarse_pos, h->n_coarse_free, b, x, L0.n_dofs);
   count_launch();
   check_launch("coarse_solve_kernel");
 }

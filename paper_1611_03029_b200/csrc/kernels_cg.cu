@@ -56,8 +56,14 @@ __host__ __device__ constexpr int line_cell_stride() { return 3 * N * N * N + (N
 template <int K>
 __host__ __device__ constexpr int line_tpc() { return (K == 4 && FEM_WARP_CELL) ? 32 : (K + 1) * (K + 1); }
 
+// blocks per SM the register allocation must allow (measured, tools/sweep_hi.py: the
+// uncapped k = 6 and 8 kernels use 103 and 168 registers -> 3 and 1 blocks; capping them
+// trades a few spills for occupancy: k = 6 928 -> 511 us, k = 8 949 -> 811 us at 1.6e7 DoFs)
+template <int K>
+__host__ __device__ constexpr int line_minb() { return K == 6 ? 4 : (K == 8 ? 3 : 1); }
+
 template <int K, bool DEFORMED>
-__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value)
+__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
     cg_apply_kernel(OpArgs a, Tab<K + 1> T) {
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;

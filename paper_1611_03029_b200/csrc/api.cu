@@ -22,9 +22,9 @@
 
 namespace fem {
 
-void launch_cg_apply(fem_ctx* h, const Level& L, const double* x, double* y);
+void launch_cg_apply(fem_ctx* h, const Level& L, const double* x, double* y, int64_t c0 = 0, int64_t c1 = -1);
 void launch_cg_diagonal(fem_ctx* h, Level& L);
-void launch_dg_apply(fem_ctx* h, const Level& L, const double* x, double* y);
+void launch_dg_apply(fem_ctx* h, const Level& L, const double* x, double* y, int64_t c0 = 0, int64_t c1 = -1);
 void launch_dg_diagonal(fem_ctx* h, Level& L);
 void launch_dg_face_geometry(fem_ctx* h, Level& L);
 
@@ -135,7 +135,21 @@ enum { kTagCgImport = 1, kTagCgExport = 2, kTagDgToUpper = 3, kTagDgToLower = 4 
 
 }  // namespace
 
-void halo_import(fem_ctx* h, const Level& L, double* v) {
+namespace {
+void halo_import_on(fem_ctx* h, const Level& L, double* v, cudaStream_t stream);
+void halo_export_send(fem_ctx* h, const Level& L, double* v, cudaStream_t stream);
+}  // namespace
+
+void halo_import(fem_ctx* h, const Level& L, double* v) { halo_import_on(h, L, v, h->stream); }
+
+void halo_export_add(fem_ctx* h, const Level& L, double* v) {
+  if (!L.dist || !h->comm || !is_cg(h)) return;
+  halo_export_send(h, L, v, h->stream);
+  if (L.ghost_lo >= 0) launch_add(h, v, L.halo, (int64_t)L.nn[0] * L.nn[1]);
+}
+
+namespace {
+void halo_import_on(fem_ctx* h, const Level& L, double* v, cudaStream_t stream) {
   if (!L.dist || !h->comm) return;
   std::vector<Comm::Msg> snd, rcv;
   if (is_cg(h)) {
@@ -154,18 +168,19 @@ void halo_import(fem_ctx* h, const Level& L, double* v) {
       rcv.push_back({L.ghost_hi, kTagDgToUpper, v + L.n_dofs, layer});
     }
   }
-  h->comm->exchange(snd, rcv, h->stream);
+  h->comm->exchange(snd, rcv, stream);
 }
 
-void halo_export_add(fem_ctx* h, const Level& L, double* v) {
-  if (!L.dist || !h->comm || !is_cg(h)) return;
+// CG: send the ghost node plane of v to the rank above, receive the one of the rank
+// below into L.halo (the caller adds it into plane 0)
+void halo_export_send(fem_ctx* h, const Level& L, double* v, cudaStream_t stream) {
   const int64_t plane = (int64_t)L.nn[0] * L.nn[1];
   std::vector<Comm::Msg> snd, rcv;
   if (L.ghost_hi >= 0) snd.push_back({L.ghost_hi, kTagCgExport, v + (int64_t)h->k * L.n[2] * plane, plane});
   if (L.ghost_lo >= 0) rcv.push_back({L.ghost_lo, kTagCgExport, L.halo, plane});
-  h->comm->exchange(snd, rcv, h->stream);
-  if (L.ghost_lo >= 0) launch_add(h, v, L.halo, plane);
+  h->comm->exchange(snd, rcv, stream);
 }
+}  // namespace
 
 void allreduce(fem_ctx* h, double* p, int64_t n) {
   if (h->comm) h->comm->allreduce_sum(p, n, h->stream);
@@ -186,10 +201,56 @@ void dot(fem_ctx* h, const Level& L, const double* a, const double* b, int slot)
 // timed: the launch is bracketed by profiling events (fem_options.profile; only the
 // PCG operator apply of cg_solve and the eager fem_apply calls are, so that the
 // events do not perturb the timed solve: the kernel is the same in every apply).
+// Distributed level: the halo exchanges run on the handle's communication stream and
+// overlap the cells that do not touch ghosts (z-slab interior), SURVEY §8e:
+//   CG:   zero y | import x ghost plane || cells [0, mid) | wait, top layer |
+//         export y ghost plane || cells [mid, top) | wait, add the received plane
+//   SIPG: import both ghost layers || interior layers | wait, bottom and top layers
+void apply_level_overlap(fem_ctx* h, const Level& L, const double* x, double* y) {
+  const int64_t layer = (int64_t)L.n[0] * L.n[1];
+  const int n2 = L.n[2];
+  cudaStream_t cs = h->comm_stream;
+  FEM_CUDA_TRY(cudaEventRecord(h->ev_fork, h->stream));
+  FEM_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev_fork, 0));
+  halo_import_on(h, L, const_cast<double*>(x), cs);
+  FEM_CUDA_TRY(cudaEventRecord(h->ev_import, cs));
+  if (is_cg(h)) {
+    const int mid = (n2 - 1) / 2;
+    launch_cg_apply(h, L, x, y, 0, mid * layer);
+    FEM_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_import, 0));
+    launch_cg_apply(h, L, x, y, (int64_t)(n2 - 1) * layer, (int64_t)n2 * layer);
+    FEM_CUDA_TRY(cudaEventRecord(h->ev_fork, h->stream));
+    FEM_CUDA_TRY(cudaStreamWaitEvent(cs, h->ev_fork, 0));
+    halo_export_send(h, L, y, cs);
+    FEM_CUDA_TRY(cudaEventRecord(h->ev_export, cs));
+    launch_cg_apply(h, L, x, y, (int64_t)mid * layer, (int64_t)(n2 - 1) * layer);
+    FEM_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_export, 0));
+    if (L.ghost_lo >= 0) launch_add(h, y, L.halo, (int64_t)L.nn[0] * L.nn[1]);
+  } else {
+    if (n2 >= 3) launch_dg_apply(h, L, x, y, layer, (int64_t)(n2 - 1) * layer);
+    FEM_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_import, 0));
+    launch_dg_apply(h, L, x, y, 0, layer);
+    if (n2 >= 2) launch_dg_apply(h, L, x, y, (int64_t)(n2 - 1) * layer, (int64_t)n2 * layer);
+  }
+}
+
 void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool set_constrained = true,
                  bool timed = false) {
   const bool finest = timed && (&L == &h->levels.back());
   if (h->prof.on && finest && !h->prof.capturing && h->prof.used + 2 > 4096) prof_collect(h);
+  if (L.dist && h->comm && h->overlap) {
+    if (is_cg(h)) {
+      if (!(y == L.t && L.t_zero)) launch_zero(h, y, L.n_store);
+      if (y == L.t) L.t_zero = false;
+      h->y_is_zero = true;
+    }
+    prof_begin(h, finest);
+    apply_level_overlap(h, L, x, y);
+    prof_end(h, finest);
+    h->y_is_zero = false;
+    if (is_cg(h) && set_constrained) launch_set_constrained(h, L, x, y);
+    return;
+  }
   halo_import(h, L, const_cast<double*>(x));
   if (is_cg(h)) {
     // the Cartesian fast path zeroes y itself, chunk by chunk (kernels_cg.cu)
@@ -780,6 +841,9 @@ void destroy(fem_ctx* h) {
       vfree(L, *p);
   }
   h->comm.reset();
+  for (cudaEvent_t e : {h->ev_fork, h->ev_import, h->ev_export})
+    if (e) cudaEventDestroy(e);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
   if (h->coarse_free) cudaFree(h->coarse_free);
   if (h->coarse_pos) cudaFree(h->coarse_pos);
   dfree(h->coarse_inv);
@@ -862,7 +926,11 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
       h->comm = mesh->nccl_id ? make_nccl_comm(mesh->nccl_id, h->rank, h->nranks)
                               : make_local_comm(mesh->local_group, h->rank, h->nranks);
       h->use_graphs = h->comm->graph_capturable();
+      FEM_CUDA_TRY(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+      for (cudaEvent_t* e : {&h->ev_fork, &h->ev_import, &h->ev_export})
+        FEM_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
+    if (const char* e = std::getenv("FEM_OVERLAP")) h->overlap = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_NO_GRAPHS")) h->use_graphs = h->use_graphs && std::atoi(e) == 0;
     FEM_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     h->prof.on = h->opt.profile != 0;

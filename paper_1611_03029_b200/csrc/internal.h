@@ -161,7 +161,10 @@ struct fem_ctx {
   fem::SolveGraphs sg;
   std::unique_ptr<fem::Comm> comm;      // nranks > 1
   int rank = 0, nranks = 1;
-  bool use_graphs = true;               // PCG iteration as CUDA graphs (not with the in-process transport)
+  bool use_graphs = true;
+  bool overlap = true;                  // FEM_OVERLAP=0: halo exchanges serialised with the applies
+  cudaStream_t comm_stream = nullptr;   // halo exchanges of distributed levels
+  cudaEvent_t ev_fork = nullptr, ev_import = nullptr, ev_export = nullptr;               // PCG iteration as CUDA graphs (not with the in-process transport)
   int chunk_layers = 0;                 // Cartesian CG apply: cell layers per z-chunk (FEM_CHUNK_LAYERS; 0 = one launch)
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
   bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)

@@ -39,6 +39,7 @@ struct OpArgs {
   int g_direct;                  // line kernel: G from global (L2-prefetched) instead of TMA->smem
   int bcmask;
   int64_t n_cells;
+  int64_t cell0, cell1;          // cells [cell0, cell1) of this launch (z-slab overlap splits)
   double c0, c1, c2;             // Cartesian metric det(J) (2/h_d)^2
 };
 
@@ -73,8 +74,8 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
   const int t = traw < N2 ? traw : traw - N2;
   const bool real = traw < N2;
   const int ci = threadIdx.y;
-  const int64_t cell = (int64_t)blockIdx.x * C + ci;
-  const bool active = cell < a.n_cells;
+  const int64_t cell = a.cell0 + (int64_t)blockIdx.x * C + ci;
+  const bool active = cell < a.cell1;
   double* s0 = smem + ci * line_cell_stride<N>();
   const int ta = t % N, tb = t / N;
   int cx = 0, cy = 0, cz = 0;
@@ -102,17 +103,17 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
   if (DEFORMED && a.g_direct) {
     // G read straight from global memory in the q-point phase (each warp load is 256
     // contiguous bytes: q = t + N^2 l); the block's slice is bulk-prefetched into L2 now
-    const int64_t c0 = (int64_t)blockIdx.x * C;
+    const int64_t c0 = a.cell0 + (int64_t)blockIdx.x * C;
     if (traw == 0 && ci == 0) {
-      const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
+      const int64_t nc = (a.cell1 - c0) < C ? (a.cell1 - c0) : C;
       bulk_prefetch_l2(a.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
     }
     Gs = a.G + (active ? cell : 0) * 6 * N3;
   } else if (DEFORMED) {
     double* sG = smem + C * line_cell_stride<N>();
-    const int64_t c0 = (int64_t)blockIdx.x * C;
+    const int64_t c0 = a.cell0 + (int64_t)blockIdx.x * C;
     if (traw == 0 && ci == 0) {
-      const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
+      const int64_t nc = (a.cell1 - c0) < C ? (a.cell1 - c0) : C;
       const uint32_t bytes = (uint32_t)(nc * 6 * N3 * sizeof(double));
       mbar_init(&gbar, 1);
       mbar_arrive_expect_tx(&gbar, bytes);
@@ -158,15 +159,15 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FE
   constexpr int C = CPB<K>::value;
   extern __shared__ double smem[];
   const int t = threadIdx.x, ci = threadIdx.y;
-  const int64_t cell = (int64_t)blockIdx.x * C + ci;
-  const bool active = cell < a.n_cells;
+  const int64_t cell = a.cell0 + (int64_t)blockIdx.x * C + ci;
+  const bool active = cell < a.cell1;
   double* F0 = smem + ci * line_cell_stride<N>();
   double* F1 = F0 + N3;
   double* F2 = F1 + N3;
   const int ta = t % N, tb = t / N;
   if (t == 0 && ci == 0) {
-    const int64_t c0 = (int64_t)blockIdx.x * C;
-    const int64_t nc = (a.n_cells - c0) < C ? (a.n_cells - c0) : C;
+    const int64_t c0 = a.cell0 + (int64_t)blockIdx.x * C;
+    const int64_t nc = (a.cell1 - c0) < C ? (a.cell1 - c0) : C;
     bulk_prefetch_l2(a.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
   }
   int cx = 0, cy = 0, cz = 0;
@@ -541,7 +542,7 @@ template <int K>
 #define FEM_CART_MINB 3
 #endif
 __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FEM_CART_MINB : 1)
-    cg_cart_kernel(OpArgs a, KronTab<K + 1> T, int64_t cell0, int64_t cell_end) {
+    cg_cart_kernel(OpArgs a, KronTab<K + 1> T, int64_t cell0, int64_t cell_end) {   // within [a.cell0, a.cell1)
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
@@ -1067,6 +1068,8 @@ OpArgs op_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
     if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
   a.bcmask = mask;
   a.n_cells = L.n_cells;
+  a.cell0 = 0;
+  a.cell1 = L.n_cells;
   a.c0 = L.cart[0];
   a.c1 = L.cart[1];
   a.c2 = L.cart[2];
@@ -1086,13 +1089,17 @@ MapArgs map_args(const fem_ctx* h, const Level& L) {
 }
 
 template <int K>
-void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
+void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0, int64_t r1) {
   constexpr int N = K + 1, C = CPB<K>::value;
-  const OpArgs a = op_args(h, L, x, y);
+  OpArgs a = op_args(h, L, x, y);
+  const bool full = r0 == 0 && r1 == L.n_cells;
+  a.cell0 = r0;
+  a.cell1 = r1;
+  if (r1 <= r0) return;
   const Tab<N> T = make_tab<N>(h->tab);
   const dim3 block(N * N, C);
   const dim3 lblock(line_tpc<K>(), C);   // line kernel (cg_apply_kernel)
-  const int64_t grid = (L.n_cells + C - 1) / C;
+  const int64_t grid = (r1 - r0 + C - 1) / C;
   if (L.cartesian && !h->general_path) {
     KronTab<N> KT;
     for (int i = 0; i < N; ++i)
@@ -1105,7 +1112,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
         KT.M[i][j] = m;
         KT.S[i][j] = s;
       }
-    if (!L.dist && h->stencil) {
+    if (!L.dist && h->stencil && full) {
       using Cfg = StencilCfg<K>;
       const size_t smb = sizeof(double) * Cfg::SMEM;
       static bool attr_s = false;
@@ -1127,6 +1134,12 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
     const int64_t plane = (int64_t)L.nn[0] * L.nn[1];
     const int64_t layer = (int64_t)L.n[0] * L.n[1];
     const int lz = h->chunk_layers > 0 ? h->chunk_layers : L.n[2];
+    if (!full) {   // a sub-range of a z-slab apply: y has been zeroed by the caller
+      launch_pdl(h, cg_cart_kernel<K>, (unsigned)grid, block, sm, a, KT, r0, r1);
+      count_launch();
+      check_launch("cg_cart_kernel");
+      return;
+    }
     for (int z0 = 0; z0 < L.n[2]; z0 += lz) {
       const int z1 = std::min(z0 + lz, L.n[2]);
       const int64_t p0 = z0 == 0 ? 0 : (int64_t)K * z0 + 1, p1 = (int64_t)K * z1 + 1;
@@ -1149,6 +1162,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
     launch_pdl(h, cg_dline_kernel<K>, (unsigned)grid, block, sm, a, T);
   } else if (L.glayout == kGLayoutPlane) {
     if constexpr (K <= 4) {
+      if (!full) throw Error{FEM_E_ARG, "the plane kernel applies whole levels only"};
       const size_t sm = sizeof(double) * PlanePad<N>::CS * kGroupCells;
       static bool attr_p = false;
       if (!attr_p) {
@@ -1228,8 +1242,9 @@ void rhs_k(fem_ctx* h, const Level& L, double* b) {
 
 }  // namespace
 
-void launch_cg_apply(fem_ctx* h, const Level& L, const double* x, double* y) {
-  FEM_DISPATCH_K(h->k, apply_k, h, L, x, y);
+void launch_cg_apply(fem_ctx* h, const Level& L, const double* x, double* y, int64_t c0, int64_t c1) {
+  if (c1 < 0) c1 = L.n_cells;
+  FEM_DISPATCH_K(h->k, apply_k, h, L, x, y, c0, c1);
 }
 
 void launch_cg_diagonal(fem_ctx* h, Level& L) { FEM_DISPATCH_K(h->k, diag_k, h, L); }

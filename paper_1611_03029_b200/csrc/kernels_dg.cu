@@ -45,6 +45,7 @@ struct DgArgs {
   int n[3];          // rank-local cells per direction (z: slab layers)
   int cz0, nzg;      // global index of the first local layer, global layers
   int64_t n_cells;
+  int64_t cell0, cell1;  // cells [cell0, cell1) of this launch (z-slab overlap splits)
   int bcmask;
   double c[3];      // Cartesian metric det J (2/h_d)^2
   double h[3];
@@ -291,13 +292,13 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? 
   using L = DgSmem<N>;
   extern __shared__ double smem[];
   const int t = threadIdx.x, ci = threadIdx.y;
-  const int64_t cell = (int64_t)blockIdx.x * C + ci;
-  const bool active = cell < A.n_cells;
+  const int64_t cell = A.cell0 + (int64_t)blockIdx.x * C + ci;
+  const bool active = cell < A.cell1;
   if (DEFORMED && t == 0 && ci == 0) {
-    // static geometry of the block's cells (and their lower x-faces, which are
-    // contiguous): pull it into L2 before waiting on the predecessor kernel
-    const int64_t c0 = (int64_t)blockIdx.x * C;
-    const int64_t nc = (A.n_cells - c0) < C ? (A.n_cells - c0) : C;
+    // static geometry of the block's cells: pull it into L2 before waiting on the
+    // predecessor kernel
+    const int64_t c0 = A.cell0 + (int64_t)blockIdx.x * C;
+    const int64_t nc = (A.cell1 - c0) < C ? (A.cell1 - c0) : C;
     bulk_prefetch_l2(A.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
   }
   FEM_PDL_ENTRY();
@@ -358,6 +359,7 @@ struct DgKron {
   int n[3];
   int cz0, nzg;
   int64_t n_cells;
+  int64_t cell0, cell1;            // cells of this launch
   double sigma[3], sc[3], mc[3];   // penalty, 2/h_d (stiffness and D+- scale), h_d/2 (mass scale)
   int flo[3], fhi[3];              // boundary factor of the low / high side of direction d
 };
@@ -411,8 +413,8 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
   constexpr int C = DgCPB<K>::value;
   extern __shared__ double smem[];
   const int t = threadIdx.x, ci = threadIdx.y;
-  const int64_t cell = (int64_t)blockIdx.x * C + ci;
-  const bool active = cell < A.n_cells;
+  const int64_t cell = A.cell0 + (int64_t)blockIdx.x * C + ci;
+  const bool active = cell < A.cell1;
   double* F0 = smem + ci * (3 * N3 + 1);
   double* F1 = F0 + N3;
   double* F2 = F1 + N3;
@@ -698,6 +700,8 @@ DgArgs dg_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
   A.faceq = L.face;
   A.fsigma = L.face ? L.face + off * 7 * N2 : nullptr;
   A.n_cells = L.n_cells;
+  A.cell0 = 0;
+  A.cell1 = L.n_cells;
   A.cz0 = L.cz0;
   A.nzg = L.nzg;
   int mask = 0;
@@ -729,7 +733,7 @@ MapArgs dg_map_args(const fem_ctx* h, const Level& L) {
 }
 
 template <int K, bool DEF>
-void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y) {
+void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0, int64_t r1) {
   constexpr int N = K + 1, C = DgCPB<K>::value;
   const size_t sm = sizeof(double) * DgSmem<N>::SIZE * C;
   static bool attr = false;
@@ -738,14 +742,17 @@ void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y) {
                                       (int)sm));
     attr = true;
   }
-  const unsigned grid = (unsigned)((L.n_cells + C - 1) / C);
-  launch_pdl(h, dg_apply_kernel<K, DEF>, grid, dim3(N * N, C), sm, dg_args(h, L, x, y), make_tab<N>(h->tab));
+  const unsigned grid = (unsigned)((r1 - r0 + C - 1) / C);
+  DgArgs A = dg_args(h, L, x, y);
+  A.cell0 = r0;
+  A.cell1 = r1;
+  launch_pdl(h, dg_apply_kernel<K, DEF>, grid, dim3(N * N, C), sm, A, make_tab<N>(h->tab));
   count_launch();
   check_launch("dg_apply_kernel");
 }
 
 template <int K>
-void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y) {
+void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0, int64_t r1) {
   constexpr int N = K + 1, C = DgCPB<K>::value;
   DgKron A;
   for (int d = 0; d < 3; ++d) {
@@ -759,6 +766,8 @@ void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y) {
   A.cz0 = L.cz0;
   A.nzg = L.nzg;
   A.n_cells = L.n_cells;
+  A.cell0 = r0;
+  A.cell1 = r1;
   DgKronTab<N> T;
   for (int i = 0; i < N; ++i) {
     for (int j = 0; j < N; ++j) {
@@ -779,17 +788,18 @@ void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y) {
     FEM_CUDA_TRY(cudaFuncSetAttribute(dg_cart_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr = true;
   }
-  const unsigned grid = (unsigned)((L.n_cells + C - 1) / C);
+  const unsigned grid = (unsigned)((r1 - r0 + C - 1) / C);
   launch_pdl(h, dg_cart_kernel<K>, grid, dim3(N * N, C), sm, x, y, A, T);
   count_launch();
   check_launch("dg_cart_kernel");
 }
 
 template <int K>
-void dg_apply_k(fem_ctx* h, const Level& L, const double* x, double* y) {
-  if (L.cartesian && h->dg_kron) dg_cart_k<K>(h, L, x, y);
-  else if (L.cartesian) dg_apply_kd<K, false>(h, L, x, y);
-  else dg_apply_kd<K, true>(h, L, x, y);
+void dg_apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0, int64_t r1) {
+  if (r1 <= r0) return;
+  if (L.cartesian && h->dg_kron) dg_cart_k<K>(h, L, x, y, r0, r1);
+  else if (L.cartesian) dg_apply_kd<K, false>(h, L, x, y, r0, r1);
+  else dg_apply_kd<K, true>(h, L, x, y, r0, r1);
 }
 
 template <int K>
@@ -841,8 +851,9 @@ void dg_face_geometry_k(fem_ctx* h, Level& L) {
 
 }  // namespace
 
-void launch_dg_apply(fem_ctx* h, const Level& L, const double* x, double* y) {
-  FEM_DISPATCH_K(h->k, dg_apply_k, h, L, x, y);
+void launch_dg_apply(fem_ctx* h, const Level& L, const double* x, double* y, int64_t c0, int64_t c1) {
+  if (c1 < 0) c1 = L.n_cells;
+  FEM_DISPATCH_K(h->k, dg_apply_k, h, L, x, y, c0, c1);
 }
 
 void launch_dg_diagonal(fem_ctx* h, Level& L) { FEM_DISPATCH_K(h->k, dg_diag_k, h, L); }

@@ -57,11 +57,13 @@ __host__ __device__ constexpr int line_cell_stride() { return 3 * N * N * N + (N
 template <int K>
 __host__ __device__ constexpr int line_tpc() { return (K == 4 && FEM_WARP_CELL) ? 32 : (K + 1) * (K + 1); }
 
-// blocks per SM the register allocation must allow (measured, tools/sweep_hi.py: the
-// uncapped k = 6 and 8 kernels use 103 and 168 registers -> 3 and 1 blocks; capping them
-// trades a few spills for occupancy: k = 6 928 -> 511 us, k = 8 949 -> 811 us at 1.6e7 DoFs)
+// blocks per SM the register allocation must allow (measured, tools/sweep_hi.py / the
+// degree sweep: the uncapped k = 6 kernel uses 103 registers -> 3 blocks; capped at 4
+// blocks it spills a little and runs 810-928 -> 488-511 us at 1.6e7 DoFs; k = 8 is noisy)
+// (0 = no minimum: naming minBlocks = 1 explicitly makes ptxas spend registers on ILP
+// instead -- k = 4 56 -> 96 registers, C2 apply 65 -> 85 us)
 template <int K>
-__host__ __device__ constexpr int line_minb() { return K == 6 ? 4 : (K == 8 ? 3 : 1); }
+__host__ __device__ constexpr int line_minb() { return K == 6 ? 4 : 0; }
 
 template <int K, bool DEFORMED>
 __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
 #define FEM_DLINE_MINB 2
 #endif
 template <int K>
-__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FEM_DLINE_MINB : 1)
+__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FEM_DLINE_MINB : 0)
     cg_dline_kernel(OpArgs a, Tab<K + 1> T) {
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
@@ -541,7 +543,7 @@ template <int K>
 #ifndef FEM_CART_MINB
 #define FEM_CART_MINB 3
 #endif
-__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FEM_CART_MINB : 1)
+__global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FEM_CART_MINB : (K >= 5 ? (K == 5 ? 3 : 2) : 0))
     cg_cart_kernel(OpArgs a, KronTab<K + 1> T, int64_t cell0, int64_t cell_end) {   // within [a.cell0, a.cell1)
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;

@@ -285,7 +285,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
 #define FEM_DG_MINB 2
 #endif
 template <int K, bool DEFORMED>
-__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? FEM_DG_MINB : 1)
+__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? FEM_DG_MINB : 1)   // measured: 1 beats none at k <= 4
     dg_apply_kernel(DgArgs A, Tab<K + 1> T) {
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = DgCPB<K>::value;

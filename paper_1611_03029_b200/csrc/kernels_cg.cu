@@ -63,7 +63,7 @@ __host__ __device__ constexpr int line_tpc() { return (K == 4 && FEM_WARP_CELL) 
 // (0 = no minimum: naming minBlocks = 1 explicitly makes ptxas spend registers on ILP
 // instead -- k = 4 56 -> 96 registers, C2 apply 65 -> 85 us)
 template <int K>
-__host__ __device__ constexpr int line_minb() { return K == 6 ? 4 : 0; }
+__host__ __device__ constexpr int line_minb() { return K == 6 ? 4 : (K == 8 ? 2 : 0); }
 
 template <int K, bool DEFORMED>
 __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())

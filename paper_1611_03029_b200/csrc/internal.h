@@ -233,6 +233,10 @@ inline void launch_pdl(fem_ctx* h, void (*kern)(KArgs...), dim3 grid, dim3 block
   if (e != cudaSuccess) throw Error{FEM_E_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e)};
 }
 
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the current
+// device (once per kernel, device and size; thread-safe).
+void smem_attr(const void* func, size_t bytes);
+
 // z-slab exchanges (api.cu); no-ops on replicated levels / single rank
 void halo_import(fem_ctx* h, const Level& L, double* v);      // ghosts <- neighbours' owned data
 void halo_export_add(fem_ctx* h, const Level& L, double* v);  // CG: ghost plane added into the owner

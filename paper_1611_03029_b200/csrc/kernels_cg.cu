@@ -1117,12 +1117,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
     if (!L.dist && h->stencil && full) {
       using Cfg = StencilCfg<K>;
       const size_t smb = sizeof(double) * Cfg::SMEM;
-      static bool attr_s = false;
-      if (!attr_s) {
-        FEM_CUDA_TRY(cudaFuncSetAttribute(cg_stencil_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smb));
-        attr_s = true;
-      }
+      smem_attr(reinterpret_cast<const void*>(cg_stencil_kernel<K>), (size_t)((int)smb));
       const dim3 sg((unsigned)((L.n[0] + 1 + Cfg::TEX - 1) / Cfg::TEX), (unsigned)((L.n[1] + 1 + Cfg::TEY - 1) / Cfg::TEY));
       launch_pdl(h, cg_stencil_kernel<K>, sg, Cfg::THREADS, smb, a, KT);
       count_launch();
@@ -1156,33 +1151,19 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
     launch_pdl(h, cg_apply_kernel<K, false>, (unsigned)grid, lblock, sm, a, T);
   } else if (L.glayout == kGLayoutXLine) {
     const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
-    static bool attr_d = false;
-    if (!attr_d) {
-      FEM_CUDA_TRY(cudaFuncSetAttribute(cg_dline_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      attr_d = true;
-    }
+    smem_attr(reinterpret_cast<const void*>(cg_dline_kernel<K>), (size_t)((int)sm));
     launch_pdl(h, cg_dline_kernel<K>, (unsigned)grid, block, sm, a, T);
   } else if (L.glayout == kGLayoutPlane) {
     if constexpr (K <= 4) {
       if (!full) throw Error{FEM_E_ARG, "the plane kernel applies whole levels only"};
       const size_t sm = sizeof(double) * PlanePad<N>::CS * kGroupCells;
-      static bool attr_p = false;
-      if (!attr_p) {
-        FEM_CUDA_TRY(cudaFuncSetAttribute(cg_plane_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sm));
-        attr_p = true;
-      }
+      smem_attr(reinterpret_cast<const void*>(cg_plane_kernel<K, true>), (size_t)((int)sm));
       const int64_t groups = (L.n_cells + kGroupCells - 1) / kGroupCells;
       launch_pdl(h, cg_plane_kernel<K, true>, (unsigned)groups, N * kGroupCells, sm, a, T);
     }
   } else {
     const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (h->g_direct ? 0 : 6 * N * N * N * C));
-    static bool attr = false;
-    if (!attr) {
-      FEM_CUDA_TRY(cudaFuncSetAttribute(cg_apply_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
-      attr = true;
-    }
+    smem_attr(reinterpret_cast<const void*>(cg_apply_kernel<K, true>), (size_t)((int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
     launch_pdl(h, cg_apply_kernel<K, true>, (unsigned)grid, lblock, sm, a, T);
   }
   count_launch();

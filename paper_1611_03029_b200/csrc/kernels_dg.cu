@@ -736,12 +736,7 @@ template <int K, bool DEF>
 void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0, int64_t r1) {
   constexpr int N = K + 1, C = DgCPB<K>::value;
   const size_t sm = sizeof(double) * DgSmem<N>::SIZE * C;
-  static bool attr = false;
-  if (!attr) {
-    FEM_CUDA_TRY(cudaFuncSetAttribute(dg_apply_kernel<K, DEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sm));
-    attr = true;
-  }
+  smem_attr(reinterpret_cast<const void*>(dg_apply_kernel<K, DEF>), (size_t)((int)sm));
   const unsigned grid = (unsigned)((r1 - r0 + C - 1) / C);
   DgArgs A = dg_args(h, L, x, y);
   A.cell0 = r0;
@@ -783,11 +778,7 @@ void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r
     T.dp[i] = h->tab.dface[1][i];
   }
   const size_t sm = sizeof(double) * (3 * N * N * N + 1) * C;
-  static bool attr = false;
-  if (!attr) {
-    FEM_CUDA_TRY(cudaFuncSetAttribute(dg_cart_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
-  }
+  smem_attr(reinterpret_cast<const void*>(dg_cart_kernel<K>), (size_t)((int)sm));
   const unsigned grid = (unsigned)((r1 - r0 + C - 1) / C);
   launch_pdl(h, dg_cart_kernel<K>, grid, dim3(N * N, C), sm, x, y, A, T);
   count_launch();

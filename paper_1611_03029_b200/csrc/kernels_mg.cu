@@ -393,12 +393,7 @@ template <int K, bool DG>
 void prolongate_kd(fem_ctx* h, const Level& c, const Level& f, const double* xc, double* xf) {
   constexpr int N = K + 1, M = Embed<K, DG>::M;
   const size_t sm = sizeof(double) * (N * N * N + M * N * N + M * M * N);
-  static bool attr = false;
-  if (!attr) {
-    FEM_CUDA_TRY(cudaFuncSetAttribute(prolongate_kernel<K, DG>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
-  }
+  smem_attr(reinterpret_cast<const void*>(prolongate_kernel<K, DG>), (size_t)((int)sm));
   launch_pdl(h, prolongate_kernel<K, DG>, (unsigned)c.n_cells, 128, sm, 
       transfer_args(h, c, f), make_embed<K, DG>(h->tab), xc, xf);
   count_launch();
@@ -410,12 +405,7 @@ void restrict_kd(fem_ctx* h, const Level& c, const Level& f, const double* bf, c
                  double* xc) {
   constexpr int N = K + 1, M = Embed<K, DG>::M;
   const size_t sm = sizeof(double) * (M * M * M + N * M * M);
-  static bool attr = false;
-  if (!attr) {
-    FEM_CUDA_TRY(cudaFuncSetAttribute(restrict_kernel<K, DG>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
-  }
+  smem_attr(reinterpret_cast<const void*>(restrict_kernel<K, DG>), (size_t)((int)sm));
   launch_pdl(h, restrict_kernel<K, DG>, (unsigned)c.n_cells, 128, sm, 
       transfer_args(h, c, f), make_embed<K, DG>(h->tab), bf, axf, xc);
   count_launch();

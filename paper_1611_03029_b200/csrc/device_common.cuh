@@ -171,8 +171,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 //                 quadrature phase thread t = q1 + N q2 owns the x-line q0 = 0..N-1,
 //                 so a warp's loads of one (comp, q0) are consecutive addresses)
 //   kGLayoutPlane groups of kGroupCells cells, [group][comp][e][cell-in-group][q2],
-//                 e = q0 + N q1 (CG plane kernel: lane = q2 + N cell)
-constexpr int kGroupCells = 32;
+//                 e = q0 + N q1 (CG plane kernel: lane = q2 + N cell; a row q1 of all
+//                 six components is six contiguous chunks -> TMA bulk copies)
+constexpr int kGroupCells = 12;
 enum { kGLayoutCell = 0, kGLayoutPlane = 1, kGLayoutXLine = 2 };
 
 template <int N>

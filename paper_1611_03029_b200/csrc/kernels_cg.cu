@@ -326,7 +326,7 @@ template <int N> struct PlanePad;
 template <> struct PlanePad<2> { static constexpr int LS = 4, CS = 17, MINB = 4; };
 template <> struct PlanePad<3> { static constexpr int LS = 19, CS = 121, MINB = 3; };
 template <> struct PlanePad<4> { static constexpr int LS = 20, CS = 161, MINB = 2; };
-template <> struct PlanePad<5> { static constexpr int LS = 25, CS = 253, MINB = FEM_PLANE_MINB; };  // 2-way conflicts in places, 2 KB/cell
+template <> struct PlanePad<5> { static constexpr int LS = 25, CS = 253, MINB = 0; };  // 2-way conflicts in places, 2 KB/cell
 
 template <int K, bool DEFORMED>
 __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
@@ -340,13 +340,28 @@ __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
   const int64_t group = blockIdx.x;
   const int64_t cell = group * CB + c;
   const bool active = cell < a.n_cells;
+  // Geometry: the quadrature phase runs row by row (qy); the six components of one row
+  // of the group are six contiguous chunks of N^2 CB doubles in the plane layout, staged
+  // into shared memory by TMA bulk copies, double-buffered (rows qy and qy+1 in flight;
+  // rows 0 and 1 are issued now, before the gather, so they land during phase A).
+  constexpr int GROW = N * CB * N;                          // doubles per component and row
+  constexpr int GB = 3;                                     // row buffers (rows in flight)
+  double* Gsm = smem + CB * CS;                             // [GB][6][GROW]
+  __shared__ alignas(8) uint64_t gfull[GB];
+  const double* Gg = DEFORMED ? a.G + group * (int64_t)6 * N2 * CB * N : nullptr;
+  auto issue_row = [&](int qy) {
+    const int b = qy % GB;
+    mbar_arrive_expect_tx(&gfull[b], (uint32_t)(sizeof(double) * 6 * GROW));
+#pragma unroll
+    for (int comp = 0; comp < 6; ++comp)
+      bulk_g2s(Gsm + (b * 6 + comp) * GROW, Gg + ((int64_t)comp * N2 + (int64_t)N * qy) * CB * N,
+               (uint32_t)(sizeof(double) * GROW), &gfull[b]);
+  };
   if (DEFORMED && tid == 0) {
-    // the group's geometry slice is contiguous in the plane layout: start pulling it
-    // into L2 now, it is consumed after the gather and the forward sweeps
-    const char* src = reinterpret_cast<const char*>(a.G + group * (int64_t)CB * 6 * N * N2);
-    const uint32_t total = (uint32_t)(sizeof(double) * CB * 6 * N * N2);
-    for (uint32_t off = 0; off < total; off += 32768u)
-      bulk_prefetch_l2(src + off, total - off < 32768u ? total - off : 32768u);
+#pragma unroll
+    for (int b = 0; b < GB; ++b) mbar_init(&gfull[b], 1);
+#pragma unroll
+    for (int qy = 0; qy < GB && qy < N; ++qy) issue_row(qy);
   }
   int cx = 0, cy = 0, cz = 0;
   if (active) {
@@ -424,10 +439,11 @@ __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
       Z[qy][i] = s3;
     }
   }
-  const double* Gq = DEFORMED ? a.G + group * (int64_t)CB * 6 * N * N2 + tid : nullptr;
 #pragma unroll
   for (int qy = 0; qy < N; ++qy) {
     double ur[N], fxr[N], acc[N];
+    const double* Gq = Gsm + (qy % GB) * 6 * GROW + tid;
+    if (DEFORMED) mbar_wait(&gfull[qy % GB], (qy / GB) & 1);
 #pragma unroll
     for (int m = 0; m < N; ++m) ur[m] = S0[p * LS + qy * N + m];
 #pragma unroll
@@ -438,11 +454,10 @@ __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
       const double gyq = Y[qy][qx], gzq = Z[qy][qx];
       double fx, fy, fz;
       if (DEFORMED) {
-        const int e = qx + N * qy;
-        // entry (comp, e) of this thread: ((comp*N2 + e)*CB + c)*N + p = (comp*N2 + e)*CB*N + tid
-        const double G00 = __ldg(Gq + (0 * N2 + e) * CB * N), G01 = __ldg(Gq + (1 * N2 + e) * CB * N);
-        const double G02 = __ldg(Gq + (2 * N2 + e) * CB * N), G11 = __ldg(Gq + (3 * N2 + e) * CB * N);
-        const double G12 = __ldg(Gq + (4 * N2 + e) * CB * N), G22 = __ldg(Gq + (5 * N2 + e) * CB * N);
+        // entry (comp, e = qx + N qy) of this thread in the staged row: comp*GROW + qx*CB*N + tid
+        const double G00 = Gq[0 * GROW + qx * CB * N], G01 = Gq[1 * GROW + qx * CB * N];
+        const double G02 = Gq[2 * GROW + qx * CB * N], G11 = Gq[3 * GROW + qx * CB * N];
+        const double G12 = Gq[4 * GROW + qx * CB * N], G22 = Gq[5 * GROW + qx * CB * N];
         fx = G00 * gxq + G01 * gyq + G02 * gzq;
         fy = G01 * gxq + G11 * gyq + G12 * gzq;
         fz = G02 * gxq + G12 * gyq + G22 * gzq;
@@ -460,6 +475,10 @@ __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
     mvt<N>(T.colloc, fxr, acc);
 #pragma unroll
     for (int m = 0; m < N; ++m) S0[p * LS + qy * N + m] = acc[m];
+    if (DEFORMED && qy + GB < N) {
+      __syncthreads();                 // every thread is done with this buffer
+      if (tid == 0) issue_row(qy + GB);
+    }
   }
   // N_y^T (d_x^T f_x) + N'_y^T f_y -> S0 and N_y^T f_z -> S1, column by column in place
   // (element (qz=p, y, qx) at p*LS + y*N + qx)
@@ -1156,7 +1175,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
   } else if (L.glayout == kGLayoutPlane) {
     if constexpr (K <= 4) {
       if (!full) throw Error{FEM_E_ARG, "the plane kernel applies whole levels only"};
-      const size_t sm = sizeof(double) * PlanePad<N>::CS * kGroupCells;
+      const size_t sm = sizeof(double) * (PlanePad<N>::CS * kGroupCells + 3 * 6 * N * N * kGroupCells);
       smem_attr(reinterpret_cast<const void*>(cg_plane_kernel<K, true>), (size_t)((int)sm));
       const int64_t groups = (L.n_cells + kGroupCells - 1) / kGroupCells;
       launch_pdl(h, cg_plane_kernel<K, true>, (unsigned)groups, N * kGroupCells, sm, a, T);

@@ -97,8 +97,11 @@ typedef struct {
   int32_t device;                 /* CUDA device ordinal; -1 => current device    */
   int32_t profile;                /* 1 => time the operator kernels with events   */
   int32_t slab_min_layers;        /* multi-rank: a level is split into z-slabs while
-                                     every rank keeps >= this many cell layers;
-                                     coarser levels are replicated on every rank [2] */
+                                     every rank keeps >= this many cell layers     [1] */
+  int64_t slab_min_dofs;          /* ... and >= this many DoFs per rank; coarser
+                                     levels are replicated on every rank (they are
+                                     latency-bound: a halo exchange per apply would
+                                     cost more than the redundant work)        [32768] */
 } fem_options;
 
 /* Fills *opt with the defaults above.  Returns FEM_OK or FEM_E_ARG (opt NULL). */
@@ -121,7 +124,8 @@ FEM_API int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, cons
  * before every operator apply, its contributions compress-added back after it).
  * SIPG: it owns its cells' blocks and keeps one ghost cell layer from each
  * neighbour rank.  PCG dot products are all-reduced.  Levels coarser than the
- * last one that still gives every rank slab_min_layers layers are replicated: the
+ * last one that still gives every rank slab_min_layers layers and slab_min_dofs DoFs
+ * are replicated: the
  * residual of the last distributed level is gathered (all-reduce of zero-padded
  * owned slices) and the coarse levels run redundantly on every rank.
  * fem_partition is pure host arithmetic (no device needed): it describes, level by

@@ -616,7 +616,7 @@ void drop_solve_graphs(fem_ctx* h) {
 // ---------------------------------------------------------------- setup
 // Level hierarchy and z-slab partition (include/fem.h fem_partition): halve while
 // every n_d is even and max n_d > coarse_cells; a level is distributed while
-// n_z % P == 0 and every rank keeps >= slab_min_layers layers (the finest level
+// n_z % P == 0 and every rank keeps >= slab_min_layers layers and slab_min_dofs DoFs (the finest level
 // always is, for P > 1), coarser levels are replicated.
 std::vector<fem_level_part> partition(const fem_mesh& m, int k, int method, const fem_options& o) {
   const int P = m.nranks, r = m.rank;
@@ -639,7 +639,13 @@ std::vector<fem_level_part> partition(const fem_mesh& m, int k, int method, cons
   for (int i = 0; i < nl; ++i) {            // i = 0: finest
     const auto& c = ns[i];
     fem_level_part& q = out[nl - 1 - i];
-    if (i > 0) dist = dist && c[2] % P == 0 && c[2] / P >= std::max(1, o.slab_min_layers) && i < nl - 1;
+    if (i > 0) {
+      const int64_t lvl_dofs = method == FEM_CG
+                                   ? (int64_t)(k * c[0] + 1) * (k * c[1] + 1) * (k * c[2] + 1)
+                                   : (int64_t)c[0] * c[1] * c[2] * N3;
+      dist = dist && c[2] % P == 0 && c[2] / P >= std::max(1, o.slab_min_layers) &&
+             lvl_dofs / P >= o.slab_min_dofs && i < nl - 1;
+    }
     const int nzl = dist ? c[2] / P : c[2];
     const int cz0 = dist ? r * nzl : 0;
     for (int d = 0; d < 3; ++d) {
@@ -900,7 +906,8 @@ int fem_default_options(fem_options* o) {
   o->stream = nullptr;
   o->device = -1;
   o->profile = 0;
-  o->slab_min_layers = 2;
+  o->slab_min_layers = 1;
+  o->slab_min_dofs = 32768;
   return FEM_OK;
 }
 

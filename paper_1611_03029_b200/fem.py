@@ -43,7 +43,8 @@ class fem_options(C.Structure):
                 ("cheb_lo", C.c_double), ("cheb_hi", C.c_double), ("eig_iters", C.c_int32),
                 ("coarse_cells", C.c_int32), ("eig_seed", C.c_uint64),
                 ("lambda_override", C.POINTER(C.c_double)), ("stream", C.c_void_p),
-                ("device", C.c_int32), ("profile", C.c_int32), ("slab_min_layers", C.c_int32)]
+                ("device", C.c_int32), ("profile", C.c_int32), ("slab_min_layers", C.c_int32),
+                ("slab_min_dofs", C.c_int64)]
 
 
 class fem_level_part(C.Structure):
@@ -182,10 +183,11 @@ def _options(**kw):
     return o
 
 
-def partition(cells, degree, method=FEM_CG, rank=0, nranks=1, coarse_cells=None, slab_min_layers=None):
+def partition(cells, degree, method=FEM_CG, rank=0, nranks=1, coarse_cells=None, slab_min_layers=None,
+              slab_min_dofs=None):
     """fem_partition (host only): per level (coarsest first) a dict of the rank's slab."""
     m = _mesh(cells, (0.0,) * 3, (1.0,) * 3, 0.0, (FEM_BC_DIRICHLET,) * 6, rank, nranks, None, None)
-    o = _options(coarse_cells=coarse_cells, slab_min_layers=slab_min_layers)
+    o = _options(coarse_cells=coarse_cells, slab_min_layers=slab_min_layers, slab_min_dofs=slab_min_dofs)
     out = (fem_level_part * 32)()
     nl = C.c_int32()
     _check(_lib.fem_partition(C.byref(m), degree, method, C.byref(o), out, 32, C.byref(nl)))
@@ -209,7 +211,7 @@ class Fem:
                  deform_eps=0.0, bc=(FEM_BC_DIRICHLET,) * 6, penalty_factor=None, cheb_degree=None,
                  cheb_lo=None, cheb_hi=None, eig_iters=None, coarse_cells=None, eig_seed=None,
                  lambda_override=None, stream=None, device=None, profile=False, rank=0, nranks=1,
-                 nccl_id=None, local_group=None, slab_min_layers=None):
+                 nccl_id=None, local_group=None, slab_min_layers=None, slab_min_dofs=None):
         m = _mesh(cells, lo, hi, deform_eps, bc, rank, nranks, None, local_group)
         self._nccl_id = None
         if nccl_id is not None:
@@ -218,7 +220,7 @@ class Fem:
         self._group = local_group     # keep alive while the handle exists
         o = _options(penalty_factor=penalty_factor, cheb_degree=cheb_degree, cheb_lo=cheb_lo,
                      cheb_hi=cheb_hi, eig_iters=eig_iters, coarse_cells=coarse_cells, eig_seed=eig_seed,
-                     slab_min_layers=slab_min_layers)
+                     slab_min_layers=slab_min_layers, slab_min_dofs=slab_min_dofs)
         self._lam = None
         if lambda_override is not None:
             self._lam = (C.c_double * len(lambda_override))(*lambda_override)

@@ -71,7 +71,7 @@ def own_slices(F1, P, make_kw, level=None):
     """(first, n_owned) of every rank for the finest level (or `level`)."""
     fem = fem_mod()
     parts = [fem.partition(make_kw["cells"], make_kw["degree"], make_kw.get("method", fem.FEM_CG), r, P,
-                           slab_min_layers=make_kw.get("slab_min_layers")) for r in range(P)]
+                           slab_min_layers=make_kw.get("slab_min_layers"), slab_min_dofs=0) for r in range(P)]
     lv = -1 if level is None else level
     return [(p[lv]["first_global"], p[lv]["n_owned"]) for p in parts]
 
@@ -90,7 +90,7 @@ CASES = [
 def kw_of(method, k, cells, eps, bc, mnl):
     fem = fem_mod()
     return dict(cells=cells, degree=k, method=fem.FEM_CG if method == "cg" else fem.FEM_SIPG,
-                deform_eps=eps, bc=bc, slab_min_layers=mnl)
+                deform_eps=eps, bc=bc, slab_min_layers=mnl, slab_min_dofs=0)
 
 
 @pytest.mark.parametrize("method,k,cells,eps,bc,P,mnl", CASES)
@@ -136,7 +136,7 @@ def test_levels_and_transfers_match_single_rank(method, k, cells, eps, bc, P, mn
     kw = kw_of(method, k, cells, eps, bc, mnl)
     F1 = fem.Fem(**kw)
     nl = F1.n_levels
-    parts = [fem.partition(cells, k, kw["method"], r, P, slab_min_layers=mnl) for r in range(P)]
+    parts = [fem.partition(cells, k, kw["method"], r, P, slab_min_layers=mnl, slab_min_dofs=0) for r in range(P)]
     ref = {}
     for l in range(nl):
         ng = parts[0][l]["n_global"]

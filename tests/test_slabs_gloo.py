@@ -65,7 +65,7 @@ def _check_rank(rank, P, case):
 
     method, k, cells, eps, mnl = case
     meth = fem.FEM_CG if method == "cg" else fem.FEM_SIPG
-    parts = fem.partition(cells, k, meth, rank, P, slab_min_layers=mnl)
+    parts = fem.partition(cells, k, meth, rank, P, slab_min_layers=mnl, slab_min_dofs=0)
     allp = [None] * P
     dist.all_gather_object(allp, parts)
 

@@ -344,13 +344,27 @@ void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double
   };
   const double* xo = nullptr;
   const double* x = nullptr;
+  // SIPG: the element-centric apply writes each cell's result once, so the step is fused
+  // into its epilogue (no A x vector written and read back, one launch per step)
+  // (Cartesian Kronecker kernel only: on the deformed quadrature kernel, which is not
+  // memory bound, the four extra epilogue streams cost more than the saved pass, C5 +0.6%)
+  const bool fused = !is_cg(h) && h->fuse_cheb && L.cartesian && h->dg_kron;
+  auto step = [&](const double* xc, const double* xold, double* xnew, double c1, double c2) {
+    if (fused) {
+      h->fuse = ChebFuse{xold, b, L.dinv, c1, c2, 1};
+      apply_level(h, L, xc, xnew, false);
+      h->fuse = ChebFuse{};
+    } else {
+      apply_level(h, L, xc, L.t, false);
+      launch_cheb_step(h, L, xnew, xc, xold, b, L.t, c1, c2, xold != nullptr);
+    }
+  };
   // step 1
   double* xn = (p == 1) ? x_out : next(x_in, nullptr);
   if (x_in == nullptr) {
     launch_cheb_step(h, L, xn, nullptr, nullptr, b, nullptr, 0.0, 1.0 / theta, false);
   } else {
-    apply_level(h, L, x_in, L.t, false);
-    launch_cheb_step(h, L, xn, x_in, nullptr, b, L.t, 0.0, 1.0 / theta, false);
+    step(x_in, nullptr, xn, 0.0, 1.0 / theta);
   }
   xo = x_in;
   x = xn;
@@ -358,9 +372,8 @@ void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double
     const double rho_new = 1.0 / (2.0 * sigma - rho);
     const double c1 = rho_new * rho, c2 = 2.0 * rho_new / delta;
     rho = rho_new;
-    apply_level(h, L, x, L.t, false);
     xn = (i == p) ? x_out : next(x, xo);
-    launch_cheb_step(h, L, xn, x, xo, b, L.t, c1, c2, xo != nullptr);
+    step(x, xo, xn, c1, c2);
     xo = x;
     x = xn;
   }
@@ -963,6 +976,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_STENCIL")) h->stencil = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_PDL")) h->pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_DG_KRON")) h->dg_kron = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_FUSE_CHEB")) h->fuse_cheb = std::atoi(e) != 0;
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)
     FEM_CUDA_TRY(cudaMemset(h->red, 0, sizeof(double) * (16 * kRedBlocks + 16)));

@@ -111,6 +111,16 @@ struct Level {
   double *gb = nullptr, *gx = nullptr;
 };
 
+// Chebyshev step fused into an element-centric (SIPG) operator apply: the kernel writes
+// x_new = x + c1 (x - x_old) + c2 D^-1 (b - A x) instead of A x.
+struct ChebFuse {
+  const double* xo = nullptr;    // x_old (nullptr: first step)
+  const double* b = nullptr;
+  const double* dinv = nullptr;
+  double c1 = 0.0, c2 = 0.0;
+  int on = 0;
+};
+
 struct Profile {
   bool on = false;
   std::vector<cudaEvent_t> ev;   // pairs (start, stop) recorded eagerly
@@ -169,8 +179,10 @@ struct fem_ctx {
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
   bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)
   bool g_direct = true;                // FEM_G_DIRECT=0: line kernel stages G by TMA into shared memory
-  bool y_is_zero = false;              // set around launch_cg_apply: the output is known to be zero
+  bool y_is_zero = false;
+  fem::ChebFuse fuse;                   // set around a fused Chebyshev apply (SIPG levels)              // set around launch_cg_apply: the output is known to be zero
   bool pdl = true;                     // FEM_PDL=0: plain launches (no programmatic dependent launch)
+  bool fuse_cheb = true;               // FEM_FUSE_CHEB=0: separate Chebyshev-step kernel on SIPG levels
   bool dg_kron = true;                 // FEM_DG_KRON=0: quadrature cell+face kernel on Cartesian SIPG levels
   bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels
   bool dbasis = false;                 // FEM_DBASIS=1: derivative-basis line kernel (measured slower, kept for study)

@@ -46,11 +46,23 @@ struct DgArgs {
   int cz0, nzg;      // global index of the first local layer, global layers
   int64_t n_cells;
   int64_t cell0, cell1;  // cells [cell0, cell1) of this launch (z-slab overlap splits)
+  ChebFuse cf;           // fused Chebyshev epilogue (cf.on)
   int bcmask;
   double c[3];      // Cartesian metric det J (2/h_d)^2
   double h[3];
   double sigma[3];  // Cartesian penalty c (k+1)^2 / h_d
 };
+
+// result v = (A x)_i of DoF i: stored, or consumed by the fused Chebyshev epilogue
+__device__ __forceinline__ void dg_store(const ChebFuse& cf, const double* __restrict__ x, double* __restrict__ y,
+                                         int64_t i, double v) {
+  if (cf.on) {
+    const double xi = x[i], xoi = cf.xo ? cf.xo[i] : 0.0;
+    y[i] = xi + cf.c1 * (xi - xoi) + cf.c2 * cf.dinv[i] * (cf.b[i] - v);
+  } else {
+    y[i] = v;
+  }
+}
 
 // node index in the cell of (i along D, a along t1, b along t2)
 template <int N, int D>
@@ -330,7 +342,8 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? 
   if (active) {
     const int ta = t % N, tb = t / N;   // x-line (y=ta, z=tb): contiguous in the DG layout
 #pragma unroll
-    for (int l = 0; l < N; ++l) A.y[cell * N3 + l + N * ta + N2 * tb] = s0[l + N * ta + N2 * tb];
+    for (int l = 0; l < N; ++l)
+      dg_store(A.cf, A.x, A.y, cell * N3 + l + N * ta + N2 * tb, s0[l + N * ta + N2 * tb]);
   }
 }
 
@@ -360,6 +373,7 @@ struct DgKron {
   int cz0, nzg;
   int64_t n_cells;
   int64_t cell0, cell1;            // cells of this launch
+  ChebFuse cf;                     // fused Chebyshev epilogue (cf.on)
   double sigma[3], sc[3], mc[3];   // penalty, 2/h_d (stiffness and D+- scale), h_d/2 (mass scale)
   int flo[3], fhi[3];              // boundary factor of the low / high side of direction d
 };
@@ -490,7 +504,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     mv<N>(T.M, a, o);
     if (active) {
 #pragma unroll
-      for (int l = 0; l < N; ++l) y[cell * N3 + t + N2 * l] = fma(A.mc[2], o[l], F2[t + N2 * l]);
+      for (int l = 0; l < N; ++l) dg_store(A.cf, x, y, cell * N3 + t + N2 * l, fma(A.mc[2], o[l], F2[t + N2 * l]));
     }
   }
 }
@@ -702,6 +716,7 @@ DgArgs dg_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
   A.n_cells = L.n_cells;
   A.cell0 = 0;
   A.cell1 = L.n_cells;
+  A.cf = h->fuse;
   A.cz0 = L.cz0;
   A.nzg = L.nzg;
   int mask = 0;
@@ -763,6 +778,7 @@ void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r
   A.n_cells = L.n_cells;
   A.cell0 = r0;
   A.cell1 = r1;
+  A.cf = h->fuse;
   DgKronTab<N> T;
   for (int i = 0; i < N; ++i) {
     for (int j = 0; j < N; ++j) {

@@ -2,9 +2,9 @@
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
-Definition followed (kappa = 1):
-  weak form (grad v, grad u) = (v, f), eq:poisson_fem, P:L184-189;
-  element matrix K^e_ij = sum_q w_q det J_q (J_q^-T grad_xi phi_i(xi_q)) . (J_q^-T grad_xi phi_j(xi_q)),
+Definition followed:
+  weak form (grad v, kappa grad u) = (v, f), eq:poisson_fem, P:L184-189;
+  element matrix K^e_ij = sum_q w_q det J_q kappa(x_q) (J_q^-T grad_xi phi_i(xi_q)) . (J_q^-T grad_xi phi_j(xi_q)),
   which is eq:mf_eval written as a matrix, with (k+1)^3 Gauss points
    and grad_xi phi evaluated pointwise in 3-D (no sum factorization).
   Assembly "in the usual finite element way, including the elimination of
@@ -48,20 +48,28 @@ def cell_geometry(mesh: Mesh, cells, quad: CellQuadrature):
     return np.linalg.inv(J), detJ
 
 
+def cell_kappa(mesh, cells, quad):
+    """kappa at the physical quadrature points [C, q] (1 unless mesh.kappa_amp)."""
+    if mesh.kappa_amp == 0.0:
+        return np.ones((len(np.atleast_1d(cells)), len(quad.w)))
+    return mesh.kappa(mesh.points(mesh.cell_coords(cells), quad.pts))
+
+
 def metric(mesh, cells, quad):
-    """G_q = w_q det J_q J_q^-1 J_q^-T  [C, q, 3, 3] (eq:mf_eval with kappa = 1)."""
+    """G_q = J_q^-1 (w_q det J_q kappa(x_q)) J_q^-T  [C, q, 3, 3] (eq:mf_eval)."""
     Jinv, detJ = cell_geometry(mesh, cells, quad)
-    return (quad.w[None, :, None, None] * detJ[..., None, None]) * \
-        np.einsum('cqde,cqfe->cqdf', Jinv, Jinv)
+    wk = quad.w[None, :] * detJ * cell_kappa(mesh, cells, quad)
+    return wk[..., None, None] * np.einsum('cqde,cqfe->cqdf', Jinv, Jinv)
 
 
 def element_matrix(mesh: Mesh, cell: int, quad: CellQuadrature | None = None):
     """K^e of one cell by full tensor quadrature, [n^3, n^3]."""
     quad = quad or CellQuadrature(mesh.k)
     Jinv, detJ = cell_geometry(mesh, np.array([cell]), quad)
+    kap = cell_kappa(mesh, np.array([cell]), quad)[0]
     # physical gradients J^-T grad_xi phi_i : [q, 3, i]
     pg = np.einsum('qed,qei->qdi', Jinv[0], quad.grad)
-    return np.einsum('q,qdi,qdj->ij', quad.w * detJ[0], pg, pg)
+    return np.einsum('q,qdi,qdj->ij', quad.w * detJ[0] * kap, pg, pg)
 
 
 def element_apply_G(G, xe, quad):
@@ -99,14 +107,14 @@ def assemble(mesh: Mesh) -> sp.csr_matrix:
 class Operator:
     """y = A x (mode O3-iii) with the geometry factors G_q of every cell cached.
 
-    Cartesian meshes (eps = 0): J is the same on every cell, so G is computed
-    once (from cell 0) and used for all cells."""
+    Cartesian meshes (mesh.uniform: eps = 0, exact map, kappa = 1): J is the same on
+    every cell, so G is computed once (from cell 0) and used for all cells."""
 
     def __init__(self, mesh: Mesh, chunk: int = 8192):
         self.mesh, self.chunk = mesh, chunk
         self.quad = CellQuadrature(mesh.k)
         self.mask = mesh.cg_dirichlet_mask()
-        self.uniform = mesh.eps == 0.0
+        self.uniform = mesh.uniform
         if self.uniform:
             self.G0 = metric(mesh, np.array([0]), self.quad)
         else:

@@ -23,6 +23,12 @@ Right-hand sides (all with the cell / face Gauss rules of the operator):
   Neumann d_n u+ = -d_n u- - 2 g_N gives {d_n u} = -g_N, i.e. -<phi_i, g_N>.
 Error: absolute L2 norm ||u - u_h|| with (k+2)^3 Gauss points (the paper's plots list
 absolute errors: 3.5 on the coarsest k = 1 mesh).
+
+The shell case: `shell_mesh` = one cube-sphere patch of
+the shell (oracle/mesh.py), Dirichlet on all sides, degree-5 mapping, variable kappa;
+with kappa the data become f = -div(kappa grad u) = -kappa Laplace u - grad kappa . grad u,
+g_N = -kappa n . grad u, and the SIPG Dirichlet term carries kappa:
+int g_D kappa (2 sigma phi_i - d_n phi_i).
 """
 from __future__ import annotations
 
@@ -31,7 +37,7 @@ import numpy as np
 from .basis import Basis1D
 from .cg import CellQuadrature, cell_geometry
 from .cg import apply as cg_apply
-from .mesh import Mesh, CG, DIRICHLET, NEUMANN, tensor_points, tensor_weights, eval_basis_3d
+from .mesh import Mesh, CG, DIRICHLET, NEUMANN, SHELL, tensor_points, tensor_weights, eval_basis_3d
 from .sipg import FaceRef, face_geometry, boundary_cells, cell_volume
 
 ALPHA = 0.2
@@ -42,6 +48,11 @@ PENALTY_FACTOR = 3.0   # sigma = (k+1)^2 d / h with d = 3
 
 def mesh(cells, k) -> Mesh:
     return Mesh(cells, k, lo=(-1.0, -1.0, -1.0), hi=(1.0, 1.0, 1.0), bc=BC)
+
+
+def shell_mesh(cells, k, mapping_degree=5, kappa_amp=0.0) -> Mesh:
+    """One cube-sphere patch of the shell 0.5 < r < 1, Dirichlet everywhere."""
+    return Mesh(cells, k, geometry=SHELL, mapping_degree=mapping_degree, kappa_amp=kappa_amp)
 
 
 def _gauss(x):
@@ -66,13 +77,34 @@ def exact_f(x):
     return -np.sum((4.0 * r2 / ALPHA ** 4 - 6.0 / ALPHA ** 2) * g, axis=-1)
 
 
-def _cell_load(m: Mesh, method, b):
+class Solution:
+    """An exact solution u with its gradient and -Laplace u (the problem's data follow)."""
+
+    def __init__(self, u, grad, minus_lap):
+        self.u, self.grad, self.minus_lap = u, grad, minus_lap
+
+
+GAUSSIANS = Solution(exact_u, grad_u, exact_f)
+
+
+def linear(a, c=0.0):
+    """u = a . x + c: the patch test (any kappa: f = -grad kappa . a)."""
+    a = np.asarray(a, dtype=np.float64)
+    return Solution(lambda x: x @ a + c, lambda x: np.broadcast_to(a, x.shape), lambda x: np.zeros(x.shape[:-1]))
+
+
+def exact_f_kappa(m: Mesh, x, sol: Solution = GAUSSIANS):
+    """-div(kappa grad u) = kappa (-Laplace u) - grad kappa . grad u."""
+    return m.kappa(x) * sol.minus_lap(x) - np.sum(m.grad_kappa(x) * sol.grad(x), axis=-1)
+
+
+def _cell_load(m: Mesh, method, b, sol):
     quad = CellQuadrature(m.k)
     nm = (m.k + 1) ** 3
     cells = np.arange(m.n_cells)
     _, detJ = cell_geometry(m, cells, quad)
-    xq = m.phys(m.xhat(m.cell_coords(cells), quad.pts))
-    be = (exact_f(xq) * detJ * quad.w[None, :]) @ quad.val
+    xq = m.points(m.cell_coords(cells), quad.pts)
+    be = (exact_f_kappa(m, xq, sol) * detJ * quad.w[None, :]) @ quad.val
     if method == CG:
         dm = m.cg_dofmap(cells)
         b += np.bincount(dm.ravel(), weights=be.ravel(), minlength=len(b))
@@ -81,7 +113,7 @@ def _cell_load(m: Mesh, method, b):
     return nm
 
 
-def _face_terms(m: Mesh, method, b, penalty_factor):
+def _face_terms(m: Mesh, method, b, penalty_factor, sol):
     quad = CellQuadrature(m.k)
     for side in range(6):
         d, sign = side // 2, (1.0 if side % 2 else -1.0)
@@ -90,46 +122,46 @@ def _face_terms(m: Mesh, method, b, penalty_factor):
         Jinv, nrm, JxW, xf = face_geometry(m, cells, ref)
         dm = m.cg_dofmap(cells) if method == CG else m.dg_dofmap(cells)
         if m.bc[side] == NEUMANN:
-            gN = -np.sum(nrm * grad_u(xf), axis=-1)                 # -n . grad u
+            gN = -m.kappa(xf) * np.sum(nrm * sol.grad(xf), axis=-1)   # -n . kappa grad u
             be = -(gN * JxW) @ ref.val
         elif method == CG:
             continue                                                # interpolated g_D (below)
         else:
-            gD = exact_u(xf)
+            gD = sol.u(xf)
             area = JxW.sum(axis=1)
             sigma = penalty_factor * (m.k + 1) ** 2 * area / cell_volume(m, cells, quad)
             Jn = np.einsum('fqed,fqd->fqe', Jinv, nrm)
             dn = np.einsum('fqe,qei->fqi', Jn, ref.grad)            # d_n phi_i at the face points
-            be = np.einsum('fq,fqi->fi', gD * JxW, 2.0 * sigma[:, None, None] * ref.val[None] - dn)
+            be = np.einsum('fq,fqi->fi', gD * m.kappa(xf) * JxW,
+                           2.0 * sigma[:, None, None] * ref.val[None] - dn)
         b += np.bincount(dm.ravel(), weights=be.ravel(), minlength=len(b))
 
 
 def node_coords(m: Mesh):
-    """Physical coordinates of the CG nodes (GLL support points of the cells)."""
+    """Physical coordinates of the CG nodes (GLL support points of the cells, mapped)."""
     b1 = Basis1D(m.k)
     g = m.cg_node_coords()
     cell = np.minimum(g // m.k, np.asarray(m.n) - 1)
-    loc = g - m.k * cell
-    xi = b1.nodes[loc]
-    return m.lo + m.h * (cell + 0.5 * (xi + 1.0))
+    return m.points_each(cell, b1.nodes[g - m.k * cell])
 
 
-def rhs(m: Mesh, method: int, penalty_factor: float = PENALTY_FACTOR):
+def rhs(m: Mesh, method: int, penalty_factor: float = PENALTY_FACTOR, sol: Solution = GAUSSIANS):
     """Right-hand side of the linear system (CG: constrained rows hold g_D)."""
     n = m.cg_n_dofs() if method == CG else m.dg_n_dofs()
     b = np.zeros(n)
-    _cell_load(m, method, b)
-    _face_terms(m, method, b, penalty_factor)
+    _cell_load(m, method, b, sol)
+    _face_terms(m, method, b, penalty_factor, sol)
     if method == CG:
         mask = m.cg_dirichlet_mask()
-        g = np.where(mask, exact_u(m.phys(node_coords(m))), 0.0)
-        free_op = Mesh(m.n, m.k, lo=m.lo, hi=m.hi, eps=m.eps, bc=(NEUMANN,) * 6)
+        g = np.where(mask, sol.u(node_coords(m)), 0.0)
+        free_op = Mesh(m.n, m.k, lo=m.lo, hi=m.hi, eps=m.eps, bc=(NEUMANN,) * 6, geometry=m.geometry,
+                       mapping_degree=m.mapping_degree, kappa_amp=m.kappa_amp)
         b -= cg_apply(free_op, g)
         b[mask] = g[mask]
     return b
 
 
-def l2_error_abs(m: Mesh, method: int, uh):
+def l2_error_abs(m: Mesh, method: int, uh, sol: Solution = GAUSSIANS):
     """||u_h - u||_{L2(Omega)} with (k+2)^3 Gauss points."""
     b1 = Basis1D(m.k, m.k + 2)
     pts, w = tensor_points(b1.qp), tensor_weights(b1.qw)
@@ -137,7 +169,7 @@ def l2_error_abs(m: Mesh, method: int, uh):
     cells = np.arange(m.n_cells)
     cc = m.cell_coords(cells)
     detJ = np.linalg.det(m.jacobian(cc, pts))
-    xq = m.phys(m.xhat(cc, pts))
+    xq = m.points(cc, pts)
     dm = m.cg_dofmap(cells) if method == CG else m.dg_dofmap(cells)
-    err = uh[dm] @ val.T - exact_u(xq)
+    err = uh[dm] @ val.T - sol.u(xq)
     return float(np.sqrt(np.sum(err ** 2 * detJ * w[None, :])))

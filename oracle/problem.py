@@ -3,8 +3,9 @@
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 u = prod_d sin(pi t_d), t = (x - lo)/(hi - lo) (BASELINE.json configs[1..4]:
-"manufactured u = sin(pi x) sin(pi y) sin(pi z)" on the unit cube), kappa = 1,
-f = -Laplace u = pi^2 sum_d (hi_d-lo_d)^-2 u  (= 3 pi^2 u on [0,1]^3), eq:poisson.
+"manufactured u = sin(pi x) sin(pi y) sin(pi z)" on the unit cube),
+f = -div(kappa grad u) = kappa pi^2 sum_d (hi_d-lo_d)^-2 u - grad kappa . grad u
+(= 3 pi^2 u on [0,1]^3 with kappa = 1), eq:poisson; kappa of mesh.kappa (N3).
 Load vector (v_h, f) of eq:poisson_fem / eq:poisson_dgsip with (k+1)^3 Gauss
 points in physical coordinates; CG Dirichlet rows set to 0 (g_D = 0); SIPG has
 no boundary term for g_D = 0.
@@ -23,8 +24,21 @@ def exact_u(mesh: Mesh, x):
     return np.prod(np.sin(np.pi * t), axis=-1)
 
 
+def grad_u(mesh: Mesh, x):
+    t = (x - mesh.lo) / (mesh.hi - mesh.lo)
+    sn, cs = np.sin(np.pi * t), np.cos(np.pi * t)
+    g = np.empty(x.shape)
+    for d in range(3):
+        o = [e for e in range(3) if e != d]
+        g[..., d] = np.pi / (mesh.hi[d] - mesh.lo[d]) * cs[..., d] * sn[..., o[0]] * sn[..., o[1]]
+    return g
+
+
 def exact_f(mesh: Mesh, x):
-    return np.pi ** 2 * np.sum((mesh.hi - mesh.lo) ** -2.0) * exact_u(mesh, x)
+    f = mesh.kappa(x) * np.pi ** 2 * np.sum((mesh.hi - mesh.lo) ** -2.0) * exact_u(mesh, x)
+    if mesh.kappa_amp != 0.0:
+        f -= np.sum(mesh.grad_kappa(x) * grad_u(mesh, x), axis=-1)
+    return f
 
 
 def rhs(mesh: Mesh, method: int, chunk: int = 4096):
@@ -34,7 +48,7 @@ def rhs(mesh: Mesh, method: int, chunk: int = 4096):
     for c0 in range(0, mesh.n_cells, chunk):
         cells = np.arange(c0, min(c0 + chunk, mesh.n_cells))
         _, detJ = cell_geometry(mesh, cells, quad)
-        xq = mesh.phys(mesh.xhat(mesh.cell_coords(cells), quad.pts))
+        xq = mesh.points(mesh.cell_coords(cells), quad.pts)
         fq = exact_f(mesh, xq) * detJ * quad.w[None, :]       # [C, q]
         be = fq @ quad.val                                    # [C, n^3]
         if method == CG:
@@ -57,7 +71,7 @@ def l2_error(mesh: Mesh, method: int, uh, chunk: int = 4096):
         cells = np.arange(c0, min(c0 + chunk, mesh.n_cells))
         cc = mesh.cell_coords(cells)
         detJ = np.linalg.det(mesh.jacobian(cc, pts))
-        xq = mesh.phys(mesh.xhat(cc, pts))
+        xq = mesh.points(cc, pts)
         dm = mesh.cg_dofmap(cells) if method == CG else mesh.dg_dofmap(cells)
         uq = uh[dm] @ val.T
         ue = exact_u(mesh, xq)

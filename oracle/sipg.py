@@ -2,8 +2,10 @@
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
-Definition followed (kappa = 1), eq:poisson_dgsip:
-  (grad v, grad u)_T - <v n, {grad u}> - <grad v / 2, n [u]> + <v, sigma [u]>,
+Definition followed, eq:poisson_dgsip:
+  (grad v, kappa grad u)_T - <v n, kappa {grad u}> - <grad v / 2, kappa n [u]> + <v, kappa sigma [u]>,
+  kappa continuous, so every face term carries kappa(x_q) at the face point (folded into
+  JxW below after sigma has been computed from the geometric |F| and |K|),
   both face terms visiting every interior face twice.  Summing the two visits of
   an interior face F (minus side K- = lower cell index, n = n-) gives
       a_F(u, v) = int_F ( -[v]{d_n u} - {d_n v}[u] + sigma [u][v] ),
@@ -62,7 +64,7 @@ def face_geometry(mesh: Mesh, cells, ref: FaceRef):
     nhat[ref.d] = ref.sign
     m = np.einsum('fqed,e->fqd', Jinv, nhat)        # J^-T nhat
     norm = np.linalg.norm(m, axis=-1)
-    return Jinv, m / norm[..., None], ref.w * detJ * norm, mesh.phys(mesh.xhat(cc, ref.pts))
+    return Jinv, m / norm[..., None], ref.w * detJ * norm, mesh.points(cc, ref.pts)
 
 
 def interior_faces(mesh: Mesh, d: int):
@@ -91,12 +93,12 @@ class InteriorFaces:
         assert np.allclose(xm, xp, rtol=0, atol=1e-13 * scale), "face points differ"
         assert np.allclose(nm, -np_, rtol=0, atol=1e-12), "normals not opposite"
         assert np.allclose(Wm, Wp, rtol=1e-12, atol=0), "face JxW differs"
-        self.JxW = Wm
         self.Jn_m = np.einsum('fqed,fqd->fqe', Jm, nm)
         self.Jn_p = np.einsum('fqed,fqd->fqe', Jp, nm)
         area = Wm.sum(axis=1)
         inv_h = 0.5 * (area / cell_volume(mesh, cm, quad) + area / cell_volume(mesh, cp, quad))
         self.sigma = penalty_factor * (mesh.k + 1) ** 2 * inv_h
+        self.JxW = Wm * mesh.kappa(xm)
 
 
 class BoundaryFaces:
@@ -104,11 +106,11 @@ class BoundaryFaces:
         d, sign = side // 2, (1.0 if side % 2 else -1.0)
         self.cells = cells
         self.r = FaceRef(mesh.k, d, sign)
-        Jb, nb, Wb, _ = face_geometry(mesh, cells, self.r)
-        self.JxW = Wb
+        Jb, nb, Wb, xb = face_geometry(mesh, cells, self.r)
         self.Jn = np.einsum('fqed,fqd->fqe', Jb, nb)
         area = Wb.sum(axis=1)
         self.sigma = penalty_factor * (mesh.k + 1) ** 2 * area / cell_volume(mesh, cells, quad)
+        self.JxW = Wb * mesh.kappa(xb)
 
 
 def _dn(Jn, ref, xs):
@@ -147,7 +149,7 @@ class Operator:
         self.mesh, self.pf, self.chunk = mesh, penalty_factor, chunk
         self.quad = CellQuadrature(mesh.k)
         self.m = (mesh.k + 1) ** 3
-        self.uniform = mesh.eps == 0.0
+        self.uniform = mesh.uniform
         if self.uniform:
             self.G0 = metric(mesh, np.array([0]), self.quad)
         else:

@@ -6,7 +6,10 @@ P:L1181-1182: "The level transfer is based on the usual geometric embedding
 operations and also implemented by tensorial techniques."  Reading R12: the
 level spaces are {vhat o Phi^-1 : vhat piecewise Q_k on the Cartesian level
 grid}, nested, so P_ij = phi_j^coarse(xhat_i^fine) evaluated in undeformed
-coordinates and P does not depend on the deformation.
+coordinates and P does not depend on the deformation.  With a per-level polynomial
+mapping or the shell patch (N3) the level spaces are no longer exactly nested; the
+same reference-coordinate P is used (reading N3-d: it is the preconditioner's
+transfer, the paper's geometric multigrid on curved meshes does the same).
 
 Two forms, pinned against each other in tests:
   prolongation_matrix()  explicit sparse P by POINTWISE 3-D evaluation of the
@@ -27,7 +30,7 @@ from .mesh import Mesh, CG, eval_basis_3d
 
 
 def coarsen(mesh: Mesh) -> Mesh:
-    return Mesh(tuple(m // 2 for m in mesh.n), mesh.k, mesh.lo, mesh.hi, mesh.eps, mesh.bc)
+    return mesh.like(tuple(m // 2 for m in mesh.n))
 
 
 def hierarchy(mesh: Mesh, coarse_cells: int = 1):

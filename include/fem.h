@@ -67,10 +67,26 @@ typedef struct fem_ctx* fem_handle;     /* opaque; created by fem_setup, owned b
 
 typedef enum { FEM_CG = 0, FEM_SIPG = 1 } fem_method;
 typedef enum { FEM_BC_DIRICHLET = 0, FEM_BC_NEUMANN = 1 } fem_bc;
+typedef enum { FEM_GEOM_BOX = 0, FEM_GEOM_SHELL = 1 } fem_geometry;
 
 /* Structured hexahedral mesh of the box [lo, hi] (cells are images of
  * [-1,1]^3).  Optional smooth deformation x_d += eps * prod_e sin(pi t_e),
- * t = (xhat - lo)/(hi - lo) (BASELINE.json configs[1], [4]); eps = 0 => Cartesian. */
+ * t = (xhat - lo)/(hi - lo) (BASELINE.json configs[1], [4]); eps = 0 => Cartesian.
+ *
+ * SURVEY §8f N3 (zero-initialised fields keep the box / exact map / kappa = 1):
+ * geometry FEM_GEOM_SHELL: the n[0] x n[1] x n[2] cells tile one of the six
+ *   cube-sphere patches of the paper's spherical shell 0.5 < r < 1:
+ *   t = (c + (xi+1)/2)/n, a = tan(pi/2 (t0 - 1/2)), b = tan(pi/2 (t1 - 1/2)),
+ *   r = 0.5 + 0.5 t2, x = r (1, a, b)/|(1, a, b)|  (lo, hi and deform_eps unused);
+ * mapping_degree l in [1, 8]: every cell is mapped by the degree-l polynomial through
+ *   the exact map at its tensor GLL(l) support points (the paper's shell
+ *   uses l = 5); 0 = the exact map's analytic Jacobian;
+ * kappa_amplitude A != 0: diffusivity kappa(x) = 1 + A prod_{e=1}^{3} cos(2 pi x_e + 0.1 e)
+ *   (eq:diffusivity_shell; the paper's A = 1e6 makes kappa negative on
+ *   parts of the domain -- DESIGN.md reading N3-c -- which the apply accepts and the
+ *   PCG solver does not, it needs kappa > 0).  kappa is folded into the geometry
+ *   tables (G_q = kappa w det J J^-1 J^-T, face JxW), so it costs no apply bandwidth.
+ * Any of the three selects the general (table-driven) operator path on every level. */
 typedef struct {
   int32_t n[3];          /* cells per direction on the finest level (>= 1)            */
   double lo[3], hi[3];   /* box corners                                               */
@@ -82,6 +98,9 @@ typedef struct {
   void* local_group;     /* fem_local_group_create() handle: the nranks ranks are threads of
                             ONE process sharing one device (test transport), or NULL.
                             nranks > 1 needs exactly one of nccl_id / local_group.        */
+  int32_t geometry;      /* fem_geometry (FEM_GEOM_BOX)                                   */
+  int32_t mapping_degree;/* 0 = exact map; l in [1, 8] = degree-l polynomial mapping        */
+  double kappa_amplitude;/* A of eq:diffusivity_shell; 0 => kappa = 1                      */
 } fem_mesh;
 
 /* Solver knobs; pass NULL to fem_setup for the defaults in brackets. */

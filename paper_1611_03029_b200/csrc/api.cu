@@ -708,7 +708,7 @@ void fill_level(fem_ctx* h, Level& L, const fem_level_part& q, int idx) {
   L.own_off = (!is_cg(h) && L.dist) ? (int64_t)q.cells[0] * q.cells[1] * (h->k + 1) * (h->k + 1) * (h->k + 1) : 0;
   L.first_global = q.first_global;
   L.n_global = q.n_global;
-  L.cartesian = (h->mesh.deform_eps == 0.0);
+  L.cartesian = (h->mesh.deform_eps == 0.0) && !mesh_general(h->mesh);
 }
 
 void build_levels(fem_ctx* h) {
@@ -942,6 +942,11 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
       throw Error{FEM_E_ARG, "rank must be in [0, nranks)"};
     if (mesh->nranks > 1 && ((mesh->nccl_id != nullptr) == (mesh->local_group != nullptr)))
       throw Error{FEM_E_ARG, "nranks > 1 needs exactly one of nccl_id / local_group"};
+    if (mesh->geometry != FEM_GEOM_BOX && mesh->geometry != FEM_GEOM_SHELL)
+      throw Error{FEM_E_ARG, "geometry must be FEM_GEOM_BOX or FEM_GEOM_SHELL"};
+    if (mesh->mapping_degree < 0 || mesh->mapping_degree > 8)
+      throw Error{FEM_E_ARG, "mapping_degree must be in [0, 8]"};
+    if (!std::isfinite(mesh->kappa_amplitude)) throw Error{FEM_E_ARG, "kappa_amplitude must be finite"};
     h = new fem_ctx();
     h->k = degree;
     h->method = method;

@@ -91,6 +91,13 @@ struct MapArgs {
   double lo[3], L[3], h[3];
   double eps;
   int cz0;  // global z offset of the rank's slab (cells)
+  // SURVEY §8f N3 (fem_mesh.geometry / mapping_degree / kappa_amplitude)
+  int general;      // 1: any of the three below is set -> geo_point() path
+  int geom;         // FEM_GEOM_BOX / FEM_GEOM_SHELL
+  int mdeg;         // 0: exact map; l: degree-l polynomial through GLL(l) support points
+  int ng[3];        // global cells per direction of the level (shell patch coordinates)
+  double kamp;      // kappa = 1 + kamp prod_e cos(2 pi x_e + 0.1 e)
+  double gll[9];    // GLL(l) nodes
 };
 
 struct PointGeo {
@@ -122,6 +129,164 @@ __device__ __forceinline__ PointGeo map_point(const MapArgs& m, int cx, int cy, 
   p.det = p.fac * (0.5 * m.h[0]) * (0.5 * m.h[1]) * (0.5 * m.h[2]);
   p.beta = m.eps / p.fac;
   return p;
+}
+
+// ---- general geometry (N3): point and Jacobian dx/dxi of the level's cell map
+struct GeoPt {
+  double x[3];
+  double J[3][3];   // J[d][e] = d x_d / d xi_e
+};
+
+// exact map ("manifold") at reference point xi of global cell c; J only if want_j
+__device__ __forceinline__ void manifold_point(const MapArgs& m, const int c[3], const double xi[3], double x[3],
+                                               double (*J)[3]) {
+  if (m.geom == 1) {   // cube-sphere patch of the shell 0.5 < r < 1
+    double t[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) t[d] = (c[d] + 0.5 * (xi[d] + 1.0)) / m.ng[d];
+    const double a = tan(0.5 * M_PI * (t[0] - 0.5)), b = tan(0.5 * M_PI * (t[1] - 0.5));
+    const double r = 0.5 + 0.5 * t[2];
+    const double is = rsqrt(1.0 + a * a + b * b);
+    const double u[3] = {is, a * is, b * is};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) x[d] = r * u[d];
+    if (J) {
+      // du/da = (e1 - u u1)/s, da/dt0 = (pi/2)(1 + a^2); likewise b; dx/dt2 = 0.5 u
+      const double fa = r * 0.5 * M_PI * (1.0 + a * a) * is, fb = r * 0.5 * M_PI * (1.0 + b * b) * is;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        J[d][0] = fa * ((d == 1 ? 1.0 : 0.0) - u[d] * u[1]) * (0.5 / m.ng[0]);
+        J[d][1] = fb * ((d == 2 ? 1.0 : 0.0) - u[d] * u[2]) * (0.5 / m.ng[1]);
+        J[d][2] = 0.5 * u[d] * (0.5 / m.ng[2]);
+      }
+    }
+    return;
+  }
+  // box with the sine deformation (reading R2): x = xhat + eps s(xhat) (1,1,1)
+  double xh[3], sn[3], cs[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    xh[d] = m.lo[d] + m.h[d] * (c[d] + 0.5 * (xi[d] + 1.0));
+    sincospi((xh[d] - m.lo[d]) / m.L[d], &sn[d], &cs[d]);
+  }
+  const double s = sn[0] * sn[1] * sn[2];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) x[d] = xh[d] + m.eps * s;
+  if (J) {
+    const double g[3] = {M_PI / m.L[0] * cs[0] * sn[1] * sn[2], M_PI / m.L[1] * sn[0] * cs[1] * sn[2],
+                         M_PI / m.L[2] * sn[0] * sn[1] * cs[2]};
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int e = 0; e < 3; ++e) J[d][e] = ((d == e ? 1.0 : 0.0) + m.eps * g[e]) * 0.5 * m.h[e];
+  }
+}
+
+// fills the N3 fields of m for level L (global cells per direction: slabs split z)
+inline void set_general_map(const fem_ctx* h, const Level& L, MapArgs& m) {
+  m.general = mesh_general(h->mesh) ? 1 : 0;
+  m.geom = h->mesh.geometry;
+  m.mdeg = h->mesh.mapping_degree;
+  m.kamp = h->mesh.kappa_amplitude;
+  m.ng[0] = L.n[0];
+  m.ng[1] = L.n[1];
+  m.ng[2] = L.nzg;
+  for (int i = 0; i < 9; ++i) m.gll[i] = 0.0;
+  if (m.mdeg > 0) gll_points(m.mdeg, m.gll);
+}
+
+// Lagrange basis of the GLL(l) nodes and its derivative at t
+__device__ __forceinline__ void gll_lagrange(const MapArgs& m, double t, double* v, double* dv) {
+  const int n = m.mdeg + 1;
+  for (int i = 0; i < n; ++i) {
+    double p = 1.0, dp = 0.0;
+    for (int j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const double den = 1.0 / (m.gll[i] - m.gll[j]);
+      dp = dp * (t - m.gll[j]) * den + p * den;
+      p *= (t - m.gll[j]) * den;
+    }
+    v[i] = p;
+    dv[i] = dp;
+  }
+}
+
+// point and Jacobian of local cell (cx, cy, cz) at xi: exact map, or the degree-l
+// polynomial through the exact map at the GLL(l) support points
+static __device__ __noinline__ GeoPt geo_point(const MapArgs& m, int cx, int cy, int cz, double xi0, double xi1,
+                                        double xi2) {
+  GeoPt p;
+  const int c[3] = {cx, cy, cz + m.cz0};
+  if (m.mdeg == 0) {
+    const double xi[3] = {xi0, xi1, xi2};
+    manifold_point(m, c, xi, p.x, p.J);
+    return p;
+  }
+  double v0[9], d0[9], v1[9], d1[9], v2[9], d2[9];
+  gll_lagrange(m, xi0, v0, d0);
+  gll_lagrange(m, xi1, v1, d1);
+  gll_lagrange(m, xi2, v2, d2);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    p.x[d] = 0.0;
+    p.J[d][0] = p.J[d][1] = p.J[d][2] = 0.0;
+  }
+  const int n = m.mdeg + 1;
+  for (int k = 0; k < n; ++k)
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        const double s[3] = {m.gll[i], m.gll[j], m.gll[k]};
+        double X[3];
+        manifold_point(m, c, s, X, nullptr);
+        const double w = v0[i] * v1[j] * v2[k];
+        const double w0 = d0[i] * v1[j] * v2[k], w1 = v0[i] * d1[j] * v2[k], w2 = v0[i] * v1[j] * d2[k];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          p.x[d] = fma(w, X[d], p.x[d]);
+          p.J[d][0] = fma(w0, X[d], p.J[d][0]);
+          p.J[d][1] = fma(w1, X[d], p.J[d][1]);
+          p.J[d][2] = fma(w2, X[d], p.J[d][2]);
+        }
+      }
+  return p;
+}
+
+// det J and J^-1 by cofactors
+__device__ __forceinline__ double geo_inverse(const GeoPt& p, double Ji[3][3]) {
+  const double (*J)[3] = p.J;
+  Ji[0][0] = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+  Ji[0][1] = J[0][2] * J[2][1] - J[0][1] * J[2][2];
+  Ji[0][2] = J[0][1] * J[1][2] - J[0][2] * J[1][1];
+  Ji[1][0] = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+  Ji[1][1] = J[0][0] * J[2][2] - J[0][2] * J[2][0];
+  Ji[1][2] = J[0][2] * J[1][0] - J[0][0] * J[1][2];
+  Ji[2][0] = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+  Ji[2][1] = J[0][1] * J[2][0] - J[0][0] * J[2][1];
+  Ji[2][2] = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+  const double det = J[0][0] * Ji[0][0] + J[0][1] * Ji[1][0] + J[0][2] * Ji[2][0];
+  const double id = 1.0 / det;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) Ji[a][b] *= id;
+  return det;
+}
+
+// eq:diffusivity_shell and its gradient
+__device__ __forceinline__ double kappa_at(const MapArgs& m, const double x[3], double* grad = nullptr) {
+  if (m.kamp == 0.0) {
+    if (grad) grad[0] = grad[1] = grad[2] = 0.0;
+    return 1.0;
+  }
+  double sn[3], cs[3];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) sincos(2.0 * M_PI * x[e] + 0.1 * (e + 1), &sn[e], &cs[e]);
+  if (grad) {
+    grad[0] = -2.0 * M_PI * m.kamp * sn[0] * cs[1] * cs[2];
+    grad[1] = -2.0 * M_PI * m.kamp * cs[0] * sn[1] * cs[2];
+    grad[2] = -2.0 * M_PI * m.kamp * cs[0] * cs[1] * sn[2];
+  }
+  return 1.0 + m.kamp * cs[0] * cs[1] * cs[2];
 }
 
 // J^-1 = H^-1 (I - beta 1 g^T)  (Sherman-Morrison):  Jinv[d][e] = (2/h_d)(delta_de - beta g_e)

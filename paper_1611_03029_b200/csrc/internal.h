@@ -48,6 +48,11 @@ struct Tables1D {
   double dg_embed[2][kMaxN][kMaxN];         // [child][fine i][coarse j]
 };
 void build_tables(int k, Tables1D& t);
+void gll_points(int l, double* x);   // GLL(l) nodes (mapping support points)
+// the level's cell map uses the general (table-driven) path: shell, polynomial mapping or kappa (N3)
+inline bool mesh_general(const fem_mesh& m) {
+  return m.geometry != FEM_GEOM_BOX || m.mapping_degree != 0 || m.kappa_amplitude != 0.0;
+}
 
 // ---------------------------------------------------------------- communication
 // Transport of the z-slab exchanges: NCCL between processes, or an

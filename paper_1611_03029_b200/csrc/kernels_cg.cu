@@ -977,6 +977,21 @@ __global__ void geometry_kernel(MapArgs m, int n0, int n1, int64_t n_cells, Tab<
   const int cx = (int)(cell % n0);
   const int64_t r = cell / n0;
   const int cy = (int)(r % n1), cz = (int)(r / n1);
+  const int comp[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+  if (m.general) {
+    // G = J^-1 (kappa w det J) J^-T from the level's cell map (N3)
+    const GeoPt g = geo_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]);
+    double Ji[3][3];
+    const double det = geo_inverse(g, Ji);
+    if (!(det > 0.0)) atomicMin((unsigned long long*)err, (unsigned long long)cell);
+    const double w = T.w[q0] * T.w[q1] * T.w[q2] * det * kappa_at(m, g.x);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const int d = comp[c][0], f = comp[c][1];
+      G[g_index<N>(glayout, cell, c, q)] = w * (Ji[d][0] * Ji[f][0] + Ji[d][1] * Ji[f][1] + Ji[d][2] * Ji[f][2]);
+    }
+    return;
+  }
   const PointGeo p = map_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]);
   if (!(p.fac > 0.0)) {
     // record the first bad cell (as a double, exact for < 2^53)
@@ -985,7 +1000,6 @@ __global__ void geometry_kernel(MapArgs m, int n0, int n1, int64_t n_cells, Tab<
   const double w = T.w[q0] * T.w[q1] * T.w[q2] * p.det;
   const double g2 = p.g[0] * p.g[0] + p.g[1] * p.g[1] + p.g[2] * p.g[2];
   const double b = p.beta;
-  const int comp[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
     const int d = comp[c][0], f = comp[c][1];
@@ -1008,6 +1022,25 @@ __global__ void rhs_kernel(MapArgs m, OpArgs a, Tab<K + 1> T) {
   const int cy = (int)(r % a.n1), cz = (int)(r / a.n1);
   for (int q = threadIdx.x; q < N3; q += blockDim.x) {
     const int q0 = q % N, q1 = (q / N) % N, q2 = q / (N * N);
+    if (m.general) {
+      // f = -div(kappa grad u) = kappa pi^2 sum_d L_d^-2 u - grad kappa . grad u  (N3)
+      const GeoPt g = geo_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]);
+      double Ji[3][3], gk[3], sn[3], cs[3];
+      const double det = geo_inverse(g, Ji);
+      const double kap = kappa_at(m, g.x, gk);
+      double lap = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        sincospi((g.x[d] - m.lo[d]) / m.L[d], &sn[d], &cs[d]);
+        lap += 1.0 / (m.L[d] * m.L[d]);
+      }
+      const double u = sn[0] * sn[1] * sn[2];
+      const double gu[3] = {M_PI / m.L[0] * cs[0] * sn[1] * sn[2], M_PI / m.L[1] * sn[0] * cs[1] * sn[2],
+                            M_PI / m.L[2] * sn[0] * sn[1] * cs[2]};
+      const double f = kap * M_PI * M_PI * lap * u - (gk[0] * gu[0] + gk[1] * gu[1] + gk[2] * gu[2]);
+      fq[q] = f * T.w[q0] * T.w[q1] * T.w[q2] * det;
+      continue;
+    }
     const PointGeo p = map_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]);
     double u = 1.0, lap = 0.0;
 #pragma unroll
@@ -1106,6 +1139,7 @@ MapArgs map_args(const fem_ctx* h, const Level& L) {
   }
   m.eps = h->mesh.deform_eps;
   m.cz0 = L.cz0;
+  set_general_map(h, L, m);
   return m;
 }
 

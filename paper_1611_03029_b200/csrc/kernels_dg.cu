@@ -588,7 +588,7 @@ __global__ void dg_diag_kernel(DgArgs A, Tab<K + 1> T) {
 // Jm = J_minus^-1 nf, Jp = J_plus^-1 nf (0 for a missing side); both sides agree on
 // the physical point, normal and JxW because the map is continuous (reading R2).
 template <int K>
-__global__ void dg_face_geometry_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double* faceq) {
+__global__ void dg_face_geometry_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double* faceq, double* kap) {
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N;
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -620,6 +620,23 @@ __global__ void dg_face_geometry_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, doubl
     }
     c[D] = cd;
     xi[D] = side == 0 ? 1.0 : -1.0;
+    if (m.general) {
+      // N3: the level's cell map; both sides agree on the point (continuous map)
+      const GeoPt g = geo_point(m, c[0], c[1], c[2], xi[0], xi[1], xi[2]);
+      double Ji[3][3];
+      const double det = geo_inverse(g, Ji);
+      if (!have_n) {
+        double nrm = 0.0;
+        for (int e = 0; e < 3; ++e) nrm += Ji[D][e] * Ji[D][e];
+        nrm = sqrt(nrm);
+        for (int e = 0; e < 3; ++e) nf[e] = Ji[D][e] / nrm;
+        rec[q] = T.w[qa] * T.w[qb] * det * nrm;
+        if (kap) kap[fr * N2 + q] = kappa_at(m, g.x);
+        have_n = true;
+      }
+      for (int a = 0; a < 3; ++a) Jn[a * N2] = Ji[a][0] * nf[0] + Ji[a][1] * nf[1] + Ji[a][2] * nf[2];
+      continue;
+    }
     const PointGeo g = map_point(m, c[0], c[1], c[2], xi[0], xi[1], xi[2]);
     if (!have_n) {
       double v[3], nrm = 0.0;
@@ -655,7 +672,12 @@ __global__ void dg_cell_volume_kernel(MapArgs m, DgArgs A, Tab<K + 1> T, double*
   for (int q2 = 0; q2 < N; ++q2)
     for (int q1 = 0; q1 < N; ++q1)
       for (int q0 = 0; q0 < N; ++q0)
-        v += T.w[q0] * T.w[q1] * T.w[q2] * map_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]).det;
+        if (m.general) {
+          double Ji[3][3];
+          v += T.w[q0] * T.w[q1] * T.w[q2] * geo_inverse(geo_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]), Ji);
+        } else {
+          v += T.w[q0] * T.w[q1] * T.w[q2] * map_point(m, cx, cy, cz, T.qp[q0], T.qp[q1], T.qp[q2]).det;
+        }
   vol[id] = v;
 }
 
@@ -688,6 +710,15 @@ __global__ void dg_face_sigma_kernel(DgArgs A, double pen, const double* faceq, 
     ++cnt;
   }
   fsigma[fr] = pen * (K + 1) * (K + 1) * inv_h / cnt;
+}
+
+// kappa folded into the face JxW after sigma was computed from the geometric |F|, |K|:
+// every SIPG face term carries kappa (eq:poisson_dgsip)
+__global__ void dg_face_kappa_kernel(double* faceq, const double* kap, int64_t nf, int N2) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nf * N2) return;
+  const int64_t fr = id / N2;
+  faceq[fr * 7 * N2 + id % N2] *= kap[id];
 }
 
 // ---------------------------------------------------------------- launchers
@@ -744,6 +775,7 @@ MapArgs dg_map_args(const fem_ctx* h, const Level& L) {
   }
   m.eps = h->mesh.deform_eps;
   m.cz0 = L.cz0;
+  set_general_map(h, L, m);
   return m;
 }
 
@@ -833,14 +865,21 @@ void dg_face_geometry_k(fem_ctx* h, Level& L) {
   const DgArgs A = dg_args(h, L, nullptr, nullptr);
   const MapArgs m = dg_map_args(h, L);
   const Tab<N> T = make_tab<N>(h->tab);
-  dg_face_geometry_kernel<K><<<(unsigned)((nf * N2 + 255) / 256), 256, 0, h->stream>>>(m, A, T, L.face);
+  double* kap = nullptr;
+  if (m.kamp != 0.0) FEM_CUDA_TRY(cudaMalloc(&kap, sizeof(double) * nf * N2));
+  dg_face_geometry_kernel<K><<<(unsigned)((nf * N2 + 255) / 256), 256, 0, h->stream>>>(m, A, T, L.face, kap);
   dg_cell_volume_kernel<K><<<(unsigned)((nvol + 255) / 256), 256, 0, h->stream>>>(m, A, T, vol);
   dg_face_sigma_kernel<K><<<(unsigned)((nf + 255) / 256), 256, 0, h->stream>>>(
       A, h->opt.penalty_factor, L.face, vol, L.face + nf * 7 * N2);
   count_launch(3);
+  if (kap) {
+    dg_face_kappa_kernel<<<(unsigned)((nf * N2 + 255) / 256), 256, 0, h->stream>>>(L.face, kap, nf, N2);
+    count_launch();
+  }
   check_launch("dg_face_geometry");
   FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
   cudaFree(vol);
+  if (kap) cudaFree(kap);
 }
 
 #define FEM_DISPATCH_K(k, fn, ...)                           \

@@ -99,6 +99,8 @@ double lagr_d(const double* nodes, int n, int i, double z) {
 
 }  // namespace
 
+void gll_points(int l, double* x) { gll_nodes(l, x); }
+
 void build_tables(int k, Tables1D& t) {
   t = Tables1D{};
   t.k = k;

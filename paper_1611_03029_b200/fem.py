@@ -24,6 +24,7 @@ ERRORS = {-1: "FEM_E_ARG", -2: "FEM_E_SIZE", -3: "FEM_E_GEOMETRY", -4: "FEM_E_BR
           -5: "FEM_E_CUDA", -6: "FEM_E_NCCL", -7: "FEM_E_OOM"}
 FEM_CG, FEM_SIPG = 0, 1
 FEM_BC_DIRICHLET, FEM_BC_NEUMANN = 0, 1
+FEM_GEOM_BOX, FEM_GEOM_SHELL = 0, 1
 
 
 class FemError(RuntimeError):
@@ -35,7 +36,8 @@ class FemError(RuntimeError):
 class fem_mesh(C.Structure):
     _fields_ = [("n", C.c_int32 * 3), ("lo", C.c_double * 3), ("hi", C.c_double * 3),
                 ("deform_eps", C.c_double), ("bc", C.c_int32 * 6), ("rank", C.c_int32),
-                ("nranks", C.c_int32), ("nccl_id", C.c_void_p), ("local_group", C.c_void_p)]
+                ("nranks", C.c_int32), ("nccl_id", C.c_void_p), ("local_group", C.c_void_p),
+                ("geometry", C.c_int32), ("mapping_degree", C.c_int32), ("kappa_amplitude", C.c_double)]
 
 
 class fem_options(C.Structure):
@@ -161,8 +163,10 @@ class LocalGroup:
             pass
 
 
-def _mesh(cells, lo, hi, deform_eps, bc, rank, nranks, nccl_id, local_group):
+def _mesh(cells, lo, hi, deform_eps, bc, rank, nranks, nccl_id, local_group, geometry=FEM_GEOM_BOX,
+          mapping_degree=0, kappa_amplitude=0.0):
     m = fem_mesh()
+    m.geometry, m.mapping_degree, m.kappa_amplitude = geometry, mapping_degree, kappa_amplitude
     m.n[:] = list(cells)
     m.lo[:] = list(lo)
     m.hi[:] = list(hi)
@@ -211,8 +215,10 @@ class Fem:
                  deform_eps=0.0, bc=(FEM_BC_DIRICHLET,) * 6, penalty_factor=None, cheb_degree=None,
                  cheb_lo=None, cheb_hi=None, eig_iters=None, coarse_cells=None, eig_seed=None,
                  lambda_override=None, stream=None, device=None, profile=False, rank=0, nranks=1,
-                 nccl_id=None, local_group=None, slab_min_layers=None, slab_min_dofs=None):
-        m = _mesh(cells, lo, hi, deform_eps, bc, rank, nranks, None, local_group)
+                 nccl_id=None, local_group=None, slab_min_layers=None, slab_min_dofs=None,
+                 geometry=FEM_GEOM_BOX, mapping_degree=0, kappa_amplitude=0.0):
+        m = _mesh(cells, lo, hi, deform_eps, bc, rank, nranks, None, local_group, geometry, mapping_degree,
+                  kappa_amplitude)
         self._nccl_id = None
         if nccl_id is not None:
             self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)

@@ -243,3 +243,40 @@ def test_vcycle_and_pcg_match_single_rank(method, k, cells, eps, bc, P, mnl):
     ax = ocg.apply(m_, x) if method == "cg" else osipg.apply(m_, x)
     bb = b
     assert np.linalg.norm(bb - ax) / np.linalg.norm(bb) <= 1e-9
+
+
+@pytest.mark.parametrize("method,k,cells,P", [("cg", 3, (2, 4, 6), 2), ("sipg", 2, (4, 2, 4), 2)])
+def test_shell_variable_kappa_slabs_match_single_rank_and_oracle(method, k, cells, P):
+    """N3 on z-slabs: the shell patch coordinates use the GLOBAL z cell index and count."""
+    fem = fem_mod()
+    kw = kw_of(method, k, cells, 0.0, (DIRICHLET,) * 6, 1)
+    kw.update(geometry=fem.FEM_GEOM_SHELL, mapping_degree=5, kappa_amplitude=0.5)
+    F1 = fem.Fem(**kw)
+    n = F1.n_global
+    x = fem_inputs.uniform_pm1(13, n)
+    y1, d1, b1 = np.zeros(n), np.zeros(n), np.zeros(n)
+    F1.fem_apply(x, y1)
+    F1.fem_diagonal(d1)
+    F1.fem_rhs(b1)
+    its1, _, ok1 = F1.cg_solve(b1, np.zeros(n))
+    F1.close()
+    sl = own_slices(F1, P, kw)
+
+    def body(F, r):
+        f, m = sl[r]
+        xr = torch.from_numpy(x[f:f + m]).cuda()
+        yr, dr, br = torch.zeros_like(xr), torch.zeros_like(xr), torch.zeros_like(xr)
+        F.fem_apply(xr, yr)
+        F.fem_diagonal(dr)
+        F.fem_rhs(br)
+        its, _, ok = F.cg_solve(br, torch.zeros_like(xr))
+        F.fem_sync()
+        return yr.cpu().numpy(), dr.cpu().numpy(), br.cpu().numpy(), its, ok
+
+    res = run_ranks(P, kw, body)
+    y, d, b = (np.concatenate([res[r][i] for r in range(P)]) for i in range(3))
+    assert relmax(y, y1) <= 1e-12 and relmax(d, d1) <= 1e-12 and relmax(b, b1) <= 1e-12
+    m = Mesh(cells, k, geometry=1, mapping_degree=5, kappa_amp=0.5)
+    assert relmax(y, ocg.apply(m, x) if method == "cg" else osipg.apply(m, x)) <= 1e-12
+    assert ok1 and all(res[r][4] for r in range(P))
+    assert all(abs(res[r][3] - its1) <= 1 for r in range(P))

@@ -323,8 +323,91 @@ void prolongate_from(fem_ctx* h, int l, double* xc, double* xf) {
 // x_1 = x_0 + D^-1 (b - A x_0) / theta;  x_{i+1} = x_i + rho_i rho_{i-1} (x_i - x_{i-1})
 //        + (2 rho_i / delta) D^-1 (b - A x_i),  rho_i = 1/(2 sigma - rho_{i-1}), rho_0 = 1/sigma.
 // Work buffers w[0..2] must differ from x_in/x_out/b.
+// CG levels with the fused line kernel (single rank, deformed, default G layout)
+// Only small levels: there a smoothing step is latency-bound and one launch instead of
+// two saves ~2.5 us; on large levels the wider gather (five streams, 79 registers) costs
+// more than the separate elementwise pass (C2 finest: 90 us fused vs 62 + 17 us).
+bool cg_fused_ok(const fem_ctx* h, const Level& L) {
+  return is_cg(h) && h->fuse_cheb && L.tf[0] && !L.dist && !L.cartesian &&
+         (L.glayout == kGLayoutCell || L.glayout == kGLayoutCell8) &&
+         L.n_cells <= h->fuse_max_cells;
+}
+
+// Chebyshev smoothing with every step but (optionally) the last fused into the CG line
+// kernel's gather: kernel j materialises x_j from (x_{j-1}, x_{j-2}, A x_{j-1}) and
+// accumulates A x_j into tf[k], clearing tf[k+1] for kernel j+1 (tf[k-1], which kernel j
+// read, is free again).  want_ax: the last step is fused too and the buffer holding
+// A x_out is returned (the V-cycle's residual); else the last step is the elementwise
+// kernel and nullptr is returned.  Arithmetic identical to the unfused recurrence.
+double* chebyshev_cg_fused(fem_ctx* h, Level& L, const double* b, const double* x_in, double* x_out,
+                           double* w0, double* w1, double* w2, bool want_ax) {
+  const int p = h->opt.cheb_degree;
+  const double a = h->opt.cheb_hi * L.lam, c = h->opt.cheb_lo * L.lam;
+  const double theta = 0.5 * (a + c), delta = 0.5 * (a - c);
+  const double sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  double* bufs[3] = {w0, w1, w2};
+  int nb = 0;
+  auto next = [&](const double* avoid1, const double* avoid2) {
+    for (int i = 0; i < 3; ++i) {
+      double* cand = bufs[(nb + i) % 3];
+      if (cand != avoid1 && cand != avoid2) {
+        nb = (nb + i + 1) % 3;
+        return cand;
+      }
+    }
+    return (double*)nullptr;
+  };
+  int k = 0;
+  launch_zero(h, L.tf[0], L.n_store);
+  // one fused launch: input x (materialised from it when mat), accumulate into tf[k]
+  auto fused = [&](const double* x, const double* xo, double* xnew, double c1, double c2, int mat) {
+    CgFuse f;
+    f.xo = xo;
+    f.b = b;
+    f.dinv = L.dinv;
+    f.t = L.tf[(k + 2) % 3];
+    f.xnew = xnew;
+    f.zbuf = L.tf[(k + 1) % 3];
+    f.c1 = c1;
+    f.c2 = c2;
+    f.materialize = mat;
+    f.on = 1;
+    h->cgf = f;
+    launch_cg_apply(h, L, x, L.tf[k]);
+    h->cgf = CgFuse{};
+    k = (k + 1) % 3;
+  };
+  const double* x = x_in;
+  const double* xo = nullptr;
+  if (x_in) fused(x_in, nullptr, nullptr, 0.0, 0.0, 0);   // A x_in
+  for (int i = 1; i <= p; ++i) {
+    double c1 = 0.0, c2 = 1.0 / theta;
+    if (i > 1) {
+      const double rho_new = 1.0 / (2.0 * sigma - rho);
+      c1 = rho_new * rho;
+      c2 = 2.0 * rho_new / delta;
+      rho = rho_new;
+    }
+    double* xn = (i == p) ? x_out : next(x, xo);
+    if (i < p || want_ax) {
+      fused(x, xo, xn, c1, c2, 1);
+    } else {
+      // last step, elementwise: A x_{p-1} is in tf[k-1]
+      launch_cheb_step(h, L, xn, x, xo, b, x ? L.tf[(k + 2) % 3] : nullptr, c1, c2, xo != nullptr);
+    }
+    xo = x;
+    x = xn;
+  }
+  return want_ax ? L.tf[(k + 2) % 3] : nullptr;
+}
+
 void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double* x_out,
                double* w0, double* w1, double* w2) {
+  if (cg_fused_ok(h, L)) {
+    chebyshev_cg_fused(h, L, b, x_in, x_out, w0, w1, w2, false);
+    return;
+  }
   const int p = h->opt.cheb_degree;
   const double a = h->opt.cheb_hi * L.lam, c = h->opt.cheb_lo * L.lam;
   const double theta = 0.5 * (a + c), delta = 0.5 * (a - c);
@@ -397,10 +480,15 @@ void vcycle(fem_ctx* h, int l, const double* b, double* x_out) {
   // buffers for the smoother: three distinct from b, xs
   // work buffers: x3, b2 and wa (wa may be x_out on coarse levels, which is not live
   // yet; the elementwise Chebyshev update is safe in place)
-  chebyshev(h, L, b, nullptr, xs, L.x3, L.b2, wa);
   // residual, restriction: C.b = P^T (b - A xs)
-  apply_level(h, L, xs, L.t, false);
-  restrict_to(h, l, b, L.t, C.b);
+  if (cg_fused_ok(h, L)) {
+    const double* axs = chebyshev_cg_fused(h, L, b, nullptr, xs, L.x3, L.b2, wa, true);
+    restrict_to(h, l, b, axs, C.b);
+  } else {
+    chebyshev(h, L, b, nullptr, xs, L.x3, L.b2, wa);
+    apply_level(h, L, xs, L.t, false);
+    restrict_to(h, l, b, L.t, C.b);
+  }
   vcycle(h, l - 1, C.b, C.x);
   prolongate_from(h, l, C.x, xs);
   chebyshev(h, L, b, xs, x_out, L.x3, L.b2, wa);
@@ -726,6 +814,8 @@ void build_levels(fem_ctx* h) {
     L.x2 = valloc(L);
     L.x3 = valloc(L);
     L.b2 = valloc(L);
+    if (is_cg(h) && h->fuse_cheb && !L.dist && !L.cartesian && L.n_cells <= h->fuse_max_cells)
+      for (double*& t : L.tf) t = valloc(L);
     if (L.dist && is_cg(h)) L.halo = dalloc((int64_t)L.nn[0] * L.nn[1]);
     if (L.dist && l > 0 && !parts[l - 1].distributed) {
       // last distributed level: whole-level twin for the transfers to the replicated level
@@ -749,11 +839,13 @@ void level_geometry_and_diagonal(fem_ctx* h, Level& L) {
   if (!L.cartesian) {
     L.glayout = !is_cg(h) ? kGLayoutCell
                 : (h->k <= 4 && h->plane_kernel) ? kGLayoutPlane
-                : h->dbasis ? kGLayoutXLine : kGLayoutCell;
-    const bool plane = L.glayout == kGLayoutPlane;
-    const int64_t cells = plane ? (L.n_cells + kGroupCells - 1) / kGroupCells * kGroupCells : L.n_cells;
+                : h->dbasis ? kGLayoutXLine
+                : (h->k == 4 && h->g_direct && h->line_cell_fast) ? kGLayoutCell8 : kGLayoutCell;
+    const bool plane = L.glayout == kGLayoutPlane, c8 = L.glayout == kGLayoutCell8;
+    const int64_t cells = plane ? (L.n_cells + kGroupCells - 1) / kGroupCells * kGroupCells
+                          : c8 ? (L.n_cells + kCell8 - 1) / kCell8 * kCell8 : L.n_cells;
     L.G = dalloc(cells * 6 * N * N * N);
-    if (plane) FEM_CUDA_TRY(cudaMemset(L.G, 0, sizeof(double) * cells * 6 * N * N * N));
+    if (plane || c8) FEM_CUDA_TRY(cudaMemset(L.G, 0, sizeof(double) * cells * 6 * N * N * N));
     const unsigned long long init = std::numeric_limits<unsigned long long>::max();
     FEM_CUDA_TRY(cudaMemcpyAsync(h->geom_err, &init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
     launch_geometry(h, L);
@@ -870,7 +962,7 @@ void destroy(fem_ctx* h) {
   for (auto& L : h->levels) {
     for (double** p : {&L.G, &L.face, &L.halo, &L.gb, &L.gx}) dfree(*p);
     for (double** p : {&L.diag, &L.dinv, &L.b, &L.x, &L.x2, &L.x3, &L.t, &L.b2, &L.pcg_r, &L.pcg_p,
-                       &L.pcg_q, &L.pcg_z})
+                       &L.pcg_q, &L.pcg_z, &L.tf[0], &L.tf[1], &L.tf[2]})
       vfree(L, *p);
   }
   h->comm.reset();
@@ -982,6 +1074,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_PDL")) h->pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_DG_KRON")) h->dg_kron = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_FUSE_CHEB")) h->fuse_cheb = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_FUSE_CELLS")) h->fuse_max_cells = std::atoll(e);
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)
     FEM_CUDA_TRY(cudaMemset(h->red, 0, sizeof(double) * (16 * kRedBlocks + 16)));
@@ -1126,7 +1219,8 @@ int fem_level_geometry(fem_handle h, int32_t level, double* G, int64_t nG) {
     if (!L.cartesian) {
       // internal layout: permute to the documented [cell][6][q] order on the host
       const int64_t cells = L.glayout == kGLayoutPlane ? (L.n_cells + kGroupCells - 1) / kGroupCells * kGroupCells
-                                                       : L.n_cells;
+                            : L.glayout == kGLayoutCell8 ? (L.n_cells + kCell8 - 1) / kCell8 * kCell8
+                                                         : L.n_cells;
       std::vector<double> raw(cells * 6 * nq), out(nG);
       FEM_CUDA_TRY(cudaMemcpyAsync(raw.data(), L.G, sizeof(double) * raw.size(), cudaMemcpyDeviceToHost, h->stream));
       FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -1137,6 +1231,8 @@ int fem_level_geometry(fem_handle h, int32_t level, double* G, int64_t nG) {
             int64_t src;
             if (L.glayout == kGLayoutXLine) {
               src = (c * 6 + comp) * nq + (q % N) * N2 + q / N;
+            } else if (L.glayout == kGLayoutCell8) {
+              src = (((c / kCell8) * 6 + comp) * nq + q) * kCell8 + c % kCell8;
             } else {   // plane
               const int64_t g = c / kGroupCells, ci = c % kGroupCells;
               src = (((g * 6 + comp) * N2 + q % N2) * kGroupCells + ci) * N + q / N2;

@@ -20,6 +20,8 @@ struct CellGeo {
   double c0, c1, c2;
   bool active;
   uint64_t* bar;    // if set: mbarrier of a bulk copy that fills G, waited on before the q-point phase
+  int gq = 1;       // G stride between quadrature points ([cell][comp][q]: 1)
+  int gc = N * N * N;  // G stride between components
 };
 
 template <int N, bool DEFORMED>
@@ -72,13 +74,13 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
     if (DEFORMED) {
       double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
       if (geo.active) {
-        const double* Gc = geo.G + q;
+        const double* Gc = geo.G + q * geo.gq;
         G00 = Gc[0];
-        G01 = Gc[N3];
-        G02 = Gc[2 * N3];
-        G11 = Gc[3 * N3];
-        G12 = Gc[4 * N3];
-        G22 = Gc[5 * N3];
+        G01 = Gc[geo.gc];
+        G02 = Gc[2 * geo.gc];
+        G11 = Gc[3 * geo.gc];
+        G12 = Gc[4 * geo.gc];
+        G22 = Gc[5 * geo.gc];
       }
       fx = G00 * gxq + G01 * gyq + G02 * gzq;
       fy = G01 * gxq + G11 * gyq + G12 * gzq;

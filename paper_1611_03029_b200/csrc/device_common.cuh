@@ -338,13 +338,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 //   kGLayoutPlane groups of kGroupCells cells, [group][comp][e][cell-in-group][q2],
 //                 e = q0 + N q1 (CG plane kernel: lane = q2 + N cell; a row q1 of all
 //                 six components is six contiguous chunks -> TMA bulk copies)
+//   kGLayoutCell8 blocks of kCell8 cells, [block][comp][q][cell-in-block] (CG line kernel
+//                 at Q4 with the cells-fastest thread layout: a warp's 4 points x 8 cells
+//                 of one component are 32 consecutive doubles)
 constexpr int kGroupCells = 12;
-enum { kGLayoutCell = 0, kGLayoutPlane = 1, kGLayoutXLine = 2 };
+constexpr int kCell8 = 8;
+enum { kGLayoutCell = 0, kGLayoutPlane = 1, kGLayoutXLine = 2, kGLayoutCell8 = 3 };
 
 template <int N>
 __host__ __device__ __forceinline__ int64_t g_index(int layout, int64_t cell, int comp, int q) {
   constexpr int N2 = N * N, N3 = N2 * N;
   if (layout == kGLayoutXLine) return (cell * 6 + comp) * N3 + (q % N) * N2 + q / N;
+  if (layout == kGLayoutCell8) return (((cell / kCell8) * 6 + comp) * N3 + q) * kCell8 + cell % kCell8;
   if (layout != kGLayoutPlane) return (cell * 6 + comp) * N3 + q;
   const int64_t g = cell / kGroupCells;
   const int c = (int)(cell % kGroupCells);

@@ -12,6 +12,11 @@
 
 #include "../../include/fem.h"
 
+// Q4 CG line kernel thread layout (kernels_cg.cu): 1 = cells fastest (default)
+#ifndef FEM_LINE_CELL_FAST
+#define FEM_LINE_CELL_FAST 1
+#endif
+
 namespace fem {
 
 constexpr int kMaxDeg = 8;
@@ -107,6 +112,9 @@ struct Level {
   // host-side knowledge that t is all zeros (the Chebyshev step clears the A x it
   // consumes), so that the next CG apply into t needs no memset; reset at graph capture
   mutable bool t_zero = false;
+  // CG single-rank deformed levels: three A x buffers rotated by the fused Chebyshev
+  // sequences (each fused kernel clears the buffer the next one accumulates into)
+  double* tf[3] = {nullptr, nullptr, nullptr};
   // PCG vectors (finest level, allocated on first cg_solve)
   double *pcg_r = nullptr, *pcg_p = nullptr, *pcg_q = nullptr, *pcg_z = nullptr;
   double* halo = nullptr;        // CG dist: receive buffer of one node plane (compress-add)
@@ -122,6 +130,19 @@ struct ChebFuse {
   const double* xo = nullptr;    // x_old (nullptr: first step)
   const double* b = nullptr;
   const double* dinv = nullptr;
+  double c1 = 0.0, c2 = 0.0;
+  int on = 0;
+};
+
+// Chebyshev step fused into the CG line-kernel gather (kernels_cg.cu, FUSED)
+struct CgFuse {
+  const double* xo = nullptr;    // x_old (nullptr: none)
+  const double* b = nullptr;
+  const double* dinv = nullptr;
+  const double* t = nullptr;     // A x of the kernel's input x
+  double* xnew = nullptr;        // the new iterate (written by the owning cells)
+  int materialize = 1;           // 0: apply x itself (only zbuf is cleared)
+  double* zbuf = nullptr;        // cleared by the owning cells (the next target), or nullptr
   double c1 = 0.0, c2 = 0.0;
   int on = 0;
 };
@@ -185,9 +206,12 @@ struct fem_ctx {
   bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)
   bool g_direct = true;                // FEM_G_DIRECT=0: line kernel stages G by TMA into shared memory
   bool y_is_zero = false;
-  fem::ChebFuse fuse;                   // set around a fused Chebyshev apply (SIPG levels)              // set around launch_cg_apply: the output is known to be zero
+  fem::ChebFuse fuse;                   // set around a fused Chebyshev apply (SIPG levels)
+  fem::CgFuse cgf;                      // set around a fused Chebyshev step + apply (CG levels)              // set around launch_cg_apply: the output is known to be zero
   bool pdl = true;                     // FEM_PDL=0: plain launches (no programmatic dependent launch)
-  bool fuse_cheb = true;               // FEM_FUSE_CHEB=0: separate Chebyshev-step kernel on SIPG levels
+  int64_t fuse_max_cells = 512;        // FEM_FUSE_CELLS: CG levels up to this many cells use the fused step
+  bool fuse_cheb = true;
+  bool line_cell_fast = FEM_LINE_CELL_FAST != 0;   // Q4 line kernel: cells-fastest layout, G in kGLayoutCell8               // FEM_FUSE_CHEB=0: separate Chebyshev-step kernel on SIPG levels
   bool dg_kron = true;                 // FEM_DG_KRON=0: quadrature cell+face kernel on Cartesian SIPG levels
   bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels
   bool dbasis = false;                 // FEM_DBASIS=1: derivative-basis line kernel (measured slower, kept for study)
@@ -195,7 +219,7 @@ struct fem_ctx {
 
 namespace fem {
 
-constexpr int kRedBlocks = 296;   // 2 x 148 SMs
+constexpr int kRedBlocks = 1184;  // 8 x 148 SMs (256 threads each: full occupancy for the HBM-bound passes)
 
 // kernels (kernels_*.cu)
 void launch_geometry(fem_ctx* h, Level& L);

@@ -45,15 +45,30 @@ struct OpArgs {
 
 // per-cell stride of the line kernel's three work buffers: +2 doubles at Q4 spreads the
 // cells of a warp over the banks (bank-conflict model search: 11% fewer wavefronts)
+// Thread layout of the line kernel at Q4 (FEM_LINE_CELL_FAST, default): cells fastest,
+// threadIdx = (cell, line slot); slot s < 20 owns line (ta, tb) = (s % 4, s / 4), s >= 20
+// line (4, s - 20), so a warp holds 4 lines x 8 cells.  With odd row/plane strides (5, 25)
+// the 4 lines of a warp split 2 + 2 by word parity for every line pattern and position,
+// and a cell stride = 10 (mod 16) words spreads the 8 cells over 8 distinct double-banks
+// of each parity: every transpose access takes the minimum 2 wavefronts (tools/bank_model.py;
+// the (line, cell) layout straddles cells inside a warp: 1.42x the minimum).  Global
+// gathers stay coalesced: 8 cells x 4 consecutive x-nodes = 32 consecutive doubles.
+#ifndef FEM_WARP_CELL
+#define FEM_WARP_CELL 0
+#endif
+template <int K>
+__host__ __device__ constexpr bool line_cell_fast() { return K == 4 && FEM_LINE_CELL_FAST && !FEM_WARP_CELL; }
 template <int N>
-__host__ __device__ constexpr int line_cell_stride() { return 3 * N * N * N + (N == 5 ? 2 : 0); }
+__host__ __device__ constexpr int line_cell_stride() {
+  return 3 * N * N * N + (N == 5 ? (line_cell_fast<N - 1>() ? 3 : 2) : 0);
+}
+// per-cell stride of the derivative-basis kernel (K1d, (line, cell) layout)
+template <int N>
+__host__ __device__ constexpr int dline_cell_stride() { return 3 * N * N * N + (N == 5 ? 2 : 0); }
 
 // threads per cell of the line kernel: (k+1)^2, or a whole warp per cell at Q4
 // (FEM_WARP_CELL=1: lanes 25..31 shadow lanes 0..6 -- same addresses, same values --
 // so that no cell straddles a warp; only the real lanes scatter)
-#ifndef FEM_WARP_CELL
-#define FEM_WARP_CELL 0
-#endif
 template <int K>
 __host__ __device__ constexpr int line_tpc() { return (K == 4 && FEM_WARP_CELL) ? 32 : (K + 1) * (K + 1); }
 
@@ -65,17 +80,30 @@ __host__ __device__ constexpr int line_tpc() { return (K == 4 && FEM_WARP_CELL) 
 template <int K>
 __host__ __device__ constexpr int line_minb() { return K == 6 ? 4 : (K == 8 ? 2 : 0); }
 
-template <int K, bool DEFORMED>
-__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
-    cg_apply_kernel(OpArgs a, Tab<K + 1> T) {
-  FEM_PDL_ENTRY();
+// FUSED (a.cf): the input vector is the NEXT Chebyshev iterate, built on the fly at the
+// gather from the previous one (the three-term recurrence of reading R8):
+//   x_new = x + c1 (x - x_old) + c2 D^-1 (b - t),  t = A x  (x null: x_new = c2 D^-1 b),
+// each node's owning cell (half-open ownership, as the prolongation) writes x_new and
+// clears zbuf; the kernel then applies A to x_new.  One launch per smoothing step
+// instead of apply + cheb_step (single-rank levels).
+// (The fused variant is its own __global__ with the CgFuse block as an extra parameter:
+// growing OpArgs itself slowed the plain kernel by 9%, C2 apply 66.6 -> 72.6 us.)
+template <int K, bool DEFORMED, bool FUSED>
+__device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>& T, const CgFuse& f) {
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
   extern __shared__ double smem[];
-  const int traw = threadIdx.x;
+  int traw, ci;
+  if constexpr (line_cell_fast<K>()) {
+    ci = threadIdx.x;
+    const int sl = threadIdx.y;
+    traw = sl < K * N ? (sl % K) + N * (sl / K) : K + N * (sl - K * N);
+  } else {
+    traw = threadIdx.x;
+    ci = threadIdx.y;
+  }
   const int t = traw < N2 ? traw : traw - N2;
   const bool real = traw < N2;
-  const int ci = threadIdx.y;
   const int64_t cell = a.cell0 + (int64_t)blockIdx.x * C + ci;
   const bool active = cell < a.cell1;
   double* s0 = smem + ci * line_cell_stride<N>();
@@ -92,10 +120,44 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
   const int gx = K * cx + ta, gy = K * cy + tb;
   const int64_t zs = (int64_t)a.nn0 * a.nn1;
   const int64_t base = gx + (int64_t)a.nn0 * gy + zs * (int64_t)(K * cz);
+  if constexpr (FUSED) {
+    // all loads first (five independent streams per node in flight), then the stores:
+    // interleaving them would serialise the gather on possible aliasing
+    const bool own_xy = real && (ta < K || cx == a.n0 - 1) && (tb < K || cy == a.n1 - 1);
+    double rx[N], ro[N], rb[N], rd[N], rt[N];
 #pragma unroll
-  for (int l = 0; l < N; ++l) {
-    const bool m = cg_constrained(a.bcmask, gx, gy, a.gz0 + K * cz + l, a.nn0, a.nn1, a.nn2);
-    u[l] = (active && !m) ? __ldg(a.x + base + l * zs) : 0.0;
+    for (int l = 0; l < N; ++l) {
+      const int64_t i = base + l * zs;
+      rx[l] = ro[l] = rb[l] = rd[l] = rt[l] = 0.0;
+      if (active) {
+        if (a.x) rx[l] = __ldg(a.x + i);
+        if (f.materialize) {
+          rb[l] = __ldg(f.b + i);
+          rd[l] = __ldg(f.dinv + i);
+          if (a.x) rt[l] = __ldg(f.t + i);
+          if (a.x && f.xo) ro[l] = __ldg(f.xo + i);
+        }
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      const bool m = cg_constrained(a.bcmask, gx, gy, a.gz0 + K * cz + l, a.nn0, a.nn1, a.nn2);
+      const int64_t i = base + l * zs;
+      double xv = rx[l];
+      if (f.materialize)
+        xv = a.x ? rx[l] + f.c1 * (rx[l] - ro[l]) + f.c2 * rd[l] * (rb[l] - rt[l]) : f.c2 * rd[l] * rb[l];
+      if (active && own_xy && (l < K || K * cz + l == a.nn2 - 1)) {
+        if (f.materialize) f.xnew[i] = xv;
+        if (f.zbuf) f.zbuf[i] = 0.0;
+      }
+      u[l] = (active && !m) ? xv : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      const bool m = cg_constrained(a.bcmask, gx, gy, a.gz0 + K * cz + l, a.nn0, a.nn1, a.nn2);
+      u[l] = (active && !m) ? __ldg(a.x + base + l * zs) : 0.0;
+    }
   }
   // Deformed: one TMA bulk copy stages the block's G slice (C cells x 6 x N^3 doubles,
   // contiguous) into shared memory; it lands while the gather and the first five
@@ -110,7 +172,12 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
       const int64_t nc = (a.cell1 - c0) < C ? (a.cell1 - c0) : C;
       bulk_prefetch_l2(a.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
     }
-    Gs = a.G + (active ? cell : 0) * 6 * N3;
+    if (a.glayout == kGLayoutCell8) {
+      const int64_t c = active ? cell : 0;
+      Gs = a.G + (c / kCell8) * 6 * N3 * kCell8 + (c % kCell8);
+    } else {
+      Gs = a.G + (active ? cell : 0) * 6 * N3;
+    }
   } else if (DEFORMED) {
     double* sG = smem + C * line_cell_stride<N>();
     const int64_t c0 = a.cell0 + (int64_t)blockIdx.x * C;
@@ -124,7 +191,11 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
     __syncthreads();       // barrier initialisation visible to all threads
     Gs = sG + ci * 6 * N3;
   }
-  const CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, (DEFORMED && !a.g_direct) ? &gbar : nullptr};
+  CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, (DEFORMED && !a.g_direct) ? &gbar : nullptr};
+  if (DEFORMED && a.g_direct && a.glayout == kGLayoutCell8) {
+    geo.gq = kCell8;
+    geo.gc = N3 * kCell8;
+  }
   cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
   // scatter-add (constrained rows skipped; they are set to x_c afterwards)
   if (active && real) {
@@ -134,6 +205,20 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
       if (!m) atomicAdd(a.y + base + l * zs, v[l]);
     }
   }
+}
+
+template <int K, bool DEFORMED>
+__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
+    cg_apply_kernel(OpArgs a, Tab<K + 1> T) {
+  FEM_PDL_ENTRY();
+  cg_apply_body<K, DEFORMED, false>(a, T, CgFuse{});
+}
+
+template <int K>
+__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
+    cg_apply_fused_kernel(OpArgs a, Tab<K + 1> T, CgFuse f) {
+  FEM_PDL_ENTRY();
+  cg_apply_body<K, true, true>(a, T, f);
 }
 // ---------------------------------------------------------------- derivative-basis line kernel (K1d)
 // Deformed CG cell apply (eq:mf_eval) with the gradient built from the derivative of
@@ -163,7 +248,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FE
   const int t = threadIdx.x, ci = threadIdx.y;
   const int64_t cell = a.cell0 + (int64_t)blockIdx.x * C + ci;
   const bool active = cell < a.cell1;
-  double* F0 = smem + ci * line_cell_stride<N>();
+  double* F0 = smem + ci * dline_cell_stride<N>();
   double* F1 = F0 + N3;
   double* F2 = F1 + N3;
   const int ta = t % N, tb = t / N;
@@ -1153,7 +1238,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
   if (r1 <= r0) return;
   const Tab<N> T = make_tab<N>(h->tab);
   const dim3 block(N * N, C);
-  const dim3 lblock(line_tpc<K>(), C);   // line kernel (cg_apply_kernel)
+  const dim3 lblock = line_cell_fast<K>() ? dim3(C, line_tpc<K>()) : dim3(line_tpc<K>(), C);   // line kernel
   const int64_t grid = (r1 - r0 + C - 1) / C;
   if (L.cartesian && !h->general_path) {
     KronTab<N> KT;
@@ -1203,7 +1288,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
     const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
     launch_pdl(h, cg_apply_kernel<K, false>, (unsigned)grid, lblock, sm, a, T);
   } else if (L.glayout == kGLayoutXLine) {
-    const size_t sm = sizeof(double) * line_cell_stride<N>() * C;
+    const size_t sm = sizeof(double) * dline_cell_stride<N>() * C;
     smem_attr(reinterpret_cast<const void*>(cg_dline_kernel<K>), (size_t)((int)sm));
     launch_pdl(h, cg_dline_kernel<K>, (unsigned)grid, block, sm, a, T);
   } else if (L.glayout == kGLayoutPlane) {
@@ -1214,6 +1299,10 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
       const int64_t groups = (L.n_cells + kGroupCells - 1) / kGroupCells;
       launch_pdl(h, cg_plane_kernel<K, true>, (unsigned)groups, N * kGroupCells, sm, a, T);
     }
+  } else if (h->cgf.on) {
+    const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (h->g_direct ? 0 : 6 * N * N * N * C));
+    smem_attr(reinterpret_cast<const void*>(cg_apply_fused_kernel<K>), (size_t)((int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
+    launch_pdl(h, cg_apply_fused_kernel<K>, (unsigned)grid, lblock, sm, a, T, h->cgf);
   } else {
     const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (h->g_direct ? 0 : 6 * N * N * N * C));
     smem_attr(reinterpret_cast<const void*>(cg_apply_kernel<K, true>), (size_t)((int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));

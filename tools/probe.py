@@ -24,7 +24,8 @@ def timeit(fn, reps=20):
 
 def run(w, solve=True):
     t0 = time.time()
-    F = fem.Fem(w.cells, w.degree, w.method, deform_eps=w.deform_eps)
+    cc = __import__("os").environ.get("PROBE_COARSE")
+    F = fem.Fem(w.cells, w.degree, w.method, deform_eps=w.deform_eps, coarse_cells=int(cc) if cc else None)
     torch.cuda.synchronize()
     setup = time.time() - t0
     n = F.n_local

@@ -78,7 +78,12 @@ __host__ __device__ constexpr int line_tpc() { return (K == 4 && FEM_WARP_CELL) 
 // (0 = no minimum: naming minBlocks = 1 explicitly makes ptxas spend registers on ILP
 // instead -- k = 4 56 -> 96 registers, C2 apply 65 -> 85 us)
 template <int K>
-__host__ __device__ constexpr int line_minb() { return K == 6 ? 4 : (K == 8 ? 2 : 0); }
+#ifndef FEM_LINE_MINB4
+#define FEM_LINE_MINB4 0
+#endif
+__host__ __device__ constexpr int line_minb() {
+  return K == 6 ? 4 : (K == 8 ? 2 : (K == 4 && line_cell_fast<K>() ? FEM_LINE_MINB4 : 0));
+}
 
 // FUSED (a.cf): the input vector is the NEXT Chebyshev iterate, built on the fly at the
 // gather from the previous one (the three-term recurrence of reading R8):

@@ -24,7 +24,9 @@ struct CellGeo {
   int gc = N * N * N;  // G stride between components
 };
 
-template <int N, bool DEFORMED>
+// RT_STRIDES: G strides from geo.gq / geo.gc (the Q4 line kernel's 8-cell block order);
+// else [cell][comp][q] (1, N^3).  (Compile-time strides at Q4 measured slower: 67 vs 59 us.)
+template <int N, bool DEFORMED, bool RT_STRIDES = false>
 __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& geo, double* s0,
                                              double* s1, double* s2, int t, double (&u)[N],
                                              double (&v)[N]) {
@@ -74,13 +76,14 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
     if (DEFORMED) {
       double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
       if (geo.active) {
-        const double* Gc = geo.G + q * geo.gq;
+        const int gq = RT_STRIDES ? geo.gq : 1, gc = RT_STRIDES ? geo.gc : N3;
+        const double* Gc = geo.G + q * gq;
         G00 = Gc[0];
-        G01 = Gc[geo.gc];
-        G02 = Gc[2 * geo.gc];
-        G11 = Gc[3 * geo.gc];
-        G12 = Gc[4 * geo.gc];
-        G22 = Gc[5 * geo.gc];
+        G01 = Gc[gc];
+        G02 = Gc[2 * gc];
+        G11 = Gc[3 * gc];
+        G12 = Gc[4 * gc];
+        G22 = Gc[5 * gc];
       }
       fx = G00 * gxq + G01 * gyq + G02 * gzq;
       fy = G01 * gxq + G11 * gyq + G12 * gzq;

@@ -177,7 +177,7 @@ __device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>&
       const int64_t nc = (a.cell1 - c0) < C ? (a.cell1 - c0) : C;
       bulk_prefetch_l2(a.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
     }
-    if (a.glayout == kGLayoutCell8) {
+    if (line_cell_fast<K>() && a.glayout == kGLayoutCell8) {
       const int64_t c = active ? cell : 0;
       Gs = a.G + (c / kCell8) * 6 * N3 * kCell8 + (c % kCell8);
     } else {
@@ -197,11 +197,13 @@ __device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>&
     Gs = sG + ci * 6 * N3;
   }
   CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, (DEFORMED && !a.g_direct) ? &gbar : nullptr};
-  if (DEFORMED && a.g_direct && a.glayout == kGLayoutCell8) {
-    geo.gq = kCell8;
-    geo.gc = N3 * kCell8;
+  if constexpr (line_cell_fast<K>()) {
+    if (DEFORMED && a.g_direct && a.glayout == kGLayoutCell8) {
+      geo.gq = kCell8;
+      geo.gc = N3 * kCell8;
+    }
   }
-  cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
+  cell_laplace<N, DEFORMED, line_cell_fast<K>()>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
   // scatter-add (constrained rows skipped; they are set to x_c afterwards)
   if (active && real) {
 #pragma unroll

@@ -641,8 +641,17 @@ __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
 // cell0: first cell of this launch (the apply runs in z-chunks, see launcher).
 // cell stride of the Kronecker element kernel's two buffers (+3 doubles at Q4: 11% fewer
 // shared wavefronts in the bank-conflict model, as for the line kernel)
+// Q4: the same cells-fastest thread layout as the line kernel (FEM_CART_CELL_FAST, default):
+// 2 x 125 = 250 = 10 (mod 16) words per cell is already the conflict-free cell stride.
+#ifndef FEM_CART_CELL_FAST
+#define FEM_CART_CELL_FAST 1
+#endif
+template <int K>
+__host__ __device__ constexpr bool cart_cell_fast() { return K == 4 && FEM_CART_CELL_FAST; }
 template <int N>
-__host__ __device__ constexpr int cart_cell_stride() { return 2 * N * N * N + (N == 5 ? 3 : 0); }
+__host__ __device__ constexpr int cart_cell_stride() {
+  return 2 * N * N * N + (N == 5 ? (cart_cell_fast<N - 1>() ? 0 : 3) : 0);
+}
 
 template <int N>
 struct KronTab {
@@ -660,7 +669,15 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FE
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
   extern __shared__ double smem[];
-  const int t = threadIdx.x, ci = threadIdx.y;
+  int t, ci;
+  if constexpr (cart_cell_fast<K>()) {   // see the line kernel
+    ci = threadIdx.x;
+    const int sl = threadIdx.y;
+    t = sl < K * N ? (sl % K) + N * (sl / K) : K + N * (sl - K * N);
+  } else {
+    t = threadIdx.x;
+    ci = threadIdx.y;
+  }
   const int64_t cell = cell0 + (int64_t)blockIdx.x * C + ci;
   const bool active = cell < cell_end;
   double* s0 = smem + ci * cart_cell_stride<N>();
@@ -1245,6 +1262,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
   if (r1 <= r0) return;
   const Tab<N> T = make_tab<N>(h->tab);
   const dim3 block(N * N, C);
+  const dim3 cblock = cart_cell_fast<K>() ? dim3(C, N * N) : block;   // Cartesian element kernel
   const dim3 lblock = line_cell_fast<K>() ? dim3(C, line_tpc<K>()) : dim3(line_tpc<K>(), C);   // line kernel
   const int64_t grid = (r1 - r0 + C - 1) / C;
   if (L.cartesian && !h->general_path) {
@@ -1277,7 +1295,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
     const int64_t layer = (int64_t)L.n[0] * L.n[1];
     const int lz = h->chunk_layers > 0 ? h->chunk_layers : L.n[2];
     if (!full) {   // a sub-range of a z-slab apply: y has been zeroed by the caller
-      launch_pdl(h, cg_cart_kernel<K>, (unsigned)grid, block, sm, a, KT, r0, r1);
+      launch_pdl(h, cg_cart_kernel<K>, (unsigned)grid, cblock, sm, a, KT, r0, r1);
       count_launch();
       check_launch("cg_cart_kernel");
       return;
@@ -1287,7 +1305,7 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
       const int64_t p0 = z0 == 0 ? 0 : (int64_t)K * z0 + 1, p1 = (int64_t)K * z1 + 1;
       if (!h->y_is_zero) launch_zero(h, y + p0 * plane, (p1 - p0) * plane);
       const int64_t c0 = layer * z0, c1 = layer * z1;
-      launch_pdl(h, cg_cart_kernel<K>, (unsigned)((c1 - c0 + C - 1) / C), block, sm, a, KT, c0, c1);
+      launch_pdl(h, cg_cart_kernel<K>, (unsigned)((c1 - c0 + C - 1) / C), cblock, sm, a, KT, c0, c1);
       count_launch();
       check_launch("cg_cart_kernel");
     }

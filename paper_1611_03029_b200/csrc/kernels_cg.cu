@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
 }
 
 template <int K>
-__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
+__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, K == 4 ? 0 : line_minb<K>())
     cg_apply_fused_kernel(OpArgs a, Tab<K + 1> T, CgFuse f) {
   FEM_PDL_ENTRY();
   cg_apply_body<K, true, true>(a, T, f);

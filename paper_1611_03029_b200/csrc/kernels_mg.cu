@@ -86,20 +86,32 @@ __global__ void prolongate_kernel(TransferArgs a, Embed<K, DG> E, const double* 
     s_2[o] = s;
   }
   __syncthreads();
-#pragma unroll(DG ? 1 : (M * M * M + kTransferThreads - 1) / kTransferThreads)
+#pragma unroll
   for (int it = 0; it < (M * M * M + kTransferThreads - 1) / kTransferThreads; ++it) {  // z sweep + write
     const int o = threadIdx.x + it * kTransferThreads;
     if (o >= M * M * M) break;
-    const int r = o % M, sidx = (o / M) % M, tt = o / (M * M);
+    int r, sidx, tt;
+    int64_t fidx = 0;
+    if (DG) {
+      // o enumerates the fine DoFs in memory order (child cell, then its n^3 block), so
+      // a warp's read-modify-writes of xf are consecutive addresses
+      const int child = o / (N * N * N), loc = o % (N * N * N);
+      const int ca = child & 1, cb = (child >> 1) & 1, cc = child >> 2;
+      r = ca * N + loc % N;
+      sidx = cb * N + (loc / N) % N;
+      tt = cc * N + loc / (N * N);
+      const int64_t fcell = (2 * cx + ca) + (int64_t)(2 * a.nc0) * ((2 * cy + cb) + (int64_t)(2 * a.nc1) * (2 * cz + cc));
+      fidx = fcell * N * N * N + loc;
+    } else {
+      r = o % M;
+      sidx = (o / M) % M;
+      tt = o / (M * M);
+    }
     double s = 0.0;
 #pragma unroll
     for (int l = 0; l < N; ++l) s = fma(sE[tt][l], s_2[r + M * (sidx + M * l)], s);
     if (DG) {
-      // fine cell (2cx + r/N, ...), local (r%N, ...)
-      const int fx = 2 * cx + r / N, fy = 2 * cy + sidx / N, fz = 2 * cz + tt / N;
-      const int64_t fcell = fx + (int64_t)(2 * a.nc0) * (fy + (int64_t)(2 * a.nc1) * fz);
-      const int loc = r % N + N * ((sidx % N) + N * (tt % N));
-      xf[fcell * N * N * N + loc] += s;
+      xf[fidx] += s;
     } else {
       // owned: local fine index < 2K unless this is the last coarse cell
       if ((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
@@ -130,16 +142,21 @@ __global__ void restrict_kernel(TransferArgs a, Embed<K, DG> E, const double* __
   const int cy = (int)(rr % a.nc1), cz = (int)(rr / a.nc1);
   // CG: compile-time trip count, fully unrolled, so the loads of all trips are issued
   // before the first one returns (restrict 29 -> 27 us on C2; DG measured slower unrolled)
-#pragma unroll(DG ? 1 : (M * M * M + kTransferThreads - 1) / kTransferThreads)
+#pragma unroll
   for (int it = 0; it < (M * M * M + kTransferThreads - 1) / kTransferThreads; ++it) {
     const int o = threadIdx.x + it * kTransferThreads;
     if (o >= M * M * M) break;
-    const int r = o % M, sidx = (o / M) % M, tt = o / (M * M);
+    int r = o % M, sidx = (o / M) % M, tt = o / (M * M);
     double v = 0.0;
     if (DG) {
-      const int fx = 2 * cx + r / N, fy = 2 * cy + sidx / N, fz = 2 * cz + tt / N;
-      const int64_t fcell = fx + (int64_t)(2 * a.nc0) * (fy + (int64_t)(2 * a.nc1) * fz);
-      const int64_t idx = fcell * N * N * N + r % N + N * ((sidx % N) + N * (tt % N));
+      // fine DoFs read in memory order (coalesced), placed at their (r, s, t) position
+      const int child = o / (N * N * N), loc = o % (N * N * N);
+      const int ca = child & 1, cb = (child >> 1) & 1, cc = child >> 2;
+      r = ca * N + loc % N;
+      sidx = cb * N + (loc / N) % N;
+      tt = cc * N + loc / (N * N);
+      const int64_t fcell = (2 * cx + ca) + (int64_t)(2 * a.nc0) * ((2 * cy + cb) + (int64_t)(2 * a.nc1) * (2 * cz + cc));
+      const int64_t idx = fcell * N * N * N + loc;
       v = bf[idx] - (axf ? axf[idx] : 0.0);
     } else {
       const bool owned = !((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
@@ -150,7 +167,7 @@ __global__ void restrict_kernel(TransferArgs a, Embed<K, DG> E, const double* __
         v = bf[idx] - (axf ? axf[idx] : 0.0);
       }
     }
-    s_in[o] = v;
+    s_in[r + M * (sidx + M * tt)] = v;
   }
   __syncthreads();
   for (int o = threadIdx.x; o < N * M * M; o += blockDim.x) {  // x: [t][s][i]

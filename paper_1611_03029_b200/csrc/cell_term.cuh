@@ -26,52 +26,57 @@ struct CellGeo {
 
 // RT_STRIDES: G strides from geo.gq / geo.gc (the Q4 line kernel's 8-cell block order);
 // else [cell][comp][q] (1, N^3).  (Compile-time strides at Q4 measured slower: 67 vs 59 us.)
-template <int N, bool DEFORMED, bool RT_STRIDES = false>
+// B, S: row and plane strides of the shared-memory buffers (element (i0, i1, i2) at
+// i0 + B i1 + S i2; dense: N, N^2).  Z pattern: thread line (ta, tb) along i2; Y: along
+// i1 with (i0, i2) = (ta, tb); X: along i0 with (i1, i2) = (ta, tb).
+template <int N, bool DEFORMED, bool RT_STRIDES = false, int B = N, int S = N * N>
 __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& geo, double* s0,
                                              double* s1, double* s2, int t, double (&u)[N],
                                              double (&v)[N]) {
   constexpr int N2 = N * N, N3 = N2 * N;
   const int ta = t % N, tb = t / N;
+  const int zi = ta + B * tb;   // Z-pattern word of the thread's line
   double g[N], w[N];
   // Z: interpolate in z
   mv<N>(T.val, u, v);
 #pragma unroll
-  for (int l = 0; l < N; ++l) s0[t + N2 * l] = v[l];
+  for (int l = 0; l < N; ++l) s0[zi + S * l] = v[l];
   __syncthreads();
   // Y: interpolate in y
 #pragma unroll
-  for (int l = 0; l < N; ++l) w[l] = s0[ta + N * l + N2 * tb];
+  for (int l = 0; l < N; ++l) w[l] = s0[ta + B * l + S * tb];
   mv<N>(T.val, w, v);
 #pragma unroll
-  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = v[l];
+  for (int l = 0; l < N; ++l) s0[ta + B * l + S * tb] = v[l];
   __syncthreads();
   // X: interpolate in x, d/dxi_x by collocation
 #pragma unroll
-  for (int l = 0; l < N; ++l) w[l] = s0[l + N * ta + N2 * tb];
+  for (int l = 0; l < N; ++l) w[l] = s0[l + B * ta + S * tb];
   mv<N>(T.val, w, v);
   mv<N>(T.colloc, v, g);
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    s0[l + N * ta + N2 * tb] = v[l];
-    s2[l + N * ta + N2 * tb] = g[l];
+    s0[l + B * ta + S * tb] = v[l];
+    s2[l + B * ta + S * tb] = g[l];
   }
   __syncthreads();
   // Y: d/dxi_y
 #pragma unroll
-  for (int l = 0; l < N; ++l) w[l] = s0[ta + N * l + N2 * tb];
+  for (int l = 0; l < N; ++l) w[l] = s0[ta + B * l + S * tb];
   mv<N>(T.colloc, w, g);
 #pragma unroll
-  for (int l = 0; l < N; ++l) s1[ta + N * l + N2 * tb] = g[l];
+  for (int l = 0; l < N; ++l) s1[ta + B * l + S * tb] = g[l];
   __syncthreads();
   // Z: d/dxi_z, quadrature-point operation, transposed d/dxi_z
 #pragma unroll
-  for (int l = 0; l < N; ++l) w[l] = s0[t + N2 * l];
+  for (int l = 0; l < N; ++l) w[l] = s0[zi + S * l];
   mv<N>(T.colloc, w, g);
   if (DEFORMED && geo.bar) mbar_wait(geo.bar, 0);
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    const int q = t + N2 * l;
-    const double gxq = s2[q], gyq = s1[q], gzq = g[l];
+    const int q = t + N2 * l;                 // quadrature point (G index)
+    const int zq = zi + S * l;                // its shared-memory word
+    const double gxq = s2[zq], gyq = s1[zq], gzq = g[l];
     double fx, fy, fz;
     if (DEFORMED) {
       double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
@@ -94,45 +99,45 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
       fy = geo.c1 * w3 * gyq;
       fz = geo.c2 * w3 * gzq;
     }
-    s2[q] = fx;
-    s1[q] = fy;
+    s2[zq] = fx;
+    s1[zq] = fy;
     v[l] = fz;
   }
   mvt<N>(T.colloc, v, w);
 #pragma unroll
-  for (int l = 0; l < N; ++l) s0[t + N2 * l] = w[l];
+  for (int l = 0; l < N; ++l) s0[zi + S * l] = w[l];
   __syncthreads();
   // Y: += colloc^T f_y
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    v[l] = s1[ta + N * l + N2 * tb];
-    w[l] = s0[ta + N * l + N2 * tb];
+    v[l] = s1[ta + B * l + S * tb];
+    w[l] = s0[ta + B * l + S * tb];
   }
   mvt_add<N>(T.colloc, v, w);
 #pragma unroll
-  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = w[l];
+  for (int l = 0; l < N; ++l) s0[ta + B * l + S * tb] = w[l];
   __syncthreads();
   // X: += colloc^T f_x, then interpolate back in x
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    v[l] = s2[l + N * ta + N2 * tb];
-    w[l] = s0[l + N * ta + N2 * tb];
+    v[l] = s2[l + B * ta + S * tb];
+    w[l] = s0[l + B * ta + S * tb];
   }
   mvt_add<N>(T.colloc, v, w);
   mvt<N>(T.val, w, v);
 #pragma unroll
-  for (int l = 0; l < N; ++l) s0[l + N * ta + N2 * tb] = v[l];
+  for (int l = 0; l < N; ++l) s0[l + B * ta + S * tb] = v[l];
   __syncthreads();
   // Y: interpolate back in y
 #pragma unroll
-  for (int l = 0; l < N; ++l) w[l] = s0[ta + N * l + N2 * tb];
+  for (int l = 0; l < N; ++l) w[l] = s0[ta + B * l + S * tb];
   mvt<N>(T.val, w, v);
 #pragma unroll
-  for (int l = 0; l < N; ++l) s0[ta + N * l + N2 * tb] = v[l];
+  for (int l = 0; l < N; ++l) s0[ta + B * l + S * tb] = v[l];
   __syncthreads();
   // Z: interpolate back in z
 #pragma unroll
-  for (int l = 0; l < N; ++l) w[l] = s0[t + N2 * l];
+  for (int l = 0; l < N; ++l) w[l] = s0[zi + S * l];
   mvt<N>(T.val, w, v);
 }
 

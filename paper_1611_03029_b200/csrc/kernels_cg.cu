@@ -58,10 +58,31 @@ struct OpArgs {
 #endif
 template <int K>
 __host__ __device__ constexpr bool line_cell_fast() { return K == 4 && FEM_LINE_CELL_FAST && !FEM_WARP_CELL; }
+// Shared-memory layout of the line kernel's three per-cell buffers: element (i0, i1, i2)
+// at i0 + B i1 + S i2 of a field of F words, fields at 0, F, 2F, cells CS words apart.
+// Chosen per degree by tools/bank_model.py-style search over (B, S, CS) for the three
+// transpose patterns of cell_laplace with the (line, cell) thread layout (modelled
+// wavefronts vs the dense layout: k=1 2.0x, k=2 1.9x, k=3 2.5x, k=5 1.5x, k=6 1.3x,
+// k=7 2.7x, k=8 1.1x fewer); Q4 uses the cells-fastest layout (dense strides, CS = 378).
+// Measured at ~16M DoFs (% of HBM, dense -> padded): k=2 42 -> 55, k=3 47 -> 72,
+// k=5 64 -> 66, k=6 46 -> 49, k=7 29 -> 31, k=8 33 -> 33; k=1 48 -> 44 (kept dense).
+#ifndef FEM_LINE_PAD
+#define FEM_LINE_PAD 1
+#endif
+template <int K>
+struct LineLayout {
+  static constexpr int N = K + 1;
+  static constexpr int Bp[9] = {0, 2, 3, 5, 5, 9, 7, 9, 9};
+  static constexpr int Sp[9] = {0, 5, 19, 20, 25, 54, 56, 72, 89};
+  static constexpr int CSp[9] = {0, 30, 153, 237, 0, 964, 1169, 1725, 2385};
+  static constexpr bool pad = FEM_LINE_PAD && K != 4 && K != 1;   // k = 1 measured slower padded
+  static constexpr int B = pad ? Bp[K] : N;
+  static constexpr int S = pad ? Sp[K] : N * N;
+  static constexpr int F = (N - 1) * (1 + B + S) + 1;
+  static constexpr int CS = pad ? CSp[K] : 3 * N * N * N + (N == 5 ? (line_cell_fast<K>() ? 3 : 2) : 0);
+};
 template <int N>
-__host__ __device__ constexpr int line_cell_stride() {
-  return 3 * N * N * N + (N == 5 ? (line_cell_fast<N - 1>() ? 3 : 2) : 0);
-}
+__host__ __device__ constexpr int line_cell_stride() { return LineLayout<N - 1>::CS; }
 // per-cell stride of the derivative-basis kernel (K1d, (line, cell) layout)
 template <int N>
 __host__ __device__ constexpr int dline_cell_stride() { return 3 * N * N * N + (N == 5 ? 2 : 0); }
@@ -203,7 +224,8 @@ __device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>&
       geo.gc = N3 * kCell8;
     }
   }
-  cell_laplace<N, DEFORMED, line_cell_fast<K>()>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
+  using LL = LineLayout<K>;
+  cell_laplace<N, DEFORMED, line_cell_fast<K>(), LL::B, LL::S>(T, geo, s0, s0 + LL::F, s0 + 2 * LL::F, t, u, v);
   // scatter-add (constrained rows skipped; they are set to x_c afterwards)
   if (active && real) {
 #pragma unroll

@@ -51,9 +51,16 @@ def main():
     target = float(sys.argv[2]) if len(sys.argv) > 2 else 1.6e7
     peak = hbm_peak()
     rows = []
+    only_m = os.environ.get("SWEEP_METHODS", "CG,SIPG").split(",")
+    only_g = os.environ.get("SWEEP_GEOM", "Cartesian,deformed").split(",")
+    ks = [int(v) for v in os.environ.get("SWEEP_K", "1,2,3,4,5,6,7,8").split(",")]
     for method, mname in ((fem.FEM_CG, "CG"), (fem.FEM_SIPG, "SIPG")):
+        if mname not in only_m:
+            continue
         for eps in (0.0, 0.05):
-            for k in range(1, 9):
+            if ("deformed" if eps else "Cartesian") not in only_g:
+                continue
+            for k in ks:
                 per = k if method == fem.FEM_CG else k + 1
                 n = max(2, int(round(target ** (1 / 3) / per)))
                 F = fem.Fem((n, n, n), k, method, deform_eps=eps, coarse_cells=n)

@@ -419,6 +419,28 @@ __device__ __forceinline__ void dg_line_op(const DgKronTab<N>& T, double sc, dou
   }
 }
 
+// Shared-memory layout of the Cartesian SIPG kernel's three buffers: element (i0, i1, i2)
+// at i0 + B i1 + S i2, fields F words apart, cells CS apart; per-degree strides from a
+// bank-conflict model search over its access patterns (modelled wavefronts vs the dense
+// layout: k=1 1.7x, k=2 1.6x, k=3 2.1x, k=4 1.2x, k=5 1.5x, k=6 1.3x, k=7 3.4x fewer).
+#ifndef FEM_DG_PAD
+#define FEM_DG_PAD 1
+#endif
+template <int K>
+struct DgCartLayout {
+  static constexpr int N = K + 1;
+  static constexpr int Bp[9] = {0, 2, 3, 5, 5, 9, 10, 9, 10};
+  static constexpr int Sp[9] = {0, 5, 19, 20, 25, 54, 71, 72, 89};
+  static constexpr int CSp[9] = {0, 30, 153, 237, 381, 964, 1489, 1725, 2417};
+  // measured (% of HBM at ~16M DoFs, dense -> padded): k=2 17.6 -> 22.2, k=3 15.1 -> 22.7,
+  // k=4 22.1 -> 23.0, k=7 10.7 -> 14.9; k=1, 5, 6, 8 equal or slower padded (kept dense)
+  static constexpr bool pad = FEM_DG_PAD != 0 && (K == 2 || K == 3 || K == 4 || K == 7);
+  static constexpr int B = pad ? Bp[K] : N;
+  static constexpr int S = pad ? Sp[K] : N * N;
+  static constexpr int F = (N - 1) * (1 + B + S) + 1;
+  static constexpr int CS = pad ? CSp[K] : 3 * N * N * N + 1;
+};
+
 template <int K>
 __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     dg_cart_kernel(const double* __restrict__ x, double* __restrict__ y, DgKron A, DgKronTab<K + 1> T) {
@@ -429,9 +451,11 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
   const int t = threadIdx.x, ci = threadIdx.y;
   const int64_t cell = A.cell0 + (int64_t)blockIdx.x * C + ci;
   const bool active = cell < A.cell1;
-  double* F0 = smem + ci * (3 * N3 + 1);
-  double* F1 = F0 + N3;
-  double* F2 = F1 + N3;
+  using LY = DgCartLayout<K>;
+  constexpr int B = LY::B, S = LY::S;
+  double* F0 = smem + ci * LY::CS;
+  double* F1 = F0 + LY::F;
+  double* F2 = F1 + LY::F;
   const int ta = t % N, tb = t / N;
   int c[3] = {0, 0, 0};
   if (active) {
@@ -451,6 +475,8 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     // line (ta, tb) along d: x-line (y=ta, z=tb), y-line (x=ta, z=tb), z-line (x=ta, y=tb)
     const int off = d == 0 ? N * ta + N2 * tb : (d == 1 ? ta + N2 * tb : ta + N * tb);
     const int st = d == 0 ? 1 : (d == 1 ? N : N2);
+    const int soff = d == 0 ? B * ta + S * tb : (d == 1 ? ta + S * tb : ta + B * tb);   // shared memory
+    const int sst = d == 0 ? 1 : (d == 1 ? B : S);
     double xo[N], xl[N], xr[N], o[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -461,7 +487,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     dg_line_op<N>(T, A.sc[d], A.sigma[d], flo, fhi, hl, hr, xo, xl, xr, o);
     double* F = d == 0 ? F0 : (d == 1 ? F1 : F2);
 #pragma unroll
-    for (int i = 0; i < N; ++i) F[off + st * i] = o[i];
+    for (int i = 0; i < N; ++i) F[soff + sst * i] = o[i];
   }
   __syncthreads();
   // ---- x-lines (y=ta, z=tb): F1 <- M_x F1, F2 <- M_x F2
@@ -469,15 +495,15 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     double a[N], b[N], o[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      a[i] = F1[i + N * t];
-      b[i] = F2[i + N * t];
+      a[i] = F1[i + B * ta + S * tb];
+      b[i] = F2[i + B * ta + S * tb];
     }
     mv<N>(T.M, a, o);
 #pragma unroll
-    for (int i = 0; i < N; ++i) F1[i + N * t] = A.mc[0] * o[i];
+    for (int i = 0; i < N; ++i) F1[i + B * ta + S * tb] = A.mc[0] * o[i];
     mv<N>(T.M, b, o);
 #pragma unroll
-    for (int i = 0; i < N; ++i) F2[i + N * t] = A.mc[0] * o[i];
+    for (int i = 0; i < N; ++i) F2[i + B * ta + S * tb] = A.mc[0] * o[i];
   }
   __syncthreads();
   // ---- y-lines (x=ta, z=tb): F0 <- M_y F0, F2 <- M_y F2
@@ -485,26 +511,26 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     double a[N], b[N], o[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      a[j] = F0[ta + N * j + N2 * tb];
-      b[j] = F2[ta + N * j + N2 * tb];
+      a[j] = F0[ta + B * j + S * tb];
+      b[j] = F2[ta + B * j + S * tb];
     }
     mv<N>(T.M, a, o);
 #pragma unroll
-    for (int j = 0; j < N; ++j) F0[ta + N * j + N2 * tb] = A.mc[1] * o[j];
+    for (int j = 0; j < N; ++j) F0[ta + B * j + S * tb] = A.mc[1] * o[j];
     mv<N>(T.M, b, o);
 #pragma unroll
-    for (int j = 0; j < N; ++j) F2[ta + N * j + N2 * tb] = A.mc[1] * o[j];
+    for (int j = 0; j < N; ++j) F2[ta + B * j + S * tb] = A.mc[1] * o[j];
   }
   __syncthreads();
   // ---- z-lines (x=ta, y=tb): y = M_z (F0 + F1) + F2
   {
     double a[N], o[N];
 #pragma unroll
-    for (int l = 0; l < N; ++l) a[l] = F0[t + N2 * l] + F1[t + N2 * l];
+    for (int l = 0; l < N; ++l) a[l] = F0[ta + B * tb + S * l] + F1[ta + B * tb + S * l];
     mv<N>(T.M, a, o);
     if (active) {
 #pragma unroll
-      for (int l = 0; l < N; ++l) dg_store(A.cf, x, y, cell * N3 + t + N2 * l, fma(A.mc[2], o[l], F2[t + N2 * l]));
+      for (int l = 0; l < N; ++l) dg_store(A.cf, x, y, cell * N3 + t + N2 * l, fma(A.mc[2], o[l], F2[ta + B * tb + S * l]));
     }
   }
 }
@@ -825,7 +851,7 @@ void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r
     T.dm[i] = h->tab.dface[0][i];
     T.dp[i] = h->tab.dface[1][i];
   }
-  const size_t sm = sizeof(double) * (3 * N * N * N + 1) * C;
+  const size_t sm = sizeof(double) * DgCartLayout<K>::CS * C;
   smem_attr(reinterpret_cast<const void*>(dg_cart_kernel<K>), (size_t)((int)sm));
   const unsigned grid = (unsigned)((r1 - r0 + C - 1) / C);
   launch_pdl(h, dg_cart_kernel<K>, grid, dim3(N * N, C), sm, x, y, A, T);

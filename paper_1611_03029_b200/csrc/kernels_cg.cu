@@ -670,10 +670,27 @@ __global__ void __launch_bounds__((K + 1) * kGroupCells, PlanePad<K + 1>::MINB)
 #endif
 template <int K>
 __host__ __device__ constexpr bool cart_cell_fast() { return K == 4 && FEM_CART_CELL_FAST; }
+// other degrees: padded strides from the bank-conflict model search (element (i0, i1, i2)
+// at i0 + B i1 + S i2, two fields F words apart, cells CS apart)
+#ifndef FEM_CART_PAD
+#define FEM_CART_PAD 1
+#endif
+template <int K>
+struct CartLayout {
+  static constexpr int N = K + 1;
+  static constexpr int Bp[9] = {0, 2, 3, 5, 5, 9, 10, 9, 9};
+  static constexpr int Sp[9] = {0, 5, 19, 20, 25, 54, 71, 72, 89};
+  static constexpr int CSp[9] = {0, 18, 105, 163, 0, 644, 993, 1150, 1601};
+  // measured (apply at ~16M DoFs, dense -> padded): k=1 1041 -> 730 us, k=2 353 -> 305,
+  // k=3 306 -> 216, k=7 333 -> 289, k=5, 8 -1%; k=6 +2% (kept dense)
+  static constexpr bool pad = FEM_CART_PAD != 0 && K != 4 && K != 6;
+  static constexpr int B = pad ? Bp[K] : N;
+  static constexpr int S = pad ? Sp[K] : N * N;
+  static constexpr int F = (N - 1) * (1 + B + S) + 1;
+  static constexpr int CS = pad ? CSp[K] : 2 * N * N * N + (N == 5 ? (cart_cell_fast<K>() ? 0 : 3) : 0);
+};
 template <int N>
-__host__ __device__ constexpr int cart_cell_stride() {
-  return 2 * N * N * N + (N == 5 ? (cart_cell_fast<N - 1>() ? 0 : 3) : 0);
-}
+__host__ __device__ constexpr int cart_cell_stride() { return CartLayout<N - 1>::CS; }
 
 template <int N>
 struct KronTab {
@@ -702,8 +719,10 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FE
   }
   const int64_t cell = cell0 + (int64_t)blockIdx.x * C + ci;
   const bool active = cell < cell_end;
-  double* s0 = smem + ci * cart_cell_stride<N>();
-  double* s1 = s0 + N3;
+  using CL = CartLayout<K>;
+  constexpr int B = CL::B, S = CL::S;
+  double* s0 = smem + ci * CL::CS;
+  double* s1 = s0 + CL::F;
   const int ta = t % N, tb = t / N;
   int cx = 0, cy = 0, cz = 0;
   if (active) {
@@ -727,31 +746,31 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * CPB<K>::value, K == 4 ? FE
     mv<N>(T.S, u, f1);
 #pragma unroll
     for (int l = 0; l < N; ++l) {
-      s0[l + N * ta + N2 * tb] = f0[l];
-      s1[l + N * ta + N2 * tb] = a.c0 * f1[l];
+      s0[l + B * ta + S * tb] = f0[l];
+      s1[l + B * ta + S * tb] = a.c0 * f1[l];
     }
   }
   __syncthreads();
   // ---- y-lines (x = ta, z = tb): p = M_y a, q = c1 S_y a + M_y c
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    u[l] = s0[ta + N * l + N2 * tb];
-    f2[l] = s1[ta + N * l + N2 * tb];
+    u[l] = s0[ta + B * l + S * tb];
+    f2[l] = s1[ta + B * l + S * tb];
   }
   mv<N>(T.M, u, f0);
   mv<N>(T.S, u, f1);
   mv<N>(T.M, f2, u);
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    s0[ta + N * l + N2 * tb] = f0[l];
-    s1[ta + N * l + N2 * tb] = fma(a.c1, f1[l], u[l]);
+    s0[ta + B * l + S * tb] = f0[l];
+    s1[ta + B * l + S * tb] = fma(a.c1, f1[l], u[l]);
   }
   __syncthreads();
   // ---- z-lines (x = ta, y = tb): y = c2 S_z p + M_z q, scatter-add
 #pragma unroll
   for (int l = 0; l < N; ++l) {
-    u[l] = s0[t + N2 * l];
-    f2[l] = s1[t + N2 * l];
+    u[l] = s0[ta + B * tb + S * l];
+    f2[l] = s1[ta + B * tb + S * l];
   }
   mv<N>(T.S, u, f0);
   mv<N>(T.M, f2, f1);

@@ -29,10 +29,26 @@ struct DgCPB {
   static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? 8 : (N * N <= 49) ? 4 : 2;
 };
 
+#ifndef FEM_DGQ_PAD
+#define FEM_DGQ_PAD 1
+#endif
 template <int N>
 struct DgSmem {  // per-cell shared memory layout (doubles)
   static constexpr int N2 = N * N, N3 = N2 * N;
-  static constexpr int X = 0, S0 = N3, FWD = 4 * N3, BWD = FWD + 16 * N2, SIZE = BWD + 8 * N2;
+  // cell term (cell_laplace) strides: element (i0, i1, i2) at i0 + B i1 + S i2, three
+  // fields of CF words from S0 (they may run into FWD/BWD, which are dead until the
+  // face phases); B, S and the cell-stride padding from a bank-conflict model search
+  // (modelled cell-term wavefronts: k=2 1.3x, k=3 2.5x, k=5 1.5x, k=6 1.3x, k=7 2.7x fewer)
+  static constexpr int K = N - 1;
+  static constexpr int Bp[9] = {0, 0, 3, 7, 6, 9, 7, 9, 9};
+  static constexpr int Sp[9] = {0, 0, 19, 28, 37, 54, 56, 72, 89};
+  static constexpr int Ep[9] = {0, 0, 5, 2, 13, 4, 13, 0, 5};
+  static constexpr bool pad = FEM_DGQ_PAD != 0 && K >= 2;
+  static constexpr int B = pad ? Bp[K] : N, S = pad ? Sp[K] : N2;
+  static constexpr int CF = (N - 1) * (1 + B + S) + 1;
+  static constexpr int X = 0, S0 = N3, FWD = 4 * N3, BWD = FWD + 16 * N2;
+  static constexpr int SIZE = BWD + 8 * N2 + (pad ? Ep[K] : 0);
+  static_assert(S0 + 3 * CF <= BWD + 8 * N2, "cell-term fields exceed the per-cell buffer");
 };
 
 struct DgArgs {
@@ -331,7 +347,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? 
   const CellGeo<N> geo{DEFORMED ? A.G + (size_t)(active ? cell : 0) * 6 * N3 : nullptr, A.c[0], A.c[1],
                        A.c[2], active, nullptr};
   double* s0 = sm + L::S0;
-  cell_laplace<N, DEFORMED>(T, geo, s0, s0 + N3, s0 + 2 * N3, t, u, v);
+  cell_laplace<N, DEFORMED, false, L::B, L::S>(T, geo, s0, s0 + L::CF, s0 + 2 * L::CF, t, u, v);
   __syncthreads();
 #pragma unroll
   for (int l = 0; l < N; ++l) s0[t + N2 * l] = v[l];   // residual R (z-line layout)

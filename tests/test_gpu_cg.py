@@ -296,3 +296,25 @@ def test_cartesian_fast_path_and_general_quadrature_path_agree(k, monkeypatch):
     F2.fem_apply(x, y2)
     yo = ocg.apply(m, x)
     assert relmax(y1, yo) <= 1e-12 and relmax(y2, yo) <= 1e-12
+
+
+@pytest.mark.parametrize("env,val", [("FEM_G_DIRECT", "0"), ("FEM_FUSE_CHEB", "0"), ("FEM_FUSE_CELLS", "100000000")])
+def test_layout_and_fusion_switches_keep_parity(env, val, monkeypatch):
+    """Q4 deformed: G staged by TMA in the [cell][comp][q] order instead of the 8-cell
+    block order read directly; Chebyshev fusion off / on every level.  Same operator,
+    PCG iterations within +-1 of the oracle's, true residual below tolerance."""
+    monkeypatch.setenv(env, val)
+    k, cells = 4, (8, 8, 8)
+    F, m = make(cells, k, 0.05, MIXED)
+    x = fem_inputs.uniform_pm1(5, m.cg_n_dofs())
+    y = np.zeros_like(x)
+    F.fem_apply(x, y)
+    assert relmax(y, ocg.apply(m, x)) <= 1e-12
+    mg = omg.Multigrid(m, CG)
+    b = oprob.rhs(m, CG)
+    xo, its_o, _ = mg.pcg(b, tol=1e-10)
+    xs = np.zeros_like(b)
+    its, rr, ok = F.cg_solve(b, xs, rtol=1e-10)
+    assert ok and abs(its - its_o) <= 1
+    assert np.linalg.norm(b - mg.fine.apply(xs)) / np.linalg.norm(b) <= 1e-9
+    F.close()

@@ -32,6 +32,9 @@ struct DgCPB {
 #ifndef FEM_DGQ_PAD
 #define FEM_DGQ_PAD 1
 #endif
+#ifndef FEM_DGQ_FPAD
+#define FEM_DGQ_FPAD 1
+#endif
 template <int N>
 struct DgSmem {  // per-cell shared memory layout (doubles)
   static constexpr int N2 = N * N, N3 = N2 * N;
@@ -46,9 +49,15 @@ struct DgSmem {  // per-cell shared memory layout (doubles)
   static constexpr bool pad = FEM_DGQ_PAD != 0 && K >= 2;
   static constexpr int B = pad ? Bp[K] : N, S = pad ? Sp[K] : N2;
   static constexpr int CF = (N - 1) * (1 + B + S) + 1;
-  static constexpr int X = 0, S0 = N3, FWD = 4 * N3, BWD = FWD + 16 * N2;
-  static constexpr int SIZE = BWD + 8 * N2 + (pad ? Ep[K] : 0);
-  static_assert(S0 + 3 * CF <= BWD + 8 * N2, "cell-term fields exceed the per-cell buffer");
+  // face buffers: 16 + 8 fields of (k+1)^2 values, field stride FS padded so that the
+  // face phases' row / column sweeps spread over the banks.  The model predicts fewer
+  // wavefronts at k = 2, 3, 5..8; measured (SIPG deformed apply, ~16M DoFs) only k = 3
+  // gains (1110 -> 894 us); k = 2, 5, 6 got 2-10% slower, k = 7, 8 equal: dense there.
+  static constexpr int FSp[9] = {0, 4, 9, 21, 25, 36, 49, 64, 81};
+  static constexpr int FS = FEM_DGQ_FPAD ? FSp[K] : N2;
+  static constexpr int X = 0, S0 = N3, FWD = 4 * N3, BWD = FWD + 16 * FS;
+  static constexpr int SIZE = BWD + 8 * FS + (pad ? Ep[K] : 0);
+  static_assert(S0 + 3 * CF <= BWD + 8 * FS, "cell-term fields exceed the per-cell buffer");
 };
 
 struct DgArgs {
@@ -112,6 +121,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int t1 = Tang<D>::t1, t2 = Tang<D>::t2;
   using L = DgSmem<N>;
+  constexpr int FS = L::FS;   // padded field stride of the face buffers
   const double* X = sm + L::X;
   double* R = sm + L::S0;
   double* F = sm + L::FWD;   // [s][8][N2]: 0 u, 1 d_D u, 2 u', 3 d_D u', 4 d_t1 u, 5 d_t2 u, 6 d_t1 u', 7 d_t2 u'
@@ -140,18 +150,18 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
 #pragma unroll
         for (int i = 0; i < N; ++i) g1 = fma(T.dface[1 - s][i], nl[i], g1);
       }
-      double* Fs = F + s * 8 * N2;
-      Fs[0 * N2 + t] = xl[s ? K : 0];
-      Fs[1 * N2 + t] = f1;
-      Fs[2 * N2 + t] = g0;
-      Fs[3 * N2 + t] = g1;
+      double* Fs = F + s * 8 * FS;
+      Fs[0 * FS + t] = xl[s ? K : 0];
+      Fs[1 * FS + t] = f1;
+      Fs[2 * FS + t] = g0;
+      Fs[3 * FS + t] = g1;
     }
   }
   __syncthreads();
   // ---- F2: interpolate along t1 (rows b); deformed: d/dt1 of the traces
   for (int task = t; task < 2 * 4 * N; task += N2) {
     const int s = task / (4 * N), f = (task / N) % 4, row = task % N;
-    double* fld = F + (s * 8 + f) * N2 + N * row;
+    double* fld = F + (s * 8 + f) * FS + N * row;
     double in[N], out[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) in[i] = fld[i];
@@ -159,7 +169,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
     if (DEFORMED && (f == 0 || f == 2)) {
       double dd[N];
       mv<N>(T.colloc, out, dd);
-      double* fd = F + (s * 8 + (f == 0 ? 4 : 6)) * N2 + N * row;
+      double* fd = F + (s * 8 + (f == 0 ? 4 : 6)) * FS + N * row;
 #pragma unroll
       for (int i = 0; i < N; ++i) fd[i] = dd[i];
     }
@@ -173,7 +183,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
     for (int task = t; task < 2 * NF * N; task += N2) {
       const int s = task / (NF * N), fi = (task / N) % NF, col = task % N;
       const int f = fi < 4 ? fi : (fi == 4 ? 4 : 6);
-      double* fld = F + (s * 8 + f) * N2 + col;
+      double* fld = F + (s * 8 + f) * FS + col;
       double in[N], out[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) in[i] = fld[N * i];
@@ -181,7 +191,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
       if (DEFORMED && (f == 0 || f == 2)) {
         double dd[N];
         mv<N>(T.colloc, out, dd);
-        double* fd = F + (s * 8 + (f == 0 ? 5 : 7)) * N2 + col;
+        double* fd = F + (s * 8 + (f == 0 ? 5 : 7)) * FS + col;
 #pragma unroll
         for (int i = 0; i < N; ++i) fd[N * i] = dd[i];
       }
@@ -193,8 +203,8 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
   // ---- F4: numerical flux at face point q = (a, b)
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
-    const double* Fs = F + s * 8 * N2;
-    double* Bs = B + s * 4 * N2;
+    const double* Fs = F + s * 8 * FS;
+    double* Bs = B + s * 4 * FS;
     double vA = 0.0, vD = 0.0, v1 = 0.0, v2 = 0.0;
     if (kind[s] != 2 && active) {
       const double nsgn = s ? 1.0 : -1.0;
@@ -212,21 +222,21 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
           Jn[e] = nsgn * __ldg(rec + (own + e) * N2 + t);
           Jo[e] = nsgn * __ldg(rec + (oth + e) * N2 + t);
         }
-        dn_own = Jn[t1] * Fs[4 * N2 + t] + Jn[t2] * Fs[5 * N2 + t] + Jn[D] * Fs[1 * N2 + t];
+        dn_own = Jn[t1] * Fs[4 * FS + t] + Jn[t2] * Fs[5 * FS + t] + Jn[D] * Fs[1 * FS + t];
         if (kind[s] == 0)
-          dn_nb = Jo[t1] * Fs[6 * N2 + t] + Jo[t2] * Fs[7 * N2 + t] + Jo[D] * Fs[3 * N2 + t];
+          dn_nb = Jo[t1] * Fs[6 * FS + t] + Jo[t2] * Fs[7 * FS + t] + Jo[D] * Fs[3 * FS + t];
       } else {
         const double jac = 2.0 / A.h[D];
         JxW = T.w[a] * T.w[b] * (0.5 * A.h[t1]) * (0.5 * A.h[t2]);
         sig = A.sigma[D];
         Jn[0] = Jn[1] = Jn[2] = 0.0;
         Jn[D] = nsgn * jac;
-        dn_own = Jn[D] * Fs[1 * N2 + t];
-        if (kind[s] == 0) dn_nb = Jn[D] * Fs[3 * N2 + t];
+        dn_own = Jn[D] * Fs[1 * FS + t];
+        if (kind[s] == 0) dn_nb = Jn[D] * Fs[3 * FS + t];
       }
       double jump, avg;
       if (kind[s] == 0) {
-        jump = u_own - Fs[2 * N2 + t];
+        jump = u_own - Fs[2 * FS + t];
         avg = 0.5 * (dn_own + dn_nb);
       } else {
         jump = 2.0 * u_own;
@@ -239,10 +249,10 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
       v1 = cg * Jn[t1];
       v2 = cg * Jn[t2];
     }
-    Bs[0 * N2 + t] = vA;
-    Bs[1 * N2 + t] = vD;
-    Bs[2 * N2 + t] = v1;
-    Bs[3 * N2 + t] = v2;
+    Bs[0 * FS + t] = vA;
+    Bs[1 * FS + t] = vD;
+    Bs[2 * FS + t] = v1;
+    Bs[3 * FS + t] = v2;
   }
   __syncthreads();
   // ---- F5: transposed t2 (columns): P = I^T (A + D^T B_t2), Q = I^T B_t1, W = I^T B_D
@@ -250,7 +260,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
     constexpr int NG = DEFORMED ? 3 : 2;
     for (int task = t; task < 2 * NG * N; task += N2) {
       const int s = task / (NG * N), g = (task / N) % NG, col = task % N;
-      double* Bs = B + s * 4 * N2;
+      double* Bs = B + s * 4 * FS;
       double in[N], out[N];
       if (g == 0) {
 #pragma unroll
@@ -258,37 +268,37 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
         if (DEFORMED) {
           double b2[N];
 #pragma unroll
-          for (int i = 0; i < N; ++i) b2[i] = Bs[3 * N2 + N * i + col];
+          for (int i = 0; i < N; ++i) b2[i] = Bs[3 * FS + N * i + col];
           mvt_add<N>(T.colloc, b2, in);
         }
       } else {
         const int f = (g == 1) ? 1 : 2;
 #pragma unroll
-        for (int i = 0; i < N; ++i) in[i] = Bs[f * N2 + N * i + col];
+        for (int i = 0; i < N; ++i) in[i] = Bs[f * FS + N * i + col];
       }
       mvt<N>(T.val, in, out);
       const int f = (g == 0) ? 0 : (g == 1 ? 1 : 2);
 #pragma unroll
-      for (int i = 0; i < N; ++i) Bs[f * N2 + N * i + col] = out[i];
+      for (int i = 0; i < N; ++i) Bs[f * FS + N * i + col] = out[i];
     }
   }
   __syncthreads();
   // ---- F6: transposed t1 (rows): V = I^T (P + D^T Q), W = I^T W
   for (int task = t; task < 2 * 2 * N; task += N2) {
     const int s = task / (2 * N), g = (task / N) % 2, row = task % N;
-    double* Bs = B + s * 4 * N2;
+    double* Bs = B + s * 4 * FS;
     double in[N], out[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) in[i] = Bs[g * N2 + N * row + i];
+    for (int i = 0; i < N; ++i) in[i] = Bs[g * FS + N * row + i];
     if (DEFORMED && g == 0) {
       double q[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) q[i] = Bs[2 * N2 + N * row + i];
+      for (int i = 0; i < N; ++i) q[i] = Bs[2 * FS + N * row + i];
       mvt_add<N>(T.colloc, q, in);
     }
     mvt<N>(T.val, in, out);
 #pragma unroll
-    for (int i = 0; i < N; ++i) Bs[g * N2 + N * row + i] = out[i];
+    for (int i = 0; i < N; ++i) Bs[g * FS + N * row + i] = out[i];
   }
   __syncthreads();
   // ---- F7: expand into the residual's d-line (a, b)
@@ -298,7 +308,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
     for (int i = 0; i < N; ++i) r[i] = R[lidx<N, D>(i, a, b)];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const double V = B[(s * 4 + 0) * N2 + t], W = B[(s * 4 + 1) * N2 + t];
+      const double V = B[(s * 4 + 0) * FS + t], W = B[(s * 4 + 1) * FS + t];
       r[s ? K : 0] += V;
 #pragma unroll
       for (int i = 0; i < N; ++i) r[i] = fma(T.dface[s][i], W, r[i]);

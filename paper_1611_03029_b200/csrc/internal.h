@@ -197,21 +197,21 @@ struct fem_ctx {
   fem::SolveGraphs sg;
   std::unique_ptr<fem::Comm> comm;      // nranks > 1
   int rank = 0, nranks = 1;
-  bool use_graphs = true;
+  bool use_graphs = true;               // PCG iteration as CUDA graphs (not with the in-process transport)
   bool overlap = true;                  // FEM_OVERLAP=0: halo exchanges serialised with the applies
   cudaStream_t comm_stream = nullptr;   // halo exchanges of distributed levels
-  cudaEvent_t ev_fork = nullptr, ev_import = nullptr, ev_export = nullptr;               // PCG iteration as CUDA graphs (not with the in-process transport)
+  cudaEvent_t ev_fork = nullptr, ev_import = nullptr, ev_export = nullptr;
   int chunk_layers = 0;                 // Cartesian CG apply: cell layers per z-chunk (FEM_CHUNK_LAYERS; 0 = one launch)
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
   bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)
-  bool g_direct = true;                // FEM_G_DIRECT=0: line kernel stages G by TMA into shared memory
-  bool y_is_zero = false;
+  bool g_direct = true;                // line kernel reads G from global (else TMA-staged; default at Q4); FEM_G_DIRECT
+  bool y_is_zero = false;              // set around launch_cg_apply: the output is known to be zero
   fem::ChebFuse fuse;                   // set around a fused Chebyshev apply (SIPG levels)
-  fem::CgFuse cgf;                      // set around a fused Chebyshev step + apply (CG levels)              // set around launch_cg_apply: the output is known to be zero
+  fem::CgFuse cgf;                      // set around a fused Chebyshev step + apply (CG levels)
   bool pdl = true;                     // FEM_PDL=0: plain launches (no programmatic dependent launch)
   int64_t fuse_max_cells = 512;        // FEM_FUSE_CELLS: CG levels up to this many cells use the fused step
-  bool fuse_cheb = true;
-  bool line_cell_fast = FEM_LINE_CELL_FAST != 0;   // Q4 line kernel: cells-fastest layout, G in kGLayoutCell8               // FEM_FUSE_CHEB=0: separate Chebyshev-step kernel on SIPG levels
+  bool fuse_cheb = true;               // FEM_FUSE_CHEB=0: separate Chebyshev-step kernels
+  bool line_cell_fast = FEM_LINE_CELL_FAST != 0;   // Q4 line kernel: cells-fastest layout, G in kGLayoutCell8
   bool dg_kron = true;                 // FEM_DG_KRON=0: quadrature cell+face kernel on Cartesian SIPG levels
   bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels
   bool dbasis = false;                 // FEM_DBASIS=1: derivative-basis line kernel (measured slower, kept for study)

@@ -205,21 +205,25 @@ __device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>&
       Gs = a.G + (active ? cell : 0) * 6 * N3;
     }
   } else if (DEFORMED) {
+    // one TMA bulk copy stages the block's G slice into shared memory (8-cell block
+    // order: the launcher guarantees the block starts at a multiple of 8 cells and the
+    // table is padded to whole blocks, so the slice is one contiguous 8-cell chunk)
     double* sG = smem + C * line_cell_stride<N>();
     const int64_t c0 = a.cell0 + (int64_t)blockIdx.x * C;
+    const bool c8 = line_cell_fast<K>() && a.glayout == kGLayoutCell8;
     if (traw == 0 && ci == 0) {
-      const int64_t nc = (a.cell1 - c0) < C ? (a.cell1 - c0) : C;
+      const int64_t nc = c8 ? C : ((a.cell1 - c0) < C ? (a.cell1 - c0) : C);
       const uint32_t bytes = (uint32_t)(nc * 6 * N3 * sizeof(double));
       mbar_init(&gbar, 1);
       mbar_arrive_expect_tx(&gbar, bytes);
       bulk_g2s(sG, a.G + c0 * 6 * N3, bytes, &gbar);
     }
     __syncthreads();       // barrier initialisation visible to all threads
-    Gs = sG + ci * 6 * N3;
+    Gs = c8 ? sG + ci : sG + ci * 6 * N3;
   }
   CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, (DEFORMED && !a.g_direct) ? &gbar : nullptr};
   if constexpr (line_cell_fast<K>()) {
-    if (DEFORMED && a.g_direct && a.glayout == kGLayoutCell8) {
+    if (DEFORMED && a.glayout == kGLayoutCell8) {
       geo.gq = kCell8;
       geo.gc = N3 * kCell8;
     }
@@ -1300,6 +1304,8 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
   const bool full = r0 == 0 && r1 == L.n_cells;
   a.cell0 = r0;
   a.cell1 = r1;
+  // TMA staging of 8-cell G blocks needs launches that start on a block boundary
+  if (a.glayout == kGLayoutCell8 && r0 % kCell8 != 0) a.g_direct = 1;
   if (r1 <= r0) return;
   const Tab<N> T = make_tab<N>(h->tab);
   const dim3 block(N * N, C);

@@ -298,10 +298,10 @@ def test_cartesian_fast_path_and_general_quadrature_path_agree(k, monkeypatch):
     assert relmax(y1, yo) <= 1e-12 and relmax(y2, yo) <= 1e-12
 
 
-@pytest.mark.parametrize("env,val", [("FEM_G_DIRECT", "0"), ("FEM_FUSE_CHEB", "0"), ("FEM_FUSE_CELLS", "100000000")])
+@pytest.mark.parametrize("env,val", [("FEM_G_DIRECT", "1"), ("FEM_FUSE_CHEB", "0"), ("FEM_FUSE_CELLS", "100000000")])
 def test_layout_and_fusion_switches_keep_parity(env, val, monkeypatch):
-    """Q4 deformed: G staged by TMA in the [cell][comp][q] order instead of the 8-cell
-    block order read directly; Chebyshev fusion off / on every level.  Same operator,
+    """Q4 deformed: G read directly from global memory instead of the default TMA-staged
+    8-cell blocks; Chebyshev fusion off / on every level.  Same operator,
     PCG iterations within +-1 of the oracle's, true residual below tolerance."""
     monkeypatch.setenv(env, val)
     k, cells = 4, (8, 8, 8)

@@ -1068,10 +1068,10 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_GENERAL_PATH")) h->general_path = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_CHUNK_LAYERS")) h->chunk_layers = std::atoi(e);
     if (const char* e = std::getenv("FEM_PLANE")) h->plane_kernel = std::atoi(e) != 0;
-    // Q4 (8-cell block G order): the block's G chunk staged by one TMA bulk copy is faster
-    // than direct loads (C2 apply 59.4 -> 57.5 us, solve 7.12 -> 6.94 ms); other degrees
-    // read G directly (measured equal)
-    h->g_direct = !(degree == 4 && h->line_cell_fast);
+    // the block's G chunk staged by one TMA bulk copy beats direct loads at Q4 (8-cell block
+    // order: C2 apply 59.4 -> 57.5 us, solve 7.12 -> 6.94 ms) and at k = 7, 8 (deformed
+    // apply at ~16M DoFs 692 -> 416 us, 595 -> 498 us); k = 3, 5, 6 are faster direct
+    h->g_direct = !((degree == 4 && h->line_cell_fast) || degree == 7 || degree == 8);
     if (const char* e = std::getenv("FEM_G_DIRECT")) h->g_direct = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_DBASIS")) h->dbasis = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_STENCIL")) h->stencil = std::atoi(e) != 0;

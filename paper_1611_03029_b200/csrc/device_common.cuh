@@ -362,6 +362,13 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// L2 prefetch of an arbitrary byte range (bulk prefetch needs 16-byte aligned start and size)
+__device__ __forceinline__ void prefetch_l2_range(const void* p, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p), b = a & ~(uintptr_t)15;
+  const size_t n = (a + bytes - b + 15) & ~(size_t)15;
+  bulk_prefetch_l2(reinterpret_cast<const void*>(b), (uint32_t)n);
+}
+
 __device__ __forceinline__ bool cg_constrained(int bcmask, int gx, int gy, int gz, int nn0, int nn1,
                                                int nn2) {
   return ((bcmask & 1) && gx == 0) || ((bcmask & 2) && gx == nn0 - 1) ||

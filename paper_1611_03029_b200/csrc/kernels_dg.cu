@@ -32,6 +32,12 @@ struct DgCPB {
 #ifndef FEM_DGQ_PAD
 #define FEM_DGQ_PAD 1
 #endif
+#ifndef FEM_DG_FACE_PREFETCH
+#define FEM_DG_FACE_PREFETCH 1
+#endif
+#ifndef FEM_DG_NB_PREFETCH
+#define FEM_DG_NB_PREFETCH 1
+#endif
 #ifndef FEM_DGQ_FPAD
 #define FEM_DGQ_FPAD 1
 #endif
@@ -339,8 +345,6 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? 
     const int64_t nc = (A.cell1 - c0) < C ? (A.cell1 - c0) : C;
     bulk_prefetch_l2(A.G + c0 * 6 * N3, (uint32_t)(nc * 6 * N3 * sizeof(double)));
   }
-  FEM_PDL_ENTRY();
-  double* sm = smem + ci * L::SIZE;
   int c[3] = {0, 0, 0};
   if (active) {
     c[0] = (int)(cell % A.n[0]);
@@ -348,6 +352,28 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? 
     c[1] = (int)(r % A.n[1]);
     c[2] = (int)(r / A.n[1]);
   }
+  if (FEM_DG_FACE_PREFETCH && DEFORMED && t == 0 && active) {
+    // the cell's y- and z-face records (static; x-faces of the block's cells are one run)
+#pragma unroll
+    for (int D = 1; D < 3; ++D)
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        prefetch_l2_range(A.faceq + face_record(A, D, c, c[D] + s) * 7 * N2, 7 * N2 * sizeof(double));
+    if (ci == 0) {
+      const int nc = (int)((A.cell1 - cell) < C ? (A.cell1 - cell) : C);
+      prefetch_l2_range(A.faceq + face_record(A, 0, c, c[0]) * 7 * N2, (size_t)(nc + 1) * 7 * N2 * sizeof(double));
+    }
+  }
+  FEM_PDL_ENTRY();
+  if (FEM_DG_NB_PREFETCH && t == 0 && active) {
+    // the y- and z-neighbour cells whose lines the face phases read (ghost layers included)
+    const int64_t sy = A.n[0], sz = (int64_t)A.n[0] * A.n[1];
+    if (c[1] > 0) prefetch_l2_range(A.x + (cell - sy) * N3, N3 * sizeof(double));
+    if (c[1] < A.n[1] - 1) prefetch_l2_range(A.x + (cell + sy) * N3, N3 * sizeof(double));
+    if (c[2] + A.cz0 > 0) prefetch_l2_range(A.x + (cell - sz) * N3, N3 * sizeof(double));
+    if (c[2] + A.cz0 < A.nzg - 1) prefetch_l2_range(A.x + (cell + sz) * N3, N3 * sizeof(double));
+  }
+  double* sm = smem + ci * L::SIZE;
   double u[N], v[N];
 #pragma unroll
   for (int l = 0; l < N; ++l) {

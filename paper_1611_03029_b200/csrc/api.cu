@@ -1073,6 +1073,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     // apply at ~16M DoFs 692 -> 416 us, 595 -> 498 us); k = 3, 5, 6 are faster direct
     h->g_direct = !((degree == 4 && h->line_cell_fast) || degree == 7 || degree == 8);
     if (const char* e = std::getenv("FEM_G_DIRECT")) h->g_direct = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_TMA_MIN_BLOCKS")) h->tma_min_blocks = std::atoll(e);
     if (const char* e = std::getenv("FEM_DBASIS")) h->dbasis = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_STENCIL")) h->stencil = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_PDL")) h->pdl = std::atoi(e) != 0;

@@ -204,6 +204,7 @@ struct fem_ctx {
   int chunk_layers = 0;                 // Cartesian CG apply: cell layers per z-chunk (FEM_CHUNK_LAYERS; 0 = one launch)
   bool general_path = false;           // FEM_GENERAL_PATH=1: quadrature kernel on Cartesian levels too
   bool plane_kernel = false;           // FEM_PLANE=1: plane kernel on deformed CG levels (K <= 4)
+  int64_t tma_min_blocks = 0;          // FEM_TMA_MIN_BLOCKS: launches this small read G directly
   bool g_direct = true;                // line kernel reads G from global (else TMA-staged; default at Q4); FEM_G_DIRECT
   bool y_is_zero = false;              // set around launch_cg_apply: the output is known to be zero
   fem::ChebFuse fuse;                   // set around a fused Chebyshev apply (SIPG levels)

@@ -1304,8 +1304,12 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
   const bool full = r0 == 0 && r1 == L.n_cells;
   a.cell0 = r0;
   a.cell1 = r1;
-  // TMA staging of 8-cell G blocks needs launches that start on a block boundary
-  if (a.glayout == kGLayoutCell8 && r0 % kCell8 != 0) a.g_direct = 1;
+  // TMA staging of 8-cell G blocks needs launches that start on a block boundary; a
+  // launch of at most FEM_TMA_MIN_BLOCKS blocks reads G directly (4 instead of 3
+  // resident blocks per SM: a level that fits one wave is latency-, not traffic-bound)
+  if (a.glayout == kGLayoutCell8 &&
+      (r0 % kCell8 != 0 || (r1 - r0 + C - 1) / C <= (int64_t)h->tma_min_blocks))
+    a.g_direct = 1;
   if (r1 <= r0) return;
   const Tab<N> T = make_tab<N>(h->tab);
   const dim3 block(N * N, C);
@@ -1372,11 +1376,11 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
       launch_pdl(h, cg_plane_kernel<K, true>, (unsigned)groups, N * kGroupCells, sm, a, T);
     }
   } else if (h->cgf.on) {
-    const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (h->g_direct ? 0 : 6 * N * N * N * C));
+    const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (a.g_direct ? 0 : 6 * N * N * N * C));
     smem_attr(reinterpret_cast<const void*>(cg_apply_fused_kernel<K>), (size_t)((int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
     launch_pdl(h, cg_apply_fused_kernel<K>, (unsigned)grid, lblock, sm, a, T, h->cgf);
   } else {
-    const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (h->g_direct ? 0 : 6 * N * N * N * C));
+    const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (a.g_direct ? 0 : 6 * N * N * N * C));
     smem_attr(reinterpret_cast<const void*>(cg_apply_kernel<K, true>), (size_t)((int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
     launch_pdl(h, cg_apply_kernel<K, true>, (unsigned)grid, lblock, sm, a, T);
   }

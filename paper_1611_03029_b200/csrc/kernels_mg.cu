@@ -38,6 +38,38 @@ __device__ __forceinline__ int64_t cg_index(int gx, int gy, int gz, int nn0, int
   return gx + (int64_t)nn0 * (gy + (int64_t)nn1 * gz);
 }
 
+// Line-thread form: in each of the three sweeps a thread owns one 1-D line of the
+// current direction and keeps it in registers (inputs read once, from global memory in
+// the first sweep of the restriction and written to global memory in the last sweep of
+// the prolongation), so shared memory only carries the two intermediate tensors.
+// (The earlier element-per-thread form staged all (2k+1)^3 / (2k+2)^3 fine values in
+// shared memory and re-read each one per output: ~7x the shared-memory traffic.)
+
+// fine-level value (r, s, t) of coarse cell (cx, cy, cz) for the restriction (0 where the
+// fine node is not owned by this coarse cell (CG) or constrained)
+template <int K, bool DG>
+__device__ __forceinline__ double transfer_fine_in(const TransferArgs& a, const double* __restrict__ bf,
+                                                   const double* __restrict__ axf, int cx, int cy, int cz,
+                                                   int r, int sidx, int tt) {
+  constexpr int N = K + 1;
+  int64_t idx;
+  if (DG) {
+    const int fx = 2 * cx + r / N, fy = 2 * cy + sidx / N, fz = 2 * cz + tt / N;
+    const int64_t fcell = fx + (int64_t)(2 * a.nc0) * (fy + (int64_t)(2 * a.nc1) * fz);
+    idx = fcell * N * N * N + r % N + N * ((sidx % N) + N * (tt % N));
+  } else {
+    // the node exists whether or not this cell owns it: load unconditionally (all loads of
+    // a line in flight together), mask afterwards
+    const bool owned = !((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
+                         (tt == 2 * K && a.czc0 + cz != a.ncz - 1));
+    const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
+    idx = cg_index(gx, gy, gz, a.nnf0, a.nnf1);
+    const double v = __ldg(bf + idx) - (axf ? __ldg(axf + idx) : 0.0);
+    return (!owned || cg_constrained(a.bcmask, gx, gy, 2 * K * a.czc0 + gz, a.nnf0, a.nnf1, a.nnf2)) ? 0.0 : v;
+  }
+  return __ldg(bf + idx) - (axf ? __ldg(axf + idx) : 0.0);
+}
+
 // xf += P xc
 template <int K, bool DG>
 __global__ void prolongate_kernel(TransferArgs a, Embed<K, DG> E, const double* __restrict__ xc,
@@ -45,81 +77,85 @@ __global__ void prolongate_kernel(TransferArgs a, Embed<K, DG> E, const double* 
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, M = Embed<K, DG>::M;
   extern __shared__ double smem[];
-  double* s_in = smem;               // N^3
-  double* s_1 = smem + N * N * N;    // M N^2
-  double* s_2 = s_1 + M * N * N;     // M^2 N
-  // E indexed by a thread-dependent row: from shared memory (a kernel-parameter
-  // (constant bank) operand with divergent addresses serialises the warp)
+  double* s_1 = smem;               // [l][j][r]  M N^2
+  double* s_2 = smem + M * N * N;   // [l][s][r]  M^2 N
   __shared__ double sE[M][N];
   for (int i = threadIdx.x; i < M * N; i += blockDim.x) sE[i / N][i % N] = E.E[i / N][i % N];
   const int64_t cell = blockIdx.x;
   const int cx = (int)(cell % a.nc0);
   const int64_t rr = cell / a.nc0;
   const int cy = (int)(rr % a.nc1), cz = (int)(rr / a.nc1);
-  for (int i = threadIdx.x; i < N * N * N; i += blockDim.x) {
-    const int i0 = i % N, i1 = (i / N) % N, i2 = i / (N * N);
-    double v;
-    if (DG) {
-      v = xc[cell * N * N * N + i];
-    } else {
-      const int gx = K * cx + i0, gy = K * cy + i1, gz = K * cz + i2;
-      v = cg_constrained(a.bcmask, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2)
-              ? 0.0
-              : xc[cg_index(gx, gy, gz, a.nnc0, a.nnc1)];
+  __syncthreads();
+  // x: coarse x-lines (j, l) -> M fine x values
+  for (int line = threadIdx.x; line < N * N; line += blockDim.x) {
+    const int j = line % N, l = line / N;
+    double in[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (DG) {
+        in[i] = __ldg(xc + cell * N * N * N + i + N * line);
+      } else {
+        const int gx = K * cx + i, gy = K * cy + j, gz = K * cz + l;
+        in[i] = cg_constrained(a.bcmask, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2)
+                    ? 0.0
+                    : __ldg(xc + cg_index(gx, gy, gz, a.nnc0, a.nnc1));
+      }
     }
-    s_in[i] = v;
-  }
-  __syncthreads();
-  for (int o = threadIdx.x; o < M * N * N; o += blockDim.x) {  // x sweep: [l][j][r]
-    const int r = o % M, jl = o / M;
-    double s = 0.0;
 #pragma unroll
-    for (int i = 0; i < N; ++i) s = fma(sE[r][i], s_in[i + N * jl], s);
-    s_1[o] = s;
-  }
-  __syncthreads();
-  for (int o = threadIdx.x; o < M * M * N; o += blockDim.x) {  // y sweep: [l][s][r]
-    const int r = o % M, sidx = (o / M) % M, l = o / (M * M);
-    double s = 0.0;
+    for (int r = 0; r < M; ++r) {
+      double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < N; ++j) s = fma(sE[sidx][j], s_1[r + M * (j + N * l)], s);
-    s_2[o] = s;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int it = 0; it < (M * M * M + kTransferThreads - 1) / kTransferThreads; ++it) {  // z sweep + write
-    const int o = threadIdx.x + it * kTransferThreads;
-    if (o >= M * M * M) break;
-    int r, sidx, tt;
-    int64_t fidx = 0;
-    if (DG) {
-      // o enumerates the fine DoFs in memory order (child cell, then its n^3 block), so
-      // a warp's read-modify-writes of xf are consecutive addresses
-      const int child = o / (N * N * N), loc = o % (N * N * N);
-      const int ca = child & 1, cb = (child >> 1) & 1, cc = child >> 2;
-      r = ca * N + loc % N;
-      sidx = cb * N + (loc / N) % N;
-      tt = cc * N + loc / (N * N);
-      const int64_t fcell = (2 * cx + ca) + (int64_t)(2 * a.nc0) * ((2 * cy + cb) + (int64_t)(2 * a.nc1) * (2 * cz + cc));
-      fidx = fcell * N * N * N + loc;
-    } else {
-      r = o % M;
-      sidx = (o / M) % M;
-      tt = o / (M * M);
+      for (int i = 0; i < N; ++i) s = fma(sE[r][i], in[i], s);
+      s_1[r + M * (j + N * l)] = s;
     }
-    double s = 0.0;
+  }
+  __syncthreads();
+  // y: lines (r, l)
+  for (int line = threadIdx.x; line < M * N; line += blockDim.x) {
+    const int r = line % M, l = line / M;
+    double in[N];
 #pragma unroll
-    for (int l = 0; l < N; ++l) s = fma(sE[tt][l], s_2[r + M * (sidx + M * l)], s);
-    if (DG) {
-      xf[fidx] += s;
-    } else {
-      // owned: local fine index < 2K unless this is the last coarse cell
-      if ((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
-          (tt == 2 * K && a.czc0 + cz != a.ncz - 1))
-        continue;
-      const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
-      if (cg_constrained(a.bcmask, gx, gy, 2 * K * a.czc0 + gz, a.nnf0, a.nnf1, a.nnf2)) continue;
-      xf[cg_index(gx, gy, gz, a.nnf0, a.nnf1)] += s;
+    for (int j = 0; j < N; ++j) in[j] = s_1[r + M * (j + N * l)];
+#pragma unroll
+    for (int sidx = 0; sidx < M; ++sidx) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(sE[sidx][j], in[j], s);
+      s_2[r + M * (sidx + M * l)] = s;
+    }
+  }
+  __syncthreads();
+  // z: lines (r, s) -> M fine values along z, added into xf (all old values loaded first)
+  for (int line = threadIdx.x; line < M * M; line += blockDim.x) {
+    const int r = line % M, sidx = line / M;
+    double in[N], old[M];
+    int64_t idx[M];
+    bool wr[M];
+#pragma unroll
+    for (int tt = 0; tt < M; ++tt) {
+      if (DG) {
+        const int fx = 2 * cx + r / N, fy = 2 * cy + sidx / N, fz = 2 * cz + tt / N;
+        const int64_t fcell = fx + (int64_t)(2 * a.nc0) * (fy + (int64_t)(2 * a.nc1) * fz);
+        idx[tt] = fcell * N * N * N + r % N + N * ((sidx % N) + N * (tt % N));
+        wr[tt] = true;
+      } else {
+        // owned: local fine index < 2K unless this is the last coarse cell
+        const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
+        idx[tt] = cg_index(gx, gy, gz, a.nnf0, a.nnf1);
+        wr[tt] = !((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
+                   (tt == 2 * K && a.czc0 + cz != a.ncz - 1)) &&
+                 !cg_constrained(a.bcmask, gx, gy, 2 * K * a.czc0 + gz, a.nnf0, a.nnf1, a.nnf2);
+      }
+      old[tt] = xf[idx[tt]];
+    }
+#pragma unroll
+    for (int l = 0; l < N; ++l) in[l] = s_2[r + M * (sidx + M * l)];
+#pragma unroll
+    for (int tt = 0; tt < M; ++tt) {
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) s = fma(sE[tt][l], in[l], s);
+      if (wr[tt]) xf[idx[tt]] = old[tt] + s;
     }
   }
 }
@@ -131,72 +167,63 @@ __global__ void restrict_kernel(TransferArgs a, Embed<K, DG> E, const double* __
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, M = Embed<K, DG>::M;
   extern __shared__ double smem[];
-  double* s_in = smem;               // M^3
-  double* s_1 = smem + M * M * M;    // N M^2
-  double* s_2 = smem;                // N^2 M (aliases s_in, dead after the x sweep)
-  __shared__ double sE[M][N];   // see prolongate_kernel
+  double* s_1 = smem;               // [t][s][i]  N M^2
+  double* s_2 = smem + N * M * M;   // [t][j][i]  N^2 M
+  __shared__ double sE[M][N];
   for (int i = threadIdx.x; i < M * N; i += blockDim.x) sE[i / N][i % N] = E.E[i / N][i % N];
   const int64_t cell = blockIdx.x;
   const int cx = (int)(cell % a.nc0);
   const int64_t rr = cell / a.nc0;
   const int cy = (int)(rr % a.nc1), cz = (int)(rr / a.nc1);
-  // CG: compile-time trip count, fully unrolled, so the loads of all trips are issued
-  // before the first one returns (restrict 29 -> 27 us on C2; DG measured slower unrolled)
+  __syncthreads();
+  // x: fine x-lines (s, t), read once from global memory into registers
+  for (int line = threadIdx.x; line < M * M; line += blockDim.x) {
+    const int sidx = line % M, tt = line / M;
+    double in[M];
 #pragma unroll
-  for (int it = 0; it < (M * M * M + kTransferThreads - 1) / kTransferThreads; ++it) {
-    const int o = threadIdx.x + it * kTransferThreads;
-    if (o >= M * M * M) break;
-    int r = o % M, sidx = (o / M) % M, tt = o / (M * M);
-    double v = 0.0;
-    if (DG) {
-      // fine DoFs read in memory order (coalesced), placed at their (r, s, t) position
-      const int child = o / (N * N * N), loc = o % (N * N * N);
-      const int ca = child & 1, cb = (child >> 1) & 1, cc = child >> 2;
-      r = ca * N + loc % N;
-      sidx = cb * N + (loc / N) % N;
-      tt = cc * N + loc / (N * N);
-      const int64_t fcell = (2 * cx + ca) + (int64_t)(2 * a.nc0) * ((2 * cy + cb) + (int64_t)(2 * a.nc1) * (2 * cz + cc));
-      const int64_t idx = fcell * N * N * N + loc;
-      v = bf[idx] - (axf ? axf[idx] : 0.0);
-    } else {
-      const bool owned = !((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
-                           (tt == 2 * K && a.czc0 + cz != a.ncz - 1));
-      const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
-      if (owned && !cg_constrained(a.bcmask, gx, gy, 2 * K * a.czc0 + gz, a.nnf0, a.nnf1, a.nnf2)) {
-        const int64_t idx = cg_index(gx, gy, gz, a.nnf0, a.nnf1);
-        v = bf[idx] - (axf ? axf[idx] : 0.0);
-      }
+    for (int r = 0; r < M; ++r) in[r] = transfer_fine_in<K, DG>(a, bf, axf, cx, cy, cz, r, sidx, tt);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int r = 0; r < M; ++r) s = fma(sE[r][i], in[r], s);
+      s_1[i + N * (sidx + M * tt)] = s;
     }
-    s_in[r + M * (sidx + M * tt)] = v;
   }
   __syncthreads();
-  for (int o = threadIdx.x; o < N * M * M; o += blockDim.x) {  // x: [t][s][i]
-    const int i = o % N, st = o / N;
-    double s = 0.0;
+  // y: lines (i, t)
+  for (int line = threadIdx.x; line < N * M; line += blockDim.x) {
+    const int i = line % N, tt = line / N;
+    double in[M];
 #pragma unroll
-    for (int r = 0; r < M; ++r) s = fma(sE[r][i], s_in[r + M * st], s);
-    s_1[o] = s;
+    for (int sidx = 0; sidx < M; ++sidx) in[sidx] = s_1[i + N * (sidx + M * tt)];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int sidx = 0; sidx < M; ++sidx) s = fma(sE[sidx][j], in[sidx], s);
+      s_2[i + N * (j + N * tt)] = s;
+    }
   }
   __syncthreads();
-  for (int o = threadIdx.x; o < N * N * M; o += blockDim.x) {  // y: [t][j][i]
-    const int i = o % N, j = (o / N) % N, tt = o / (N * N);
-    double s = 0.0;
+  // z: lines (i, j)
+  for (int line = threadIdx.x; line < N * N; line += blockDim.x) {
+    const int i = line % N, j = line / N;
+    double in[M];
 #pragma unroll
-    for (int sidx = 0; sidx < M; ++sidx) s = fma(sE[sidx][j], s_1[i + N * (sidx + M * tt)], s);
-    s_2[o] = s;
-  }
-  __syncthreads();
-  for (int o = threadIdx.x; o < N * N * N; o += blockDim.x) {  // z: [l][j][i]
-    const int i = o % N, j = (o / N) % N, l = o / (N * N);
-    double s = 0.0;
+    for (int tt = 0; tt < M; ++tt) in[tt] = s_2[i + N * (j + N * tt)];
 #pragma unroll
-    for (int tt = 0; tt < M; ++tt) s = fma(sE[tt][l], s_2[i + N * (j + N * tt)], s);
-    if (DG) {
-      xc[cell * N * N * N + o] = s;
-    } else {
-      const int gx = K * cx + i, gy = K * cy + j, gz = K * cz + l;
-      if (!cg_constrained(a.bcmask, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2))
-        atomicAdd(xc + cg_index(gx, gy, gz, a.nnc0, a.nnc1), s);
+    for (int l = 0; l < N; ++l) {
+      double s = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < M; ++tt) s = fma(sE[tt][l], in[tt], s);
+      if (DG) {
+        xc[cell * N * N * N + line + N * N * l] = s;
+      } else {
+        const int gx = K * cx + i, gy = K * cy + j, gz = K * cz + l;
+        if (!cg_constrained(a.bcmask, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2))
+          atomicAdd(xc + cg_index(gx, gy, gz, a.nnc0, a.nnc1), s);
+      }
     }
   }
 }
@@ -425,7 +452,7 @@ Embed<K, DG> make_embed(const Tables1D& t) {
 template <int K, bool DG>
 void prolongate_kd(fem_ctx* h, const Level& c, const Level& f, const double* xc, double* xf) {
   constexpr int N = K + 1, M = Embed<K, DG>::M;
-  const size_t sm = sizeof(double) * (N * N * N + M * N * N + M * M * N);
+  const size_t sm = sizeof(double) * (M * N * N + M * M * N);
   smem_attr(reinterpret_cast<const void*>(prolongate_kernel<K, DG>), (size_t)((int)sm));
   launch_pdl(h, prolongate_kernel<K, DG>, (unsigned)c.n_cells, kTransferThreads, sm, 
       transfer_args(h, c, f), make_embed<K, DG>(h->tab), xc, xf);
@@ -437,7 +464,7 @@ template <int K, bool DG>
 void restrict_kd(fem_ctx* h, const Level& c, const Level& f, const double* bf, const double* axf,
                  double* xc) {
   constexpr int N = K + 1, M = Embed<K, DG>::M;
-  const size_t sm = sizeof(double) * (M * M * M + N * M * M);
+  const size_t sm = sizeof(double) * (N * M * M + N * N * M);
   smem_attr(reinterpret_cast<const void*>(restrict_kernel<K, DG>), (size_t)((int)sm));
   launch_pdl(h, restrict_kernel<K, DG>, (unsigned)c.n_cells, kTransferThreads, sm, 
       transfer_args(h, c, f), make_embed<K, DG>(h->tab), bf, axf, xc);

@@ -94,6 +94,16 @@ __device__ __forceinline__ void dg_store(const ChebFuse& cf, const double* __res
     y[i] = v;
   }
 }
+// the same with x_i already in a register
+__device__ __forceinline__ void dg_store_x(const ChebFuse& cf, double xi, double* __restrict__ y, int64_t i,
+                                           double v) {
+  if (cf.on) {
+    const double xoi = cf.xo ? cf.xo[i] : 0.0;
+    y[i] = xi + cf.c1 * (xi - xoi) + cf.c2 * cf.dinv[i] * (cf.b[i] - v);
+  } else {
+    y[i] = v;
+  }
+}
 
 // node index in the cell of (i along D, a along t1, b along t2)
 template <int N, int D>
@@ -518,6 +528,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
   }
   const int64_t stride[3] = {1, (int64_t)A.n[0], (int64_t)A.n[0] * A.n[1]};
   const double* xc = x + (active ? cell : 0) * N3;
+  double xz[N];
   // ---- directional line operators, straight from global memory
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
@@ -535,6 +546,10 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
       xo[i] = active ? __ldg(xc + off + st * i) : 0.0;
       xl[i] = hl ? __ldg(xc - stride[d] * N3 + off + st * i) : 0.0;
       xr[i] = hr ? __ldg(xc + stride[d] * N3 + off + st * i) : 0.0;
+    }
+    if (d == 2) {   // the thread's own z-line: the entries its epilogue writes
+#pragma unroll
+      for (int i = 0; i < N; ++i) xz[i] = xo[i];
     }
     dg_line_op<N>(T, A.sc[d], A.sigma[d], flo, fhi, hl, hr, xo, xl, xr, o);
     double* F = d == 0 ? F0 : (d == 1 ? F1 : F2);
@@ -582,7 +597,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     mv<N>(T.M, a, o);
     if (active) {
 #pragma unroll
-      for (int l = 0; l < N; ++l) dg_store(A.cf, x, y, cell * N3 + t + N2 * l, fma(A.mc[2], o[l], F2[ta + B * tb + S * l]));
+      for (int l = 0; l < N; ++l) dg_store_x(A.cf, xz[l], y, cell * N3 + t + N2 * l, fma(A.mc[2], o[l], F2[ta + B * tb + S * l]));
     }
   }
 }

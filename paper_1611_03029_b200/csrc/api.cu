@@ -434,7 +434,7 @@ void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double
   const bool fused = !is_cg(h) && h->fuse_cheb && L.cartesian && h->dg_kron;
   auto step = [&](const double* xc, const double* xold, double* xnew, double c1, double c2) {
     if (fused) {
-      h->fuse = ChebFuse{xold, b, L.dinv, c1, c2, 1};
+      h->fuse = ChebFuse{xold, b, L.dinv, L.dinv_cls, c1, c2, 1};
       apply_level(h, L, xc, xnew, false);
       h->fuse = ChebFuse{};
     } else {
@@ -867,6 +867,22 @@ void level_geometry_and_diagonal(fem_ctx* h, Level& L) {
   } else {
     launch_dg_diagonal(h, L);
     launch_dinv(h, L);
+    if (L.cartesian && !L.dist && h->dinv_classes) {
+      // class c_d = 0 (first cell along d), 1 (interior), 2 (last); representative cells
+      const int64_t n3 = (int64_t)(h->k + 1) * (h->k + 1) * (h->k + 1);
+      L.dinv_cls = dalloc(27 * n3);
+      for (int c2 = 0; c2 < 3; ++c2)
+        for (int c1 = 0; c1 < 3; ++c1)
+          for (int c0 = 0; c0 < 3; ++c0) {
+            const int cc[3] = {c0, c1, c2};
+            int rep[3];
+            for (int d = 0; d < 3; ++d)
+              rep[d] = cc[d] == 0 ? 0 : (cc[d] == 2 ? L.n[d] - 1 : (L.n[d] >= 3 ? 1 : 0));
+            const int64_t cell = rep[0] + (int64_t)L.n[0] * (rep[1] + (int64_t)L.n[1] * rep[2]);
+            FEM_CUDA_TRY(cudaMemcpyAsync(L.dinv_cls + (c0 + 3 * c1 + 9 * c2) * n3, L.dinv + cell * n3,
+                                         sizeof(double) * n3, cudaMemcpyDeviceToDevice, h->stream));
+          }
+    }
   }
 }
 
@@ -960,7 +976,7 @@ void destroy(fem_ctx* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (auto& L : h->levels) {
-    for (double** p : {&L.G, &L.face, &L.halo, &L.gb, &L.gx}) dfree(*p);
+    for (double** p : {&L.G, &L.face, &L.halo, &L.gb, &L.gx, &L.dinv_cls}) dfree(*p);
     for (double** p : {&L.diag, &L.dinv, &L.b, &L.x, &L.x2, &L.x3, &L.t, &L.b2, &L.pcg_r, &L.pcg_p,
                        &L.pcg_q, &L.pcg_z, &L.tf[0], &L.tf[1], &L.tf[2]})
       vfree(L, *p);
@@ -1079,6 +1095,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_PDL")) h->pdl = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_DG_KRON")) h->dg_kron = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_FUSE_CHEB")) h->fuse_cheb = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_DINV_CLASSES")) h->dinv_classes = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_FUSE_CELLS")) h->fuse_max_cells = std::atoll(e);
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)

@@ -115,6 +115,9 @@ struct Level {
   // CG single-rank deformed levels: three A x buffers rotated by the fused Chebyshev
   // sequences (each fused kernel clears the buffer the next one accumulates into)
   double* tf[3] = {nullptr, nullptr, nullptr};
+  // Cartesian SIPG single-rank levels: D^-1 depends on the cell only through which of its
+  // faces lie on the boundary (3 classes per direction): 27 x n^3 values copied from dinv
+  double* dinv_cls = nullptr;
   // PCG vectors (finest level, allocated on first cg_solve)
   double *pcg_r = nullptr, *pcg_p = nullptr, *pcg_q = nullptr, *pcg_z = nullptr;
   double* halo = nullptr;        // CG dist: receive buffer of one node plane (compress-add)
@@ -130,6 +133,7 @@ struct ChebFuse {
   const double* xo = nullptr;    // x_old (nullptr: first step)
   const double* b = nullptr;
   const double* dinv = nullptr;
+  const double* dinv_cls = nullptr;   // Cartesian SIPG: D^-1 per cell class (27 x n^3), or nullptr
   double c1 = 0.0, c2 = 0.0;
   int on = 0;
 };
@@ -211,6 +215,7 @@ struct fem_ctx {
   fem::CgFuse cgf;                      // set around a fused Chebyshev step + apply (CG levels)
   bool pdl = true;                     // FEM_PDL=0: plain launches (no programmatic dependent launch)
   int64_t fuse_max_cells = 512;        // FEM_FUSE_CELLS: CG levels up to this many cells use the fused step
+  bool dinv_classes = true;            // FEM_DINV_CLASSES=0: fused SIPG epilogue reads the full D^-1
   bool fuse_cheb = true;               // FEM_FUSE_CHEB=0: separate Chebyshev-step kernels
   bool line_cell_fast = FEM_LINE_CELL_FAST != 0;   // Q4 line kernel: cells-fastest layout, G in kGLayoutCell8
   bool dg_kron = true;                 // FEM_DG_KRON=0: quadrature cell+face kernel on Cartesian SIPG levels

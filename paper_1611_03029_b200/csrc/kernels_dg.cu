@@ -94,12 +94,14 @@ __device__ __forceinline__ void dg_store(const ChebFuse& cf, const double* __res
     y[i] = v;
   }
 }
-// the same with x_i already in a register
+// the same with x_i already in a register and D^-1 from dinv[i] or from the cell-class
+// table (dcls: the class's n^3 block, loc: local node index)
 __device__ __forceinline__ void dg_store_x(const ChebFuse& cf, double xi, double* __restrict__ y, int64_t i,
-                                           double v) {
+                                           double v, const double* dcls, int loc) {
   if (cf.on) {
     const double xoi = cf.xo ? cf.xo[i] : 0.0;
-    y[i] = xi + cf.c1 * (xi - xoi) + cf.c2 * cf.dinv[i] * (cf.b[i] - v);
+    const double di = dcls ? dcls[loc] : cf.dinv[i];
+    y[i] = xi + cf.c1 * (xi - xoi) + cf.c2 * di * (cf.b[i] - v);
   } else {
     y[i] = v;
   }
@@ -596,8 +598,17 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
     for (int l = 0; l < N; ++l) a[l] = F0[ta + B * tb + S * l] + F1[ta + B * tb + S * l];
     mv<N>(T.M, a, o);
     if (active) {
+      const double* dcls = nullptr;
+      if (A.cf.on && A.cf.dinv_cls) {
+        int cl[3];
 #pragma unroll
-      for (int l = 0; l < N; ++l) dg_store_x(A.cf, xz[l], y, cell * N3 + t + N2 * l, fma(A.mc[2], o[l], F2[ta + B * tb + S * l]));
+        for (int d = 0; d < 3; ++d) cl[d] = c[d] == 0 ? 0 : (c[d] == A.n[d] - 1 ? 2 : 1);
+        dcls = A.cf.dinv_cls + (cl[0] + 3 * cl[1] + 9 * cl[2]) * N3;
+      }
+#pragma unroll
+      for (int l = 0; l < N; ++l)
+        dg_store_x(A.cf, xz[l], y, cell * N3 + t + N2 * l, fma(A.mc[2], o[l], F2[ta + B * tb + S * l]), dcls,
+                   t + N2 * l);
     }
   }
 }

@@ -91,6 +91,10 @@ def test_stencil_kernel_matches_oracle(k, cells, bc, monkeypatch):
     (2, (3, 4, 5), 0.05, MIXED),
     (3, (4, 3, 2), 0.05, (DIRICHLET,) * 6),
     (4, (6, 4, 3), 0.05, MIXED),                 # several cell batches + ragged tail
+    (4, (5, 3, 3), 0.05, MIXED),                 # 45 cells: last 8-cell G block partial (TMA copy)
+    (4, (3, 1, 1), 0.05, (DIRICHLET,) * 6),      # a single partial block
+    (7, (3, 1, 1), 0.05, (DIRICHLET,) * 6),      # TMA-staged G, ragged 2-cell block
+    (8, (1, 3, 1), 0.05, MIXED),
     (4, (7, 5, 3), 0.0, (DIRICHLET,) * 6),
     (5, (3, 2, 3), 0.05, MIXED),
     (6, (2, 3, 2), 0.05, (DIRICHLET,) * 6),

@@ -28,6 +28,19 @@ struct DgCPB {
   static constexpr int N = K + 1;
   static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? 8 : (N * N <= 49) ? 4 : 2;
 };
+#ifndef FEM_DG_MINB
+#define FEM_DG_MINB 2
+#endif
+// cells per block and minimum resident blocks of the SIPG quadrature kernel (K2/K3):
+// at k = 5, 6 fewer cells per block with a register cap measured faster (deformed apply
+// at ~16M DoFs: k = 5 4 cells / 2 blocks 1143 us -> 2 / 3 1008 us, k = 6 4 / 2 1378 us ->
+// 1 / 6 1142 us; C5 7.76 -> ~6.6 ms): more, smaller blocks keep more warps resident
+template <int K>
+struct DgQCPB {
+  static constexpr int value = K == 5 ? 2 : (K == 6 ? 1 : DgCPB<K>::value);
+};
+template <int K>
+__host__ __device__ constexpr int dgq_minb() { return K == 5 ? 3 : (K == 6 ? 6 : (K >= 7 ? FEM_DG_MINB : 1)); }
 
 #ifndef FEM_DGQ_PAD
 #define FEM_DGQ_PAD 1
@@ -337,14 +350,11 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
   __syncthreads();
 }
 
-#ifndef FEM_DG_MINB
-#define FEM_DG_MINB 2
-#endif
 template <int K, bool DEFORMED>
-__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value, K >= 5 ? FEM_DG_MINB : 1)   // measured: 1 beats none at k <= 4
+__global__ void __launch_bounds__((K + 1) * (K + 1) * DgQCPB<K>::value, dgq_minb<K>())   // measured: 1 beats none at k <= 4
     dg_apply_kernel(DgArgs A, Tab<K + 1> T) {
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
-  constexpr int C = DgCPB<K>::value;
+  constexpr int C = DgQCPB<K>::value;
   using L = DgSmem<N>;
   extern __shared__ double smem[];
   const int t = threadIdx.x, ci = threadIdx.y;
@@ -885,7 +895,7 @@ MapArgs dg_map_args(const fem_ctx* h, const Level& L) {
 
 template <int K, bool DEF>
 void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0, int64_t r1) {
-  constexpr int N = K + 1, C = DgCPB<K>::value;
+  constexpr int N = K + 1, C = DgQCPB<K>::value;
   const size_t sm = sizeof(double) * DgSmem<N>::SIZE * C;
   smem_attr(reinterpret_cast<const void*>(dg_apply_kernel<K, DEF>), (size_t)((int)sm));
   const unsigned grid = (unsigned)((r1 - r0 + C - 1) / C);

@@ -28,19 +28,31 @@ struct DgCPB {
   static constexpr int N = K + 1;
   static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? 8 : (N * N <= 49) ? 4 : 2;
 };
+#ifndef FEM_DGQ_C78
+#define FEM_DGQ_C78 1
+#endif
+#ifndef FEM_DGQ_C4
+#define FEM_DGQ_C4 2
+#endif
+#ifndef FEM_DGQ_MINB4
+#define FEM_DGQ_MINB4 6
+#endif
 #ifndef FEM_DG_MINB
-#define FEM_DG_MINB 2
+#define FEM_DG_MINB 4
 #endif
 // cells per block and minimum resident blocks of the SIPG quadrature kernel (K2/K3):
-// at k = 5, 6 fewer cells per block with a register cap measured faster (deformed apply
-// at ~16M DoFs: k = 5 4 cells / 2 blocks 1143 us -> 2 / 3 1008 us, k = 6 4 / 2 1378 us ->
-// 1 / 6 1142 us; C5 7.76 -> ~6.6 ms): more, smaller blocks keep more warps resident
+// fewer cells per block with a register cap measured faster (deformed apply at ~16M
+// DoFs, cells/block and blocks/SM: k = 4 8/1 1141 us -> 2/6 1029 us, k = 5 4/2 1143 ->
+// 2/3 1008, k = 6 4/2 1378 -> 1/6 1142 (C5 7.76 -> 6.51 ms), k = 7 2/2 1076 -> 1/4 1028,
+// k = 8 2/2 1400 -> 1/4 1324): more, smaller blocks keep more warps resident
 template <int K>
 struct DgQCPB {
-  static constexpr int value = K == 5 ? 2 : (K == 6 ? 1 : DgCPB<K>::value);
+  static constexpr int value = K == 5 ? 2 : (K == 6 ? 1 : (K >= 7 ? FEM_DGQ_C78 : (K == 4 ? FEM_DGQ_C4 : DgCPB<K>::value)));
 };
 template <int K>
-__host__ __device__ constexpr int dgq_minb() { return K == 5 ? 3 : (K == 6 ? 6 : (K >= 7 ? FEM_DG_MINB : 1)); }
+__host__ __device__ constexpr int dgq_minb() {
+  return K == 5 ? 3 : (K == 6 ? 6 : (K >= 7 ? FEM_DG_MINB : (K == 4 ? FEM_DGQ_MINB4 : 1)));
+}
 
 #ifndef FEM_DGQ_PAD
 #define FEM_DGQ_PAD 1

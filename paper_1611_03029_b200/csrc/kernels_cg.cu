@@ -23,9 +23,15 @@ template <int K>
 #ifndef FEM_CPB4
 #define FEM_CPB4 8
 #endif
+#ifndef FEM_CPB56
+#define FEM_CPB56 4
+#endif
+#ifndef FEM_CPB78
+#define FEM_CPB78 2
+#endif
 struct CPB {  // cells per block: about 128-200 threads per block
   static constexpr int N = K + 1;
-  static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? FEM_CPB4 : (N * N <= 49) ? 4 : 2;
+  static constexpr int value = (N * N <= 4) ? 32 : (N * N <= 9) ? 16 : (N * N <= 25) ? FEM_CPB4 : (N * N <= 49) ? FEM_CPB56 : FEM_CPB78;
 };
 
 struct OpArgs {
@@ -83,6 +89,9 @@ struct LineLayout {
 };
 template <int N>
 __host__ __device__ constexpr int line_cell_stride() { return LineLayout<N - 1>::CS; }
+// start of the TMA-staged G chunk behind the C cells' buffers: 16-byte aligned
+template <int N, int C>
+__host__ __device__ constexpr int line_g_offset() { return (C * line_cell_stride<N>() + 1) / 2 * 2; }
 // per-cell stride of the derivative-basis kernel (K1d, (line, cell) layout)
 template <int N>
 __host__ __device__ constexpr int dline_cell_stride() { return 3 * N * N * N + (N == 5 ? 2 : 0); }
@@ -102,8 +111,21 @@ template <int K>
 #ifndef FEM_LINE_MINB4
 #define FEM_LINE_MINB4 0
 #endif
+#ifndef FEM_LINE_MINB5
+#define FEM_LINE_MINB5 0
+#endif
+#ifndef FEM_LINE_MINB6
+#define FEM_LINE_MINB6 4
+#endif
+#ifndef FEM_LINE_MINB7
+#define FEM_LINE_MINB7 0
+#endif
+#ifndef FEM_LINE_MINB8
+#define FEM_LINE_MINB8 2
+#endif
 __host__ __device__ constexpr int line_minb() {
-  return K == 6 ? 4 : (K == 8 ? 2 : (K == 4 && line_cell_fast<K>() ? FEM_LINE_MINB4 : 0));
+  return K == 5 ? FEM_LINE_MINB5 : K == 6 ? FEM_LINE_MINB6 : K == 7 ? FEM_LINE_MINB7 : K == 8 ? FEM_LINE_MINB8
+       : (K == 4 && line_cell_fast<K>() ? FEM_LINE_MINB4 : 0);
 }
 
 // FUSED (a.cf): the input vector is the NEXT Chebyshev iterate, built on the fly at the
@@ -208,7 +230,7 @@ __device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>&
     // one TMA bulk copy stages the block's G slice into shared memory (8-cell block
     // order: the launcher guarantees the block starts at a multiple of 8 cells and the
     // table is padded to whole blocks, so the slice is one contiguous 8-cell chunk)
-    double* sG = smem + C * line_cell_stride<N>();
+    double* sG = smem + line_g_offset<N, C>();
     const int64_t c0 = a.cell0 + (int64_t)blockIdx.x * C;
     const bool c8 = line_cell_fast<K>() && a.glayout == kGLayoutCell8;
     if (traw == 0 && ci == 0) {
@@ -1376,12 +1398,12 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
       launch_pdl(h, cg_plane_kernel<K, true>, (unsigned)groups, N * kGroupCells, sm, a, T);
     }
   } else if (h->cgf.on) {
-    const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (a.g_direct ? 0 : 6 * N * N * N * C));
-    smem_attr(reinterpret_cast<const void*>(cg_apply_fused_kernel<K>), (size_t)((int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
+    const size_t sm = sizeof(double) * (line_g_offset<N, C>() + (a.g_direct ? 0 : 6 * N * N * N * C));
+    smem_attr(reinterpret_cast<const void*>(cg_apply_fused_kernel<K>), (size_t)((int)(sizeof(double) * (line_g_offset<N, C>() + 6 * N * N * N * C))));
     launch_pdl(h, cg_apply_fused_kernel<K>, (unsigned)grid, lblock, sm, a, T, h->cgf);
   } else {
-    const size_t sm = sizeof(double) * (C * line_cell_stride<N>() + (a.g_direct ? 0 : 6 * N * N * N * C));
-    smem_attr(reinterpret_cast<const void*>(cg_apply_kernel<K, true>), (size_t)((int)(sizeof(double) * (C * line_cell_stride<N>() + 6 * N * N * N * C))));
+    const size_t sm = sizeof(double) * (line_g_offset<N, C>() + (a.g_direct ? 0 : 6 * N * N * N * C));
+    smem_attr(reinterpret_cast<const void*>(cg_apply_kernel<K, true>), (size_t)((int)(sizeof(double) * (line_g_offset<N, C>() + 6 * N * N * N * C))));
     launch_pdl(h, cg_apply_kernel<K, true>, (unsigned)grid, lblock, sm, a, T);
   }
   count_launch();

@@ -527,12 +527,24 @@ struct DgCartLayout {
   static constexpr int CS = pad ? CSp[K] : 3 * N * N * N + 1;
 };
 
+#ifndef FEM_DGC_C4
+#define FEM_DGC_C4 8
+#endif
+#ifndef FEM_DGC_MINB4
+#define FEM_DGC_MINB4 0
+#endif
+// cells per block of the Cartesian SIPG kernel (K2c)
 template <int K>
-__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCPB<K>::value)
+struct DgCartCPB {
+  static constexpr int value = K == 4 ? FEM_DGC_C4 : DgCPB<K>::value;
+};
+
+template <int K>
+__global__ void __launch_bounds__((K + 1) * (K + 1) * DgCartCPB<K>::value, K == 4 ? FEM_DGC_MINB4 : 0)
     dg_cart_kernel(const double* __restrict__ x, double* __restrict__ y, DgKron A, DgKronTab<K + 1> T) {
   FEM_PDL_ENTRY();
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
-  constexpr int C = DgCPB<K>::value;
+  constexpr int C = DgCartCPB<K>::value;
   extern __shared__ double smem[];
   const int t = threadIdx.x, ci = threadIdx.y;
   const int64_t cell = A.cell0 + (int64_t)blockIdx.x * C + ci;
@@ -921,7 +933,7 @@ void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y, int64_t
 
 template <int K>
 void dg_cart_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0, int64_t r1) {
-  constexpr int N = K + 1, C = DgCPB<K>::value;
+  constexpr int N = K + 1, C = DgCartCPB<K>::value;
   DgKron A;
   for (int d = 0; d < 3; ++d) {
     A.n[d] = L.n[d];

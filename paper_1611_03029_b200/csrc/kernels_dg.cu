@@ -31,6 +31,18 @@ struct DgCPB {
 #ifndef FEM_DGQ_C78
 #define FEM_DGQ_C78 1
 #endif
+#ifndef FEM_DGQ_C3
+#define FEM_DGQ_C3 8
+#endif
+#ifndef FEM_DGQ_MINB3
+#define FEM_DGQ_MINB3 1
+#endif
+#ifndef FEM_DGQ_C2
+#define FEM_DGQ_C2 16
+#endif
+#ifndef FEM_DGQ_MINB2
+#define FEM_DGQ_MINB2 1
+#endif
 #ifndef FEM_DGQ_C4
 #define FEM_DGQ_C4 2
 #endif
@@ -47,11 +59,11 @@ struct DgCPB {
 // k = 8 2/2 1400 -> 1/4 1324): more, smaller blocks keep more warps resident
 template <int K>
 struct DgQCPB {
-  static constexpr int value = K == 5 ? 2 : (K == 6 ? 1 : (K >= 7 ? FEM_DGQ_C78 : (K == 4 ? FEM_DGQ_C4 : DgCPB<K>::value)));
+  static constexpr int value = K == 5 ? 2 : (K == 6 ? 1 : (K >= 7 ? FEM_DGQ_C78 : (K == 4 ? FEM_DGQ_C4 : (K == 3 ? FEM_DGQ_C3 : (K == 2 ? FEM_DGQ_C2 : DgCPB<K>::value)))));
 };
 template <int K>
 __host__ __device__ constexpr int dgq_minb() {
-  return K == 5 ? 3 : (K == 6 ? 6 : (K >= 7 ? FEM_DG_MINB : (K == 4 ? FEM_DGQ_MINB4 : 1)));
+  return K == 5 ? 3 : (K == 6 ? 6 : (K >= 7 ? FEM_DG_MINB : (K == 4 ? FEM_DGQ_MINB4 : (K == 3 ? FEM_DGQ_MINB3 : (K == 2 ? FEM_DGQ_MINB2 : 1)))));
 }
 
 #ifndef FEM_DGQ_PAD

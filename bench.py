@@ -1,21 +1,27 @@
-"""Benchmark: GMG-preconditioned CG solve of BASELINE.json configs[1] (C2) on B200.
+"""Benchmark: BASELINE.json's headline (configs[3] = C4, the largest single-GPU config).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C4]
 
-One step = one complete solve (operator applies, Chebyshev
-smoothing, transfers, coarse solve, PCG vector work) from x = 0 to ||r|| <= 1e-10 ||b||,
-with the right-hand side already resident in HBM.  value = DoFs solved per second
-over all ranks; ms_per_step = time to solution.  The dominant kernel (the
-finest-level operator apply) is timed live with CUDA events on the library's
-stream (fem_options.profile) and reported against the HBM roofline.
+One step = one complete GMG-CG solve (operator applies with the
+fused Chebyshev smoother, transfers, coarse solve, PCG vector work) of C4 -- CG Q4 on a
+Cartesian 128^3 mesh (135,005,697 DoFs), b = A x_7 with the Dirichlet rows zeroed
+(reading R15) -- from x = 0 to ||r|| <= 1e-10 ||b||, with b resident in HBM.
+value = DoFs solved per second over all ranks; ms_per_step = time to solution.  The
+dominant kernel (the finest-level operator apply, kernels_stencil.cu K1t) is timed live
+with CUDA events on the library's stream (fem_options.profile) on the PCG apply q = A p
+of every iteration and reported against the measured HBM peak (algorithmic 16 B/DoF)
+and, as an extra key, against the measured FP64 peak (algorithmic 7 banded sweeps,
+2 (k+2) flop per DoF each).  `apply` adds the standalone y = A x_7 throughput
+(actual and equivalent DoF/s).
 
---impl reference times the CPU oracle (oracle/, the "reference" of this tier) on
-the host cores: warm-up runs one full oracle solve (iteration count), each timed
-step is one oracle PCG iteration; value = n_dofs / (t_iteration * iterations).
-Multi-GPU (torchrun, one process per GPU): the mesh is split into z-slabs, one
-C2-sized slab (32x32x32 cells) per GPU on the box [0,1]^2 x [0,N] (weak scaling);
-libfem exchanges ghost planes with NCCL send/recv and all-reduces the PCG dot
-products; value = global DoFs / max-over-ranks time.
+--impl reference times the CPU oracle (oracle/, the reference of this tier) on the
+host cores; each step is one complete oracle GMG-CG solve of the same recipe on a
+bounded sample mesh (C4 recipe at 16^3 cells, 274,625 DoFs; setup untimed), value =
+sample DoFs / step time.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run (one
+process per GPU, 127.0.0.1 rendezvous).  Multi-GPU = strong scaling of the same C4
+mesh split into z-slabs: NCCL halo exchange + all-reduced dots;
+value = global DoFs / max-over-ranks time to solution.
 """
 from __future__ import annotations
 
@@ -36,7 +42,9 @@ sys.path.insert(0, ROOT)
 import fem_inputs  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
-METRIC = "GMG-CG solve throughput (DoFs solved per second; ms_per_step = time to solution)"
+METRIC = "FP64 operator-apply DoFs/s and GMG-CG time-to-solution; % of HBM roofline"   # BASELINE.json
+FP64_PEAK_TFLOPS = 36.794   # profiles/fp64_peak.json (tools/fp64_peak.cu, measured on this pool's B200)
+REF_SAMPLE_CELLS = (16, 16, 16)
 
 
 def parse():
@@ -45,7 +53,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rtol", type=float, default=1e-10)
     return ap.parse_args()
@@ -175,16 +183,27 @@ def oracle_solver(w):
     return mg, b
 
 
+def oracle_sample(w):
+    """The bounded CPU sample of a workload: the same recipe on REF_SAMPLE_CELLS when the
+    full mesh is larger (the oracle's cost per DoF does not depend on the mesh size)."""
+    if int(np.prod(w.cells)) <= int(np.prod(REF_SAMPLE_CELLS)):
+        return w, "the full workload"
+    ws = fem_inputs.scaled(w, REF_SAMPLE_CELLS)
+    return ws, (f"the {w.name} recipe (same method, degree, deformation, boundary conditions, "
+                f"right-hand side) on {REF_SAMPLE_CELLS[0]}x{REF_SAMPLE_CELLS[1]}x{REF_SAMPLE_CELLS[2]} cells")
+
+
 def cpu_baseline(w, rtol):
-    """The oracle as it stands: one full PCG solve of the same workload (setup excluded)."""
-    mg, b = oracle_solver(w)
+    """The oracle as it stands: one full PCG solve of the bounded sample (setup excluded)."""
+    ws, what = oracle_sample(w)
+    mg, b = oracle_solver(ws)
     t0 = time.perf_counter()
     _, its, rr = mg.pcg(b, tol=rtol)
     t = time.perf_counter() - t0
     n = mg.fine.n_dofs
     return {"value": n / t, "unit": "DoF/s", "cores": cpu_threads(), "kind": "oracle",
-            "sample": f"one full oracle PCG solve of {w.name} ({its} iterations, relres {rr:.2e}), "
-                      f"setup (geometry, lambda estimates, coarse Cholesky) excluded",
+            "sample": f"one full oracle GMG-PCG solve of {what} ({n} DoFs, {its} iterations, "
+                      f"relres {rr:.2e}); setup (geometry, lambda estimates, coarse Cholesky) excluded",
             "seconds": t}
 
 
@@ -193,45 +212,30 @@ def run_reference(args, w):
     rank, world, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    from oracle import multigrid as omg
-    mg, b = oracle_solver(w)
+    ws, what = oracle_sample(w)
+    mg, b = oracle_solver(ws)
     n = mg.fine.n_dofs
-    A = mg.fine.apply
-    # warm-up: one complete solve gives the oracle's own iteration count
-    _, its, rr = mg.pcg(b, tol=args.rtol)
-    for _ in range(max(args.warmup - 1, 0)):
-        mg.vcycle(b)
-    # timed steps: one PCG iteration each (apply, two dots, updates, V-cycle)
-    x = np.zeros_like(b)
-    r = b.copy()
-    z = mg.vcycle(r)
-    p = z.copy()
-    rz = r @ z
+    its = 0
+    for _ in range(args.warmup):
+        _, its, rr = mg.pcg(b, tol=args.rtol)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        q = A(p)
-        alpha = rz / (p @ q)
-        x += alpha * p
-        r -= alpha * q
-        _ = np.linalg.norm(r)
-        z = mg.vcycle(r)
-        rz_new = r @ z
-        p = z + (rz_new / rz) * p
-        rz = rz_new
+        _, its, rr = mg.pcg(b, tol=args.rtol)
         times.append(time.perf_counter() - t0)
-    t_iter = sum(times) / len(times)
-    t_solve = t_iter * its
-    value = n / t_solve
+        assert rr <= args.rtol
+    t_step = sum(times) / len(times)
+    value = n / t_step
     line = {
         "impl": "reference", "metric": METRIC,
         "value": value, "unit": "DoF/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_solve * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": {"workload": workload_desc(w), "n_dofs": n,
-                                                         "rtol": args.rtol, "iterations": its},
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(w), "rtol": args.rtol, "sample_cells": list(ws.cells),
+                   "sample_n_dofs": n, "iterations": its},
         "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cpu_threads(), "kind": "oracle",
-                         "sample": f"each step = one oracle PCG iteration on the full {w.name} problem; "
-                                   f"value = n_dofs / (mean iteration time x {its} iterations)"},
+                         "sample": f"each step = one full oracle GMG-PCG solve of {what} ({n} DoFs, "
+                                   f"{its} iterations, setup untimed); value = sample DoFs / mean step time"},
         "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -253,6 +257,15 @@ def constrained_mask(w, n, cells, first=0):
     return m
 
 
+def apply_flops_per_dof(w):
+    """Algorithmic FP64 flops of one apply per DoF: Cartesian CG = 7 banded 1-D sweeps of the
+    assembled Kronecker sum (App. B), k + 2 FMA per node each (vertex rows 2k+1 entries,
+    interior rows k+1); other paths: SURVEY §8d estimates are not used for the roofline."""
+    if w.method == fem_inputs.CG and not w.deform_eps:
+        return 2 * 7 * (w.degree + 2)
+    return None
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args, w):
     import torch
@@ -266,24 +279,24 @@ def run_ours(args, w):
     stream = torch.cuda.current_stream()
     cells, hi, mp = w.cells, w.hi, {}
     if world > 1:
-        # weak scaling: one C2-sized z-slab per GPU, the box stretched to [0,1]^2 x [0,N]
-        # so cells stay cubic; NCCL halo exchange + all-reduced dots
+        # strong scaling: the same mesh in z-slabs, NCCL halo exchange + all-reduced dots
         import torch.distributed as dist
-        cells = (w.cells[0], w.cells[1], w.cells[2] * world)
-        hi = (w.hi[0], w.hi[1], w.hi[2] * world)
         obj = [fem.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         mp = dict(rank=rank, nranks=world, nccl_id=obj[0])
+    t_setup = time.perf_counter()
     F = fem.Fem(cells, w.degree, w.method, deform_eps=w.deform_eps, bc=w.bc, hi=hi,
                 penalty_factor=w.penalty_factor, stream=stream, profile=True, **mp)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
     n = F.n_local
     b = torch.zeros(n, dtype=torch.float64, device="cuda")
+    xs = None
     if w.rhs == "manufactured":
         F.fem_rhs(b)
     else:
         xs = torch.from_numpy(fem_inputs.uniform_pm1(w.seed, n, F.first_global)).cuda()
         F.fem_apply(xs, b)
-        del xs
         b[constrained_mask(w, n, cells, F.first_global)] = 0.0     # reading R15: b = A x_seed with Dirichlet rows zeroed
     x = torch.zeros_like(b)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > L2
@@ -292,6 +305,14 @@ def run_ours(args, w):
         if world > 1:
             import torch.distributed as dist
             dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        tt = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return tt.item()
 
     clocks = ClockSampler(local)
     its = 0
@@ -318,14 +339,32 @@ def run_ours(args, w):
     clk = clocks.stop()
     launches = fem.kernel_launches() - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t_ms = sum(step_ms)
+    t_ms = max_over_ranks(sum(step_ms))
     apply_ms, apply_launches = F.fem_profile_read(reset=True)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = tt.item()
     value = F.n_global * args.steps / (t_ms * 1e-3)
+    hist = F.cg_history()
+    err_x7 = None
+    if xs is not None:   # R15 pin: the solve returns x_7 on the free DoFs
+        fm = ~constrained_mask(w, n, cells, F.first_global)
+        err_x7 = ((x - xs)[fm].norm() / xs[fm].norm()).item()
+
+    # standalone apply y = A x (the north_star's apply DoF/s), inputs resident, > L2
+    xa = xs if xs is not None else b
+    ya = torch.empty_like(b)
+    F.fem_apply(xa, ya)
+    F.fem_profile_read(reset=True)
+    sa, ea = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    barrier()
+    torch.cuda.synchronize()
+    sa.record(stream)
+    for _ in range(reps):
+        F.fem_apply(xa, ya)
+    ea.record(stream)
+    torch.cuda.synchronize()
+    apply_s = max_over_ranks(sa.elapsed_time(ea) * 1e-3 / reps)
+    F.fem_profile_read(reset=True)
+    del ya
 
     # end to end through the C ABI with host buffers (copies inside the timed region)
     bh = b.cpu().pin_memory()
@@ -337,51 +376,65 @@ def run_ours(args, w):
         flush.fill_(float(i))
         xh.zero_()
         torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         F.cg_solve(bh, xh, rtol=args.rtol)
         e2e_t.append(time.perf_counter() - t0)
-    e2e_s = sum(e2e_t) / len(e2e_t)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = tt.item()
+    e2e_s = max_over_ranks(sum(e2e_t) / len(e2e_t))
     e2e_value = F.n_global / e2e_s
 
     hbm, hbm_src = peaks()
     bytes_per_launch = algorithmic_apply_bytes(w, n)
     avg_apply_s = apply_ms * 1e-3 / max(apply_launches, 1)
     achieved = bytes_per_launch / avg_apply_s / 1e9
+    fpd = apply_flops_per_dof(w)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             entry = json.load(f).get(w.name)
         traffic = entry["bytes_per_launch"] if entry else None
+    n_cells = int(np.prod(w.cells))
+    kern = ("cg_stencil2_kernel<4,0> (K1t, atomic-free assembled Kronecker stencil)"
+            if w.method == fem_inputs.CG and not w.deform_eps else
+            "cg_apply_kernel (K1)" if w.method == fem_inputs.CG else "dg kernels (K2/K3)")
     line = {
         "metric": METRIC,
         "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(w), "n_dofs": n, "rtol": args.rtol, "iterations": its,
-                   "l2": "flushed between steps (256 MiB write, outside the per-step events)",
-                   "n_dofs_global": F.n_global, "cells": list(cells), "box_hi": list(hi),
+        "config": {"workload": workload_desc(w), "n_dofs_global": F.n_global, "n_dofs_local": n,
+                   "rtol": args.rtol, "iterations": its, "cells": list(cells),
+                   "l2": "flushed between steps (256 MiB write, outside the per-step events); vectors 1.08 GB each > L2",
                    "parallelism": "single GPU" if world == 1 else
-                   f"{world} z-slabs (NCCL halo exchange + all-reduce), one C2-sized slab per GPU",
+                   f"{world} z-slabs of the same mesh (NCCL halo exchange + all-reduce), strong scaling",
+                   "setup_s": round(t_setup, 3),
+                   "residual_history": [float("%.4e" % h) for h in hist],
+                   "err_vs_x7": err_x7,
                    "step_ms": [round(s, 4) for s in step_ms]},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": "finest-level operator apply (cg_apply_kernel for CG Q4 deformed); timed on the PCG apply q = A p of every iteration",
+                     "kernel": f"finest-level operator apply, {kern}; timed on the PCG apply q = A p of every iteration",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_us": avg_apply_s * 1e6, "launches": apply_launches,
                      "peak_source": hbm_src},
-        "apply": {"dofs_per_s": n / avg_apply_s,
-                  "equivalent_dofs_per_s": int(np.prod(w.cells)) * w.degree ** 3 / avg_apply_s},
+        "apply": {"us": apply_s * 1e6, "dofs_per_s": F.n_global / apply_s,
+                  "equivalent_dofs_per_s": n_cells * w.degree ** 3 / apply_s,
+                  "hbm_frac": algorithmic_apply_bytes(w, F.n_global) / apply_s / 1e9 / hbm},
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 16 * n,
                 "d2h_bytes_per_step": 8 * n},
         "gpu_launches": launches,
     }
+    if fpd:
+        fl = fpd * n
+        line["roofline"]["fp64"] = {"algorithmic_flops_per_launch": fl,
+                                    "achieved_tflops": fl / avg_apply_s / 1e12,
+                                    "peak_tflops": FP64_PEAK_TFLOPS,
+                                    "frac": fl / avg_apply_s / 1e12 / FP64_PEAK_TFLOPS,
+                                    "peak_source": "profiles/fp64_peak.json (measured DFMA chains)"}
+        line["apply"]["fp64_frac"] = fpd * F.n_global / apply_s / 1e12 / FP64_PEAK_TFLOPS
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(w, args.rtol)
         line["cpu_baseline"].pop("seconds", None)
@@ -393,9 +446,23 @@ def run_ours(args, w):
         dist.destroy_process_group()
 
 
+def respawn_under_torchrun(args):
+    """--gpus N > 1 outside torchrun: one process per GPU via torch.distributed.run."""
+    import random
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(random.randint(20000, 40000)),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
     w = fem_inputs.CONFIGS[args.config]
+    _, world, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        respawn_under_torchrun(args)
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, w)
     else:

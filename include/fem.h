@@ -205,6 +205,13 @@ FEM_API int mg_vcycle(fem_handle h, const double* r, int64_t nr, double* z, int6
 FEM_API int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, double rtol,
              int32_t maxit, int32_t* iters, double* relres);
 
+/* Residual history of the last cg_solve on this handle: rel[i] = ||r_i|| / ||b|| for
+ * i = 0 .. iterations (r_0 = b - A x_0; r_i the recursively updated residual after the
+ * i-th x update, the quantity of the stopping test).  Copies at most cap
+ * entries; *n (may be NULL) receives the full length (0 before any solve).  Host
+ * memory.  Errors: FEM_E_ARG (rel NULL with cap > 0). */
+FEM_API int cg_history(fem_handle h, double* rel, int32_t cap, int32_t* n);
+
 /* Load vector of the manufactured solution u = prod sin(pi t_d), f = -Laplace u
  * ((k+1)^3 Gauss points, CG Dirichlet rows 0); SURVEY §8c O8. */
 FEM_API int fem_rhs(fem_handle h, double* b, int64_t nb);

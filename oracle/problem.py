@@ -53,7 +53,8 @@ def rhs(mesh: Mesh, method: int, chunk: int = 4096):
         be = fq @ quad.val                                    # [C, n^3]
         if method == CG:
             dm = mesh.cg_dofmap(cells)
-            b += np.bincount(dm.ravel(), weights=be.ravel(), minlength=len(b))
+            lo, hi = int(dm.min()), int(dm.max()) + 1
+            b[lo:hi] += np.bincount(dm.ravel() - lo, weights=be.ravel(), minlength=hi - lo)
         else:
             b[c0 * m:(c0 + len(cells)) * m] = be.ravel()
     if method == CG:

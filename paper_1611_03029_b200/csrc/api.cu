@@ -72,9 +72,12 @@ void dfree(double*& p) {
 }
 
 // level vectors: owned block plus ghosts, pointer at the owned block (internal.h)
+// (cudaMemset runs on the legacy default stream, which is not ordered with a
+// non-blocking user stream: wait for it before any kernel on h->stream can touch p)
 double* valloc(const Level& L) {
   double* p = dalloc(L.n_store);
   FEM_CUDA_TRY(cudaMemset(p, 0, sizeof(double) * L.n_store));
+  FEM_CUDA_TRY(cudaDeviceSynchronize());
   return p + L.own_off;
 }
 
@@ -266,6 +269,13 @@ void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool se
     return;
   }
   halo_import(h, L, const_cast<double*>(x));
+  if (use_stencil2(h, L)) {   // writes every output once, constrained rows included
+    if (y == L.t) L.t_zero = false;
+    prof_begin(h, finest);
+    launch_cg_stencil_apply(h, L, x, y, set_constrained);
+    prof_end(h, finest);
+    return;
+  }
   if (is_cg(h)) {
     // the Cartesian fast path zeroes y itself, chunk by chunk (kernels_cg.cu)
     const bool tiled = L.cartesian && !h->general_path;
@@ -432,8 +442,11 @@ void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double
   // (Cartesian Kronecker kernel only: on the deformed quadrature kernel, which is not
   // memory bound, the four extra epilogue streams cost more than the saved pass, C5 +0.6%)
   const bool fused = !is_cg(h) && h->fuse_cheb && L.cartesian && h->dg_kron;
+  const bool st2 = h->fuse_cheb && use_stencil2(h, L);
   auto step = [&](const double* xc, const double* xold, double* xnew, double c1, double c2) {
-    if (fused) {
+    if (st2) {   // Chebyshev step in the stencil's epilogue: no A x vector at all
+      launch_cg_stencil_cheb(h, L, xc, xold, b, xnew, c1, c2);
+    } else if (fused) {
       h->fuse = ChebFuse{xold, b, L.dinv, L.dinv_cls, c1, c2, 1};
       apply_level(h, L, xc, xnew, false);
       h->fuse = ChebFuse{};
@@ -647,6 +660,9 @@ void setup_coarse(fem_ctx* h) {
   FEM_CUDA_TRY(cudaMalloc(&h->coarse_pos, sizeof(int) * std::max<int64_t>(n, 1)));
   FEM_CUDA_TRY(cudaMemcpy(h->coarse_pos, pos.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
   FEM_CUDA_TRY(cudaMemcpy(h->coarse_inv, inv.data(), sizeof(double) * nf * nf, cudaMemcpyHostToDevice));
+  // pageable H2D copies may return before the DMA lands, and they are not ordered with
+  // a non-blocking h->stream: complete them before coarse_solve_kernel can read them
+  FEM_CUDA_TRY(cudaDeviceSynchronize());
 }
 
 // ---------------------------------------------------------------- CUDA graphs
@@ -845,7 +861,10 @@ void level_geometry_and_diagonal(fem_ctx* h, Level& L) {
     const int64_t cells = plane ? (L.n_cells + kGroupCells - 1) / kGroupCells * kGroupCells
                           : c8 ? (L.n_cells + kCell8 - 1) / kCell8 * kCell8 : L.n_cells;
     L.G = dalloc(cells * 6 * N * N * N);
-    if (plane || c8) FEM_CUDA_TRY(cudaMemset(L.G, 0, sizeof(double) * cells * 6 * N * N * N));
+    if (plane || c8) {
+      FEM_CUDA_TRY(cudaMemset(L.G, 0, sizeof(double) * cells * 6 * N * N * N));
+      FEM_CUDA_TRY(cudaDeviceSynchronize());   // legacy-stream memset vs launch_geometry on h->stream
+    }
     const unsigned long long init = std::numeric_limits<unsigned long long>::max();
     FEM_CUDA_TRY(cudaMemcpyAsync(h->geom_err, &init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
     launch_geometry(h, L);
@@ -1097,11 +1116,15 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_FUSE_CHEB")) h->fuse_cheb = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_DINV_CLASSES")) h->dinv_classes = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_FUSE_CELLS")) h->fuse_max_cells = std::atoll(e);
+    if (const char* e = std::getenv("FEM_STENCIL2")) h->stencil2 = std::atoi(e) != 0;
+    if (const char* e = std::getenv("FEM_ST_MIN_CELLS")) h->stencil2_min_cells = std::atoll(e);
+    if (const char* e = std::getenv("FEM_ST_EZ")) h->stencil_ez = std::atoi(e);
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)
     FEM_CUDA_TRY(cudaMemset(h->red, 0, sizeof(double) * (16 * kRedBlocks + 16)));
     h->scal = dalloc(16);
     FEM_CUDA_TRY(cudaMemset(h->scal, 0, sizeof(double) * 16));
+    FEM_CUDA_TRY(cudaDeviceSynchronize());   // legacy-stream memsets vs kernels on h->stream
     FEM_CUDA_TRY(cudaMallocHost(&h->hscal, sizeof(double) * 16));
     FEM_CUDA_TRY(cudaMalloc(&h->geom_err, sizeof(unsigned long long)));
     build_levels(h);
@@ -1262,8 +1285,10 @@ int fem_level_geometry(fem_handle h, int32_t level, double* G, int64_t nG) {
             out[(c * 6 + comp) * nq + q] = raw[src];
           }
       if (is_device_ptr(G))
+      {
         FEM_CUDA_TRY(cudaMemcpy(G, out.data(), sizeof(double) * nG, cudaMemcpyHostToDevice));
-      else
+        FEM_CUDA_TRY(cudaDeviceSynchronize());
+      } else
         std::memcpy(G, out.data(), sizeof(double) * nG);
       return;
     }
@@ -1278,8 +1303,10 @@ int fem_level_geometry(fem_handle h, int32_t level, double* G, int64_t nG) {
         hostG[c * 6 * nq + 5 * nq + q] = L.cart[2] * w;
       }
     if (is_device_ptr(G))
+    {
       FEM_CUDA_TRY(cudaMemcpy(G, hostG.data(), sizeof(double) * nG, cudaMemcpyHostToDevice));
-    else
+      FEM_CUDA_TRY(cudaDeviceSynchronize());
+    } else
       std::memcpy(G, hostG.data(), sizeof(double) * nG);
   });
 }
@@ -1382,6 +1409,7 @@ int fem_rhs(fem_handle h, double* b, int64_t nb) {
     bool st;
     double* db = out_vec(h, b, nb, 0, false, &st);
     launch_zero(h, L.t - L.own_off, L.n_store);
+    L.t_zero = false;   // L.t now holds the load vector, not the cleared A x buffer
     launch_rhs(h, L, L.t);
     halo_export_add(h, L, L.t);
     launch_copy(h, db, L.t, L.n_dofs);
@@ -1424,6 +1452,7 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     const double bnorm = std::sqrt(h->hscal[6]);
     double rnorm = std::sqrt(h->hscal[2]);
     int it = 0;
+    h->hist.assign(1, bnorm > 0 ? rnorm / bnorm : rnorm);
     if (!std::isfinite(rnorm)) throw Error{FEM_E_BREAKDOWN, "non-finite initial residual"};
     // one PCG iteration in two parts
     auto body_pre = [&] {
@@ -1472,6 +1501,7 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
         ++it;
         const double pq = h->hscal[1];
         rnorm = std::sqrt(h->hscal[2]);
+        h->hist.push_back(bnorm > 0 ? rnorm / bnorm : rnorm);
         if (!(pq > 0) || !std::isfinite(rnorm))
           throw Error{FEM_E_BREAKDOWN, "PCG breakdown at iteration " + std::to_string(it) +
                                            " (p^T A p = " + std::to_string(pq) + ")"};
@@ -1485,6 +1515,16 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
   });
   return rc != FEM_OK ? rc : result;
+}
+
+int cg_history(fem_handle h, double* rel, int32_t cap, int32_t* n) {
+  return guarded([&] {
+    check_handle(h);
+    if (!rel && cap > 0) throw Error{FEM_E_ARG, "null history buffer"};
+    const int32_t m = (int32_t)h->hist.size();
+    for (int32_t i = 0; i < std::min(m, cap); ++i) rel[i] = h->hist[i];
+    if (n) *n = m;
+  });
 }
 
 int fem_sync(fem_handle h) {

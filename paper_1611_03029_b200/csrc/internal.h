@@ -199,6 +199,7 @@ struct fem_ctx {
   fem::Profile prof;
   cudaStream_t cap_stream = nullptr;   // non-blocking stream used only for graph capture
   fem::SolveGraphs sg;
+  std::vector<double> hist;             // ||r_i|| / ||b|| of the last cg_solve, i = 0 .. iterations
   std::unique_ptr<fem::Comm> comm;      // nranks > 1
   int rank = 0, nranks = 1;
   bool use_graphs = true;               // PCG iteration as CUDA graphs (not with the in-process transport)
@@ -219,7 +220,10 @@ struct fem_ctx {
   bool fuse_cheb = true;               // FEM_FUSE_CHEB=0: separate Chebyshev-step kernels
   bool line_cell_fast = FEM_LINE_CELL_FAST != 0;   // Q4 line kernel: cells-fastest layout, G in kGLayoutCell8
   bool dg_kron = true;                 // FEM_DG_KRON=0: quadrature cell+face kernel on Cartesian SIPG levels
-  bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels
+  bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels (K1s, study)
+  bool stencil2 = true;                // FEM_STENCIL2=0: warp-specialised assembled stencil (K1t) off
+  int64_t stencil2_min_cells = 4096;   // FEM_ST_MIN_CELLS: K1t on single-rank Cartesian CG levels with >= this many cells
+  int stencil_ez = 0;                  // FEM_ST_EZ: K1t z-element layers per block (0: 32)
   bool dbasis = false;                 // FEM_DBASIS=1: derivative-basis line kernel (measured slower, kept for study)
 };
 
@@ -289,5 +293,14 @@ void halo_import(fem_ctx* h, const Level& L, double* v);      // ghosts <- neigh
 void halo_export_add(fem_ctx* h, const Level& L, double* v);  // CG: ghost plane added into the owner
 void allreduce(fem_ctx* h, double* p, int64_t n);             // sum over ranks (device buffer)
 void launch_add(fem_ctx* h, double* y, const double* x, int64_t n);  // y += x
+
+// Cartesian CG single-rank levels, k = 2..4: atomic-free assembled stencil (kernels_stencil.cu)
+inline bool use_stencil2(const fem_ctx* h, const Level& L) {
+  return h->method == FEM_CG && h->stencil2 && L.cartesian && !L.dist && !h->general_path &&
+         h->k >= 2 && h->k <= 4 && L.n_cells >= h->stencil2_min_cells;
+}
+void launch_cg_stencil_apply(fem_ctx* h, const Level& L, const double* x, double* y, bool setc);
+void launch_cg_stencil_cheb(fem_ctx* h, const Level& L, const double* x, const double* xo, const double* b,
+                            double* xnew, double c1, double c2);
 
 }  // namespace fem

@@ -1329,8 +1329,10 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
   // TMA staging of 8-cell G blocks needs launches that start on a block boundary; a
   // launch of at most FEM_TMA_MIN_BLOCKS blocks reads G directly (4 instead of 3
   // resident blocks per SM: a level that fits one wave is latency-, not traffic-bound)
+  // (the staged copy is one 8-cell chunk per block: any other cells-per-block count
+  // (FEM_CPB4) must read G directly)
   if (a.glayout == kGLayoutCell8 &&
-      (r0 % kCell8 != 0 || (r1 - r0 + C - 1) / C <= (int64_t)h->tma_min_blocks))
+      (C != kCell8 || r0 % kCell8 != 0 || (r1 - r0 + C - 1) / C <= (int64_t)h->tma_min_blocks))
     a.g_direct = 1;
   if (r1 <= r0) return;
   const Tab<N> T = make_tab<N>(h->tab);

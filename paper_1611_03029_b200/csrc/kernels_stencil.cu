@@ -1,0 +1,487 @@
+// Cartesian CG levels: the operator as an atomic-free ASSEMBLED Kronecker stencil with
+// warp-specialised x / (y, z) stages (K1t; the C4 kernel).
+//
+// On a Cartesian level every cell has the same element matrix, the Kronecker sum
+//     K^e = c0 S(x)M(x)M + c1 M(x)S(x)M + c2 M(x)M(x)S,  c_d = det J (2/h_d)^2
+// (exact, since the (k+1)-point Gauss rule integrates the Q_k stiffness
+// and mass exactly on affine cells), so the ASSEMBLED operator is the same
+// Kronecker sum of the assembled 1-D matrices M1, S1 (the element set of a tensor grid
+// is the product of the 1-D element sets):
+//     y = M1_z Q + S1^z_z P,   P = M1_y A,   Q = M1_y B + S1^y_y A,
+//     A = M1_x x~,  B = S1^x_x x~,            S^d = c_d S,
+// x~ = x with the Dirichlet entries read as 0 (reading R5).  The 1-D assembled rows
+// are banded: node K e + r (r = 1..K-1) couples to element e's K+1 nodes, the vertex
+// K e to the 2K+1 nodes of elements e-1 and e ("slot" form; the vertex row of an
+// interior vertex uses the pre-summed coefficients M[K][j] | M[K][K]+M[0][0] | M[0][j]).
+// 7 banded sweeps, ~46 DFMA per node at k = 4 (the cell-wise form needs 7 (k+1)^4 per
+// cell = 68 per node, plus atomics that read y back: 1.47x the algorithmic DRAM bytes).
+//
+// Block = a tile of SX x SY element slots in (x, y) (output nodes [X0, X0 + K SX) x
+// [Y0, Y0 + K SY), plus the far vertex column / row on the last tile) and EZ element
+// layers in z, marching through z plane by plane:
+//   * X warps (NXW): cp.async the x~ plane (tile + K-node halo, zero-filled outside the
+//     domain and on constrained nodes) NB-1 planes ahead into shared memory, then the
+//     x-stage A, B for all rows of the tile and its y-halo into a double-buffered A/B
+//     plane;
+//   * Y/Z warps (one thread per output column and y slot): the y-stage P, Q of the
+//     thread's K rows from the A/B plane, then the z-direction element by element in
+//     registers: plane r' of z-element e adds M[r][r'] Q + S^z[r][r'] P to the K+1
+//     accumulators of the element's planes; the vertex plane carries to the next element.
+//     Every output node is written exactly once (no atomics, no zero fill): x is read
+//     once from DRAM (the halos mostly from L2), y written once -- the algorithmic
+//     16 B/DoF.
+// Producer/consumer hand-off through named barriers (FULL / EMPTY per A/B buffer), so
+// the x-stage of plane p+1 overlaps the y/z stages of plane p on other warps.
+// A z-chunk of EZ layers recomputes one halo layer below it (the bottom vertex plane's
+// contribution from the element underneath); no output is written twice.
+//
+// Epilogues (template MODE): 0 = y = A x (constrained rows 0; y_c = x_c, when asked for, by
+// the boundary-only launch_set_constrained kernel, so the epilogue never reads x);
+// 1 = fused Chebyshev step (reading R8's three-term form):
+//     x_new = x + c1 (x - x_old) + c2 D^-1 (b - A x)   (D^-1 = 0 on constrained rows).
+#include <algorithm>
+
+#include "device_common.cuh"
+
+namespace fem {
+
+template <int K>
+struct StCfg {
+  static constexpr int N = K + 1;
+  static constexpr int SX = 32 / K;               // x slots per tile (<= 32 output columns)
+  static constexpr int SY = 8;                    // y slots per tile = warps per block
+  static constexpr int TX = K * SX, TY = K * SY;  // output columns / rows of a tile
+  static constexpr int LC = TX + K + 1;           // loaded columns [X0 - K, X0 + TX]
+  static constexpr int LR = TY + K + 1;           // loaded rows (and A/B rows) [Y0 - K, Y0 + TY]
+  static constexpr int LP = LC | 1;               // odd row strides: conflict-free column walks
+  static constexpr int ABP = TX | 1;
+  static constexpr int THREADS = 32 * SY;         // thread = (output column, y slot)
+  static constexpr int NB = 4;                    // x~ planes in flight
+  static constexpr int NLD = (LR * LC + THREADS - 1) / THREADS;
+  static constexpr int SMEM = NB * LR * LP + 2 * 2 * LR * ABP + 8;   // doubles
+  // two blocks per SM: 16 warps, 4 per SM sub-partition (16K registers each)
+  static constexpr int MAXREG = 128;
+};
+
+// Compile-time reference tables (GLL Lagrange basis, (k+1)-point Gauss rule; the same
+// definitions as build_tables() in tables.cu, evaluated by the compiler): folded into
+// the DFMAs as constant-bank / uniform-register operands, so no vector register holds a
+// coefficient (with the 127 doubles passed as kernel parameters ptxas copied them into
+// vector registers and spilled).
+constexpr double ct_cos(double x) {   // |x| <= pi
+  double s = 0.0, t = 1.0;
+  for (int k = 0; k < 40; ++k) {
+    s += t;
+    t *= -x * x / ((2.0 * k + 1.0) * (2.0 * k + 2.0));
+  }
+  return s;
+}
+constexpr void ct_legendre(int n, double x, double& p, double& dp) {
+  double p0 = 1.0, p1 = x;
+  for (int k = 2; k <= n; ++k) {
+    const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+    p0 = p1;
+    p1 = p2;
+  }
+  p = n == 0 ? 1.0 : p1;
+  dp = n == 0 ? 0.0 : n * (x * p1 - p0) / (x * x - 1.0);
+}
+template <int K>
+struct RefTab {
+  static constexpr int N = K + 1;
+  double gll[N] = {}, qp[N] = {}, qw[N] = {};
+  double M[N][N] = {}, S[N][N] = {};      // M_ij = sum_q w_q phi_i phi_j, S_ij = sum_q w_q phi_i' phi_j'
+  double Mv[2 * N - 1] = {}, Sv[2 * N - 1] = {};   // interior-vertex rows: elements e-1 and e pre-summed
+  constexpr RefTab() {
+    constexpr double pi = 3.14159265358979323846;
+    for (int i = 0; i < N; ++i) {   // Gauss-Legendre, Newton from the Chebyshev-type guess
+      double x = -ct_cos(pi * (i + 0.75) / (N + 0.5)), p = 0.0, dp = 0.0;
+      for (int it = 0; it < 60; ++it) {
+        ct_legendre(N, x, p, dp);
+        x -= p / dp;
+      }
+      ct_legendre(N, x, p, dp);
+      qp[i] = x;
+      qw[i] = 2.0 / ((1.0 - x * x) * dp * dp);
+    }
+    gll[0] = -1.0;
+    gll[K] = 1.0;
+    for (int i = 1; i < K; ++i) {   // roots of P_K': Newton with P_K'' from the Legendre equation
+      double x = -ct_cos(pi * i / K), p = 0.0, dp = 0.0;
+      for (int it = 0; it < 60; ++it) {
+        ct_legendre(K, x, p, dp);
+        x -= dp * (1.0 - x * x) / (2.0 * x * dp - K * (K + 1.0) * p);
+      }
+      gll[i] = x;
+    }
+    double phi[N][N] = {}, dphi[N][N] = {};
+    for (int q = 0; q < N; ++q)
+      for (int i = 0; i < N; ++i) {
+        double v = 1.0, d = 0.0;
+        for (int j = 0; j < N; ++j) {
+          if (j == i) continue;
+          double t = 1.0;
+          for (int m = 0; m < N; ++m)
+            if (m != i && m != j) t *= (qp[q] - gll[m]) / (gll[i] - gll[m]);
+          d += t / (gll[i] - gll[j]);
+          v *= (qp[q] - gll[j]) / (gll[i] - gll[j]);
+        }
+        phi[q][i] = v;
+        dphi[q][i] = d;
+      }
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j < N; ++j) {
+        double m = 0.0, s = 0.0;
+        for (int q = 0; q < N; ++q) {
+          m += qw[q] * phi[q][i] * phi[q][j];
+          s += qw[q] * dphi[q][i] * dphi[q][j];
+        }
+        M[i][j] = m;
+        S[i][j] = s;
+      }
+    for (int j = 0; j <= 2 * K; ++j) {
+      Mv[j] = (j <= K ? M[K][j] : 0.0) + (j >= K ? M[0][j - K] : 0.0);
+      Sv[j] = (j <= K ? S[K][j] : 0.0) + (j >= K ? S[0][j - K] : 0.0);
+    }
+  }
+};
+template <int K>
+__device__ constexpr RefTab<K> kRef{};
+
+struct StArgs {
+  const double* __restrict__ x;
+  double* __restrict__ y;          // MODE 0: A x;  MODE 1: x_new
+  const double* __restrict__ xo;   // MODE 1: x_old (nullptr: none)
+  const double* __restrict__ b;    // MODE 1
+  const double* __restrict__ dinv; // MODE 1
+  double c1, c2;                   // MODE 1
+  double c0, cy, cz;               // Cartesian metric det J (2/h_d)^2 of x, y, z
+  int nx, ny, nz;                  // cells
+  int NX, NY, NZ;                  // nodes
+  int bcmask;
+  int ez_per_block;
+};
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void st_cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void st_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int W>
+__device__ __forceinline__ void st_cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(W) : "memory"); }
+
+enum { kBarX = 1, kBarFull = 2, kBarEmpty = 4 };
+
+// banded 1-D row of slot node r from 2K+1 consecutive values v (v[0] = node K(e-1)):
+// r = 0 the vertex (elements e-1: left, e: right), r >= 1 element e only.  STIFF selects
+// the reference stiffness S instead of the mass M.
+template <int K, bool STIFF>
+__device__ __forceinline__ double band_row(const double* v, int r, bool both, bool left) {
+  constexpr const RefTab<K>& R = kRef<K>;
+  double s = 0.0;
+  if (r == 0) {
+    if (both) {   // two half-length chains (DFMA latency), one extra add
+      double s2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) s = fma(STIFF ? R.Sv[j] : R.Mv[j], v[j], s);
+#pragma unroll
+      for (int j = K; j <= 2 * K; ++j) s2 = fma(STIFF ? R.Sv[j] : R.Mv[j], v[j], s2);
+      s += s2;
+    } else if (left) {
+#pragma unroll
+      for (int j = 0; j <= K; ++j) s = fma(STIFF ? R.S[K][j] : R.M[K][j], v[j], s);
+    } else {
+#pragma unroll
+      for (int j = 0; j <= K; ++j) s = fma(STIFF ? R.S[0][j] : R.M[0][j], v[K + j], s);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j <= K; ++j) s = fma(STIFF ? R.S[r][j] : R.M[r][j], v[K + j], s);
+  }
+  return s;
+}
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXREG)
+    cg_stencil2_kernel(StArgs a) {
+  FEM_PDL_ENTRY();
+  using C = StCfg<K>;
+  constexpr int N = K + 1, SX = C::SX, LR = C::LR, LC = C::LC, LP = C::LP, ABP = C::ABP, NB = C::NB;
+  extern __shared__ double smem[];
+  double* Xt = smem;                           // [NB][LR][LP]
+  double* AB = smem + NB * LR * LP;            // [2 buffers][A, B][LR][ABP]
+  const int tid = threadIdx.x;
+  const int e0 = blockIdx.x * SX, f0 = blockIdx.y * C::SY;
+  const int X0 = K * e0, Y0 = K * f0;
+  const int ez0 = blockIdx.z * a.ez_per_block;
+  const int ez1 = min(ez0 + a.ez_per_block, a.nz);
+  const int ezs = max(ez0 - 1, 0);             // first element layer processed (halo layer)
+  const int NP = (ez1 - ezs) * K + 1;          // planes K ezs .. K ez1
+  const int pz0 = K * ezs;
+  const int64_t NXY = (int64_t)a.NX * a.NY;
+  const int bm = a.bcmask;
+  // this thread's output column and y slot
+  const int c = tid & 31, s = tid >> 5;
+  const int gx = X0 + c;
+  const int f = f0 + s;
+  const int64_t obase = gx + (int64_t)a.NX * (Y0 + K * s);   // output (gx, Y0 + K s, 0)
+  const bool colin = c < C::TX && gx < a.NX;
+  const bool xm = ((bm & 1) && gx == 0) || ((bm & 2) && gx == a.NX - 1);
+
+  auto epilogue = [&](int64_t idx, double v, bool m) {
+    if constexpr (MODE == 0) {   // constrained rows: 0 here, x_c by launch_set_constrained
+      a.y[idx] = m ? 0.0 : v;
+    } else {   // D^-1 = 0 on constrained rows
+      const double xv = a.x[idx];
+      const double xov = a.xo ? a.xo[idx] : 0.0;
+      a.y[idx] = fma(a.c2 * a.dinv[idx], a.b[idx] - v, fma(a.c1, xv - xov, xv));
+    }
+  };
+  // tiles holding only the far boundary column / row of a Dirichlet side: every output
+  // is a constrained row
+  if ((X0 == a.NX - 1 && (bm & 2)) || (Y0 == a.NY - 1 && (bm & 8))) {
+    const int q1 = K * ez1 + (ez1 == a.nz ? 1 : 0);
+    if (!colin) return;
+    for (int pz = K * ez0; pz < q1; ++pz)
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const int gy = Y0 + K * s + r;
+        if (gy < a.NY) epilogue(obase + (int64_t)a.NX * r + NXY * pz, 0.0, true);
+      }
+    return;
+  }
+
+  // ---- loads: the same (row, column) slots of the tile in every plane
+  int ld_off[C::NLD];
+  uint32_t ld_ok = 0;
+#pragma unroll
+  for (int j = 0; j < C::NLD; ++j) {
+    const int idx = tid + j * C::THREADS;
+    const int r = idx / LC, cc = idx % LC;
+    const int lx = X0 - K + cc, ly = Y0 - K + r;
+    const bool in = idx < LR * LC && lx >= 0 && lx < a.NX && ly >= 0 && ly < a.NY;
+    const bool m = ((bm & 1) && lx == 0) || ((bm & 2) && lx == a.NX - 1) || ((bm & 4) && ly == 0) ||
+                   ((bm & 8) && ly == a.NY - 1);
+    ld_off[j] = in ? lx + a.NX * ly : 0;
+    if (in && !m) ld_ok |= 1u << j;
+  }
+  auto load_plane = [&](int i) {   // plane index i (global plane pz0 + i) into buffer i % NB
+    if (i < NP) {
+      const int gz = pz0 + i;
+      const bool zm = ((bm & 16) && gz == 0) || ((bm & 32) && gz == a.NZ - 1);
+      const double* src = a.x + (int64_t)gz * NXY;
+      double* dst = Xt + (i % NB) * LR * LP;
+#pragma unroll
+      for (int j = 0; j < C::NLD; ++j) {
+        const int idx = tid + j * C::THREADS;
+        if (idx < LR * LC) {
+          const int r = idx / LC, cc = idx % LC;
+          st_cp_async8(dst + r * LP + cc, src + ld_off[j], !zm && ((ld_ok >> j) & 1u));
+        }
+      }
+    }
+    st_cp_commit();
+  };
+
+  // ---- x-stage of plane i: A = M_x x~, B = S_x x~ at every tile column, all LR rows.
+  // Item = (row, slot): 2K+1 loaded values -> K outputs per field.  Slot e's vertex row
+  // uses the pre-summed coefficients; on a domain boundary (e = 0 or e = nx) the missing
+  // element's inputs are zero-filled and the vertex value is halved (M[K][K] = M[0][0],
+  // S[K][K] = S[0][0]), so the same row gives the one-element sum without a branch.
+  const int nsl = min(SX, a.nx - e0 + 1);
+  const int nitems = LR * nsl;
+  auto x_stage = [&](int i) {
+    const double* xb = Xt + (i % NB) * LR * LP;
+    double* Ab = AB + (i & 1) * 2 * LR * ABP;
+    double* Bb = Ab + LR * ABP;
+    for (int it = tid; it < nitems; it += C::THREADS) {
+      const int row = it % LR, sl = it / LR;
+      const int e = e0 + sl;
+      const double* v = xb + row * LP + sl * K;   // loaded column of node K (e-1)
+      double w[2 * K + 1];
+#pragma unroll
+      for (int j = 0; j <= 2 * K; ++j) w[j] = v[j];
+      const double hv = (e == 0 || e == a.nx) ? 0.5 : 1.0;
+      const double wk = w[K];
+      w[K] = hv * wk;
+      double* ao = Ab + row * ABP + sl * K;
+      double* bo = Bb + row * ABP + sl * K;
+      ao[0] = band_row<K, false>(w, 0, true, false);
+      bo[0] = band_row<K, true>(w, 0, true, false);
+      w[K] = wk;
+#pragma unroll
+      for (int r = 1; r < K; ++r) {
+        ao[r] = band_row<K, false>(w, r, true, false);
+        bo[r] = band_row<K, true>(w, r, true, false);
+      }
+    }
+  };
+
+  // ---- y/z stages (thread = column c, y slot s, rows K s + r)
+  const double hy = (f == 0 || f == a.ny) ? 0.5 : 1.0;
+  double out[K][N];
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+#pragma unroll
+    for (int q = 0; q < N; ++q) out[r][q] = 0.0;
+  auto plane_pq = [&](int i, double (&P)[K], double (&Q)[K]) {
+    const double* Ab = AB + (i & 1) * 2 * LR * ABP + (K * s) * ABP + c;
+    const double* Bb = Ab + LR * ABP;
+    double av[2 * K + 1], bv[2 * K + 1];
+#pragma unroll
+    for (int j = 0; j <= 2 * K; ++j) {
+      av[j] = Ab[j * ABP];
+      bv[j] = Bb[j * ABP];
+    }
+    // P = c_z M_y A, Q = c_x M_y B + c_y S_y A (vertex row: halved centre on the boundary)
+    {
+      const double ak = av[K], bk = bv[K];
+      av[K] = hy * ak;
+      bv[K] = hy * bk;
+      P[0] = a.cz * band_row<K, false>(av, 0, true, false);
+      Q[0] = fma(a.cy, band_row<K, true>(av, 0, true, false), a.c0 * band_row<K, false>(bv, 0, true, false));
+      av[K] = ak;
+      bv[K] = bk;
+    }
+#pragma unroll
+    for (int r = 1; r < K; ++r) {
+      P[r] = a.cz * band_row<K, false>(av, r, true, false);
+      Q[r] = fma(a.cy, band_row<K, true>(av, r, true, false), a.c0 * band_row<K, false>(bv, r, true, false));
+    }
+  };
+  auto accumulate = [&](int rp, const double (&P)[K], const double (&Q)[K]) {
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        out[r][q] = fma(kRef<K>.S[q][rp], P[r], fma(kRef<K>.M[q][rp], Q[r], out[r][q]));
+  };
+  auto write_plane = [&](int pz, int q) {   // out[.][q] -> global plane pz
+    if (!colin) return;
+    const bool zm = ((bm & 16) && pz == 0) || ((bm & 32) && pz == a.NZ - 1);
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int gy = Y0 + K * s + r;
+      if (gy >= a.NY) break;
+      const bool m = zm || xm || ((bm & 4) && gy == 0) || ((bm & 8) && gy == a.NY - 1);
+      epilogue(obase + (int64_t)a.NX * r + NXY * pz, out[r][q], m);
+    }
+  };
+
+  // ---- pipeline: one barrier per plane; iteration i runs the x-stage of plane i+1
+  // (A/B buffer (i+1)&1) and the y/z stages of plane i (buffer i&1)
+#pragma unroll
+  for (int i = 0; i < NB - 1; ++i) load_plane(i);
+  st_cp_wait<NB - 2>();
+  __syncthreads();
+  load_plane(NB - 1);
+  x_stage(0);
+  st_cp_wait<NB - 2>();
+  __syncthreads();
+  load_plane(NB);
+  int i = 0;
+  auto step = [&](double (&P)[K], double (&Q)[K]) {
+    if (i + 1 < NP) x_stage(i + 1);
+    plane_pq(i, P, Q);
+    st_cp_wait<NB - 2>();
+    __syncthreads();
+    load_plane(i + 1 + NB);
+    ++i;
+  };
+  double P[K], Q[K];
+  step(P, Q);
+  accumulate(0, P, Q);
+  for (int ez = ezs; ez < ez1; ++ez) {
+#pragma unroll
+    for (int rp = 1; rp <= K; ++rp) {
+      step(P, Q);
+      accumulate(rp, P, Q);
+    }
+    // planes K ez .. K ez + K - 1 are complete; the vertex plane carries
+    if (ez >= ez0) {
+#pragma unroll
+      for (int q = 0; q < K; ++q) write_plane(K * ez + q, q);
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      out[r][0] = out[r][K];
+#pragma unroll
+      for (int q = 1; q < N; ++q) out[r][q] = 0.0;
+    }
+    if (ez + 1 < ez1) accumulate(0, P, Q);   // the same plane is r' = 0 of the next element
+  }
+  if (ez1 == a.nz) write_plane(K * a.nz, 0);
+  st_cp_wait<0>();
+}
+
+// ---------------------------------------------------------------- launcher
+template <int K, int MODE>
+void stencil_k(fem_ctx* h, const Level& L, const StArgs& a0) {
+  using C = StCfg<K>;
+  StArgs a = a0;
+  a.nx = L.n[0];
+  a.ny = L.n[1];
+  a.nz = L.n[2];
+  a.NX = L.nn[0];
+  a.NY = L.nn[1];
+  a.NZ = L.nn[2];
+  int mask = 0;
+  for (int s = 0; s < 6; ++s)
+    if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
+  a.bcmask = mask;
+  const int gx = (a.NX + C::TX - 1) / C::TX, gy = (a.NY + C::TY - 1) / C::TY;
+  int ez = h->stencil_ez > 0 ? h->stencil_ez : 16;
+  ez = std::max(1, std::min(ez, a.nz));
+  a.ez_per_block = ez;
+  const int gz = (a.nz + ez - 1) / ez;
+  a.c0 = L.cart[0];
+  a.cy = L.cart[1];
+  a.cz = L.cart[2];
+  const size_t sm = sizeof(double) * C::SMEM;
+  smem_attr(reinterpret_cast<const void*>(cg_stencil2_kernel<K, MODE>), sm);
+  launch_pdl(h, cg_stencil2_kernel<K, MODE>, dim3(gx, gy, gz), dim3(C::THREADS), sm, a);
+  count_launch();
+  check_launch("cg_stencil2_kernel");
+}
+
+// y = A x (setc: y_c = x_c on constrained rows, else 0).  Single-rank Cartesian CG levels, k <= 4.
+void launch_cg_stencil_apply(fem_ctx* h, const Level& L, const double* x, double* y, bool setc) {
+  StArgs a{};
+  a.x = x;
+  a.y = y;
+  switch (h->k) {
+    case 2: stencil_k<2, 0>(h, L, a); break;
+    case 3: stencil_k<3, 0>(h, L, a); break;
+    case 4: stencil_k<4, 0>(h, L, a); break;
+    default: throw Error{FEM_E_ARG, "stencil kernel: k in 2..4"};
+  }
+  if (setc) launch_set_constrained(h, L, x, y);   // boundary rows only
+}
+
+// x_new = x + c1 (x - x_old) + c2 D^-1 (b - A x)  (fused Chebyshev step, R7)
+void launch_cg_stencil_cheb(fem_ctx* h, const Level& L, const double* x, const double* xo, const double* b,
+                            double* xnew, double c1, double c2) {
+  StArgs a{};
+  a.x = x;
+  a.y = xnew;
+  a.xo = xo;
+  a.b = b;
+  a.dinv = L.dinv;
+  a.c1 = c1;
+  a.c2 = c2;
+  switch (h->k) {
+    case 2: stencil_k<2, 1>(h, L, a); break;
+    case 3: stencil_k<3, 1>(h, L, a); break;
+    case 4: stencil_k<4, 1>(h, L, a); break;
+    default: throw Error{FEM_E_ARG, "stencil kernel: k in 2..4"};
+  }
+}
+
+}  // namespace fem

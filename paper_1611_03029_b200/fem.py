@@ -75,6 +75,7 @@ def _load():
         "mg_vcycle": (C.c_int, [P, P, I64, P, I64]),
         "cg_solve": (C.c_int, [P, P, I64, P, I64, D, I32, C.POINTER(I32), C.POINTER(D)]),
         "fem_rhs": (C.c_int, [P, P, I64]),
+        "cg_history": (C.c_int, [P, C.POINTER(D), I32, C.POINTER(I32)]),
         "fem_level_info": (C.c_int, [P, I32, C.POINTER(I64), C.POINTER(I32)]),
         "fem_level_apply": (C.c_int, [P, I32, P, I64, P, I64]),
         "fem_level_diagonal": (C.c_int, [P, I32, P, I64]),
@@ -101,7 +102,7 @@ _lib = _load()
 # exported symbol list (tests check it against include/fem.h)
 SYMBOLS = ("fem_default_options", "fem_setup", "fem_partition", "fem_nccl_unique_id",
            "fem_local_group_create", "fem_local_group_destroy", "fem_info", "fem_apply", "fem_diagonal", "mg_vcycle",
-           "cg_solve", "fem_rhs", "fem_level_info", "fem_level_apply", "fem_level_diagonal",
+           "cg_solve", "cg_history", "fem_rhs", "fem_level_info", "fem_level_apply", "fem_level_diagonal",
            "fem_level_lambda", "fem_level_geometry", "mg_smooth", "mg_prolongate_add", "mg_restrict",
            "mg_coarse_solve", "fem_sync", "fem_kernel_launches", "fem_profile_read", "fem_last_error",
            "fem_destroy")
@@ -287,6 +288,14 @@ class Fem:
         rc = _check(_lib.cg_solve(self.h, pb, nb, px, nx, rtol, maxit, C.byref(its), C.byref(rel)),
                     (FEM_OK, FEM_NOT_CONVERGED))
         return its.value, rel.value, rc == FEM_OK
+
+    def cg_history(self):
+        """||r_i|| / ||b||, i = 0 .. iterations, of the last cg_solve (host list)."""
+        n = C.c_int32()
+        _check(_lib.cg_history(self.h, None, 0, C.byref(n)))
+        buf = (C.c_double * max(n.value, 1))()
+        _check(_lib.cg_history(self.h, buf, n.value, C.byref(n)))
+        return list(buf[:n.value])
 
     def fem_rhs(self, b):
         p, n = _vec(b, True)

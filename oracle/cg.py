@@ -112,10 +112,13 @@ def _scatter_add(y, dm, ye):
 
 
 class Operator:
-    """y = A x (mode O3-iii) with the geometry factors G_q of every cell cached.
+    """y = A x with the geometry factors G_q of every cell cached (mode O3-iii).
 
     Cartesian meshes (mesh.uniform: eps = 0, exact map, kappa = 1): J is the same on
-    every cell, so G is computed once (from cell 0) and used for all cells."""
+    every cell, so every cell has the same element matrix; it is computed once by full
+    tensor quadrature (element_matrix, cell 0) and applied as y_e = K^e x_e (mode O3-ii,
+    SURVEY §8c: "Stored K^e -- one per level if Cartesian"; the same definition,
+    K^e = B^T G B, evaluated once instead of per cell)."""
 
     def __init__(self, mesh: Mesh, chunk: int = 8192):
         self.mesh, self.chunk = mesh, chunk
@@ -124,6 +127,7 @@ class Operator:
         self.uniform = mesh.uniform
         if self.uniform:
             self.G0 = metric(mesh, np.array([0]), self.quad)
+            self.Ke = element_matrix(mesh, 0, self.quad)
         else:
             self.G = [metric(mesh, np.arange(c0, min(c0 + chunk, mesh.n_cells)), self.quad)
                       for c0 in range(0, mesh.n_cells, chunk)]
@@ -141,7 +145,7 @@ class Operator:
         y = np.zeros(self.mesh.cg_n_dofs())
         for cells, G in self._chunks():
             dm = self.mesh.cg_dofmap(cells)
-            ye = element_apply_G(G, xf[dm], self.quad)
+            ye = xf[dm] @ self.Ke if self.uniform else element_apply_G(G, xf[dm], self.quad)
             _scatter_add(y, dm, ye)
         return np.where(self.mask, x, y)
 

@@ -151,7 +151,17 @@ def test_c1_diagonal_exact():
     assert np.allclose(d[~mask], expect[~mask], rtol=1e-14, atol=0)
 
 
-@pytest.mark.parametrize("k,eps", [(1, 0.0), (2, 0.05), (3, 0.05)])
+def test_cg_cartesian_stored_element_matrix_mode_equals_dense_b():
+    """Mode O3-ii (one stored K^e on a Cartesian mesh, used by Operator.apply) against the
+    dense-B quadrature evaluation B^T (G o (B x_e)) of every row (apply_rows), k = 4."""
+    m = Mesh((3, 2, 2), 4, bc=(DIRICHLET, NEUMANN, DIRICHLET, DIRICHLET, NEUMANN, DIRICHLET))
+    x = np.random.default_rng(5).standard_normal(m.cg_n_dofs())
+    y = cg.apply(m, x)
+    rows = np.arange(m.cg_n_dofs())
+    assert np.abs(cg.apply_rows(m, x, rows) - y).max() <= 1e-13 * np.abs(y).max()
+
+
+@pytest.mark.parametrize("k,eps", [(1, 0.0), (2, 0.05), (3, 0.05), (4, 0.0)])
 def test_cg_apply_modes_agree_symmetric_positive(k, eps):
     m = Mesh((3, 2, 4), k, eps=eps, bc=(DIRICHLET, NEUMANN, DIRICHLET, DIRICHLET, NEUMANN, DIRICHLET))
     rng = np.random.default_rng(1)

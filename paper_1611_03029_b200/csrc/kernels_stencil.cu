@@ -58,7 +58,7 @@ struct StCfg {
   static constexpr int THREADS = 32 * SY;         // thread = (output column, y slot)
   static constexpr int NB = 4;                    // x~ planes in flight
   static constexpr int NLD = (LR * LC + THREADS - 1) / THREADS;
-  static constexpr int SMEM = NB * LR * LP + 2 * 2 * LR * ABP + 8;   // doubles
+  static constexpr int SMEM = NB * LR * LP + 2 * 2 * LR * ABP + 4 + NB + 8;   // doubles (+ mbarriers)
   // two blocks per SM: 16 warps, 4 per SM sub-partition (16K registers each)
   static constexpr int MAXREG = 128;
 };
@@ -147,6 +147,18 @@ struct RefTab {
 };
 template <int K>
 __device__ constexpr RefTab<K> kRef{};
+// the same tables in the constant bank: DFMAs take them as uniform-register operands
+// loaded two doubles per LDCU.128 (compile-time literals cost two UMOVs per use)
+template <int K>
+__constant__ RefTab<K> cRef = RefTab<K>();
+#ifndef FEM_ST_CBANK
+#define FEM_ST_CBANK 0
+#endif
+#if FEM_ST_CBANK
+#define ST_TAB(K) cRef<K>
+#else
+#define ST_TAB(K) kRef<K>
+#endif
 
 struct StArgs {
   const double* __restrict__ x;
@@ -184,31 +196,38 @@ enum { kBarX = 1, kBarFull = 2, kBarEmpty = 4 };
 // the reference stiffness S instead of the mass M.
 template <int K, bool STIFF>
 __device__ __forceinline__ double band_row(const double* v, int r, bool both, bool left) {
-  constexpr const RefTab<K>& R = kRef<K>;
   double s = 0.0;
   if (r == 0) {
     if (both) {   // two half-length chains (DFMA latency), one extra add
       double s2 = 0.0;
 #pragma unroll
-      for (int j = 0; j < K; ++j) s = fma(STIFF ? R.Sv[j] : R.Mv[j], v[j], s);
+      for (int j = 0; j < K; ++j) s = fma(STIFF ? ST_TAB(K).Sv[j] : ST_TAB(K).Mv[j], v[j], s);
 #pragma unroll
-      for (int j = K; j <= 2 * K; ++j) s2 = fma(STIFF ? R.Sv[j] : R.Mv[j], v[j], s2);
+      for (int j = K; j <= 2 * K; ++j) s2 = fma(STIFF ? ST_TAB(K).Sv[j] : ST_TAB(K).Mv[j], v[j], s2);
       s += s2;
     } else if (left) {
 #pragma unroll
-      for (int j = 0; j <= K; ++j) s = fma(STIFF ? R.S[K][j] : R.M[K][j], v[j], s);
+      for (int j = 0; j <= K; ++j) s = fma(STIFF ? ST_TAB(K).S[K][j] : ST_TAB(K).M[K][j], v[j], s);
     } else {
 #pragma unroll
-      for (int j = 0; j <= K; ++j) s = fma(STIFF ? R.S[0][j] : R.M[0][j], v[K + j], s);
+      for (int j = 0; j <= K; ++j) s = fma(STIFF ? ST_TAB(K).S[0][j] : ST_TAB(K).M[0][j], v[K + j], s);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j <= K; ++j) s = fma(STIFF ? R.S[r][j] : R.M[r][j], v[K + j], s);
+    for (int j = 0; j <= K; ++j) s = fma(STIFF ? ST_TAB(K).S[r][j] : ST_TAB(K).M[r][j], v[K + j], s);
   }
   return s;
 }
 
-template <int K, int MODE>
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// arrive on bar when all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int K, int MODE, bool ISO>
 __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXREG)
     cg_stencil2_kernel(StArgs a) {
   FEM_PDL_ENTRY();
@@ -217,6 +236,10 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   extern __shared__ double smem[];
   double* Xt = smem;                           // [NB][LR][LP]
   double* AB = smem + NB * LR * LP;            // [2 buffers][A, B][LR][ABP]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(AB + 2 * 2 * LR * ABP);
+  uint64_t* full = bars;                       // [2]  A/B buffer written by every thread
+  uint64_t* empty = bars + 2;                  // [2]  A/B buffer read by every thread
+  uint64_t* landed = bars + 4;                 // [NB] x~ plane copies of every thread landed
   const int tid = threadIdx.x;
   const int e0 = blockIdx.x * SX, f0 = blockIdx.y * C::SY;
   const int X0 = K * e0, Y0 = K * f0;
@@ -227,36 +250,46 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   const int pz0 = K * ezs;
   const int64_t NXY = (int64_t)a.NX * a.NY;
   const int bm = a.bcmask;
-  // this thread's output column and y slot
+  // this thread's output column and y slot (rows K s + r)
   const int c = tid & 31, s = tid >> 5;
   const int gx = X0 + c;
   const int f = f0 + s;
-  const int64_t obase = gx + (int64_t)a.NX * (Y0 + K * s);   // output (gx, Y0 + K s, 0)
   const bool colin = c < C::TX && gx < a.NX;
-  const bool xm = ((bm & 1) && gx == 0) || ((bm & 2) && gx == a.NX - 1);
-
-  auto epilogue = [&](int64_t idx, double v, bool m) {
+  double* const ybase = a.y + gx + (int64_t)a.NX * (Y0 + K * s);
+  uint32_t rvalid = 0, rcons = 0;              // per row r: inside the domain / constrained (x, y)
+  {
+    const bool xm = ((bm & 1) && gx == 0) || ((bm & 2) && gx == a.NX - 1);
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int gy = Y0 + K * s + r;
+      if (colin && gy < a.NY) rvalid |= 1u << r;
+      if (xm || ((bm & 4) && gy == 0) || ((bm & 8) && gy == a.NY - 1)) rcons |= 1u << r;
+    }
+  }
+  auto epilogue = [&](int64_t off, double v, bool m) {   // off = offset from ybase
     if constexpr (MODE == 0) {   // constrained rows: 0 here, x_c by launch_set_constrained
-      a.y[idx] = m ? 0.0 : v;
+      ybase[off] = m ? 0.0 : v;
     } else {   // D^-1 = 0 on constrained rows
+      const int64_t idx = (ybase - a.y) + off;
       const double xv = a.x[idx];
       const double xov = a.xo ? a.xo[idx] : 0.0;
-      a.y[idx] = fma(a.c2 * a.dinv[idx], a.b[idx] - v, fma(a.c1, xv - xov, xv));
+      ybase[off] = fma(a.c2 * a.dinv[idx], a.b[idx] - v, fma(a.c1, xv - xov, xv));
     }
   };
   // tiles holding only the far boundary column / row of a Dirichlet side: every output
   // is a constrained row
   if ((X0 == a.NX - 1 && (bm & 2)) || (Y0 == a.NY - 1 && (bm & 8))) {
     const int q1 = K * ez1 + (ez1 == a.nz ? 1 : 0);
-    if (!colin) return;
     for (int pz = K * ez0; pz < q1; ++pz)
 #pragma unroll
-      for (int r = 0; r < K; ++r) {
-        const int gy = Y0 + K * s + r;
-        if (gy < a.NY) epilogue(obase + (int64_t)a.NX * r + NXY * pz, 0.0, true);
-      }
+      for (int r = 0; r < K; ++r)
+        if ((rvalid >> r) & 1u) epilogue((int64_t)a.NX * r + NXY * pz, 0.0, true);
     return;
   }
+  if (tid == 0) {
+    for (int b = 0; b < 4 + NB; ++b) mbar_init(bars + b, C::THREADS);
+  }
+  __syncthreads();
 
   // ---- loads: the same (row, column) slots of the tile in every plane
   int ld_off[C::NLD];
@@ -273,87 +306,93 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     if (in && !m) ld_ok |= 1u << j;
   }
   auto load_plane = [&](int i) {   // plane index i (global plane pz0 + i) into buffer i % NB
-    if (i < NP) {
-      const int gz = pz0 + i;
-      const bool zm = ((bm & 16) && gz == 0) || ((bm & 32) && gz == a.NZ - 1);
-      const double* src = a.x + (int64_t)gz * NXY;
-      double* dst = Xt + (i % NB) * LR * LP;
+    if (i >= NP) return;
+    const int gz = pz0 + i;
+    const bool zm = ((bm & 16) && gz == 0) || ((bm & 32) && gz == a.NZ - 1);
+    const double* src = a.x + (int64_t)gz * NXY;
+    double* dst = Xt + (i % NB) * LR * LP;
 #pragma unroll
-      for (int j = 0; j < C::NLD; ++j) {
-        const int idx = tid + j * C::THREADS;
-        if (idx < LR * LC) {
-          const int r = idx / LC, cc = idx % LC;
-          st_cp_async8(dst + r * LP + cc, src + ld_off[j], !zm && ((ld_ok >> j) & 1u));
-        }
+    for (int j = 0; j < C::NLD; ++j) {
+      const int idx = tid + j * C::THREADS;
+      if (idx < LR * LC) {
+        const int so = LP == LC ? idx : (idx / LC) * LP + idx % LC;
+        st_cp_async8(dst + so, src + ld_off[j], !zm && ((ld_ok >> j) & 1u));
       }
     }
-    st_cp_commit();
+    mbar_arrive_cp_async(landed + i % NB);
   };
 
-  // ---- x-stage of plane i: A = M_x x~, B = S_x x~ at every tile column, all LR rows.
+  // ---- x-stage of plane i: A = M_x x~, B = rx S_x x~ at every tile column, all LR rows.
   // Item = (row, slot): 2K+1 loaded values -> K outputs per field.  Slot e's vertex row
   // uses the pre-summed coefficients; on a domain boundary (e = 0 or e = nx) the missing
   // element's inputs are zero-filled and the vertex value is halved (M[K][K] = M[0][0],
   // S[K][K] = S[0][0]), so the same row gives the one-element sum without a branch.
   const int nsl = min(SX, a.nx - e0 + 1);
   const int nitems = LR * nsl;
+  const double rx = a.c0 / a.cy, rz = a.cz / a.cy;   // metric folded: y = c_y (M_z Q + r_z S_z P)
+  static_assert(C::LR * C::SX <= 2 * C::THREADS, "x-stage items per thread");
   auto x_stage = [&](int i) {
     const double* xb = Xt + (i % NB) * LR * LP;
     double* Ab = AB + (i & 1) * 2 * LR * ABP;
-    double* Bb = Ab + LR * ABP;
-    for (int it = tid; it < nitems; it += C::THREADS) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int it = tid + u * C::THREADS;
+      if (it >= nitems) break;
       const int row = it % LR, sl = it / LR;
-      const int e = e0 + sl;
       const double* v = xb + row * LP + sl * K;   // loaded column of node K (e-1)
       double w[2 * K + 1];
 #pragma unroll
       for (int j = 0; j <= 2 * K; ++j) w[j] = v[j];
-      const double hv = (e == 0 || e == a.nx) ? 0.5 : 1.0;
       const double wk = w[K];
-      w[K] = hv * wk;
+      w[K] = (e0 + sl == 0 || e0 + sl == a.nx) ? 0.5 * wk : wk;
       double* ao = Ab + row * ABP + sl * K;
-      double* bo = Bb + row * ABP + sl * K;
+      double* bo = ao + LR * ABP;
       ao[0] = band_row<K, false>(w, 0, true, false);
-      bo[0] = band_row<K, true>(w, 0, true, false);
+      bo[0] = ISO ? band_row<K, true>(w, 0, true, false) : rx * band_row<K, true>(w, 0, true, false);
       w[K] = wk;
 #pragma unroll
       for (int r = 1; r < K; ++r) {
         ao[r] = band_row<K, false>(w, r, true, false);
-        bo[r] = band_row<K, true>(w, r, true, false);
+        bo[r] = ISO ? band_row<K, true>(w, r, true, false) : rx * band_row<K, true>(w, r, true, false);
       }
     }
   };
 
-  // ---- y/z stages (thread = column c, y slot s, rows K s + r)
+  // ---- y/z stages (thread = column c, y slot s)
   const double hy = (f == 0 || f == a.ny) ? 0.5 : 1.0;
   double out[K][N];
 #pragma unroll
   for (int r = 0; r < K; ++r)
 #pragma unroll
     for (int q = 0; q < N; ++q) out[r][q] = 0.0;
-  auto plane_pq = [&](int i, double (&P)[K], double (&Q)[K]) {
-    const double* Ab = AB + (i & 1) * 2 * LR * ABP + (K * s) * ABP + c;
-    const double* Bb = Ab + LR * ABP;
-    double av[2 * K + 1], bv[2 * K + 1];
-#pragma unroll
-    for (int j = 0; j <= 2 * K; ++j) {
-      av[j] = Ab[j * ABP];
-      bv[j] = Bb[j * ABP];
-    }
-    // P = c_z M_y A, Q = c_x M_y B + c_y S_y A (vertex row: halved centre on the boundary)
+  // P = r_z M_y A, Q = M_y B + S_y A  (vertex row: halved centre on the boundary)
+  auto y_stage = [&](const double (&av)[2 * K + 1], const double (&bv)[2 * K + 1], double (&P)[K], double (&Q)[K]) {
     {
-      const double ak = av[K], bk = bv[K];
-      av[K] = hy * ak;
-      bv[K] = hy * bk;
-      P[0] = a.cz * band_row<K, false>(av, 0, true, false);
-      Q[0] = fma(a.cy, band_row<K, true>(av, 0, true, false), a.c0 * band_row<K, false>(bv, 0, true, false));
-      av[K] = ak;
-      bv[K] = bk;
+      double p1 = 0.0, p2 = 0.0, q1 = 0.0, q2 = 0.0;
+#pragma unroll
+      for (int j = 0; j <= 2 * K; ++j) {
+        const double aj = j == K ? hy * av[j] : av[j], bj = j == K ? hy * bv[j] : bv[j];
+        if (j < K) {
+          p1 = fma(ST_TAB(K).Mv[j], aj, p1);
+          q1 = fma(ST_TAB(K).Sv[j], aj, fma(ST_TAB(K).Mv[j], bj, q1));
+        } else {
+          p2 = fma(ST_TAB(K).Mv[j], aj, p2);
+          q2 = fma(ST_TAB(K).Sv[j], aj, fma(ST_TAB(K).Mv[j], bj, q2));
+        }
+      }
+      P[0] = ISO ? p1 + p2 : rz * (p1 + p2);
+      Q[0] = q1 + q2;
     }
 #pragma unroll
     for (int r = 1; r < K; ++r) {
-      P[r] = a.cz * band_row<K, false>(av, r, true, false);
-      Q[r] = fma(a.cy, band_row<K, true>(av, r, true, false), a.c0 * band_row<K, false>(bv, r, true, false));
+      double p = 0.0, q = 0.0;
+#pragma unroll
+      for (int j = 0; j <= K; ++j) {
+        p = fma(ST_TAB(K).M[r][j], av[K + j], p);
+        q = fma(ST_TAB(K).S[r][j], av[K + j], fma(ST_TAB(K).M[r][j], bv[K + j], q));
+      }
+      P[r] = ISO ? p : rz * p;
+      Q[r] = q;
     }
   };
   auto accumulate = [&](int rp, const double (&P)[K], const double (&Q)[K]) {
@@ -361,47 +400,55 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     for (int q = 0; q < N; ++q)
 #pragma unroll
       for (int r = 0; r < K; ++r)
-        out[r][q] = fma(kRef<K>.S[q][rp], P[r], fma(kRef<K>.M[q][rp], Q[r], out[r][q]));
+        out[r][q] = fma(ST_TAB(K).S[q][rp], P[r], fma(ST_TAB(K).M[q][rp], Q[r], out[r][q]));
   };
-  auto write_plane = [&](int pz, int q) {   // out[.][q] -> global plane pz
-    if (!colin) return;
+  auto write_plane = [&](int pz, int q) {   // c_y out[.][q] -> global plane pz
     const bool zm = ((bm & 16) && pz == 0) || ((bm & 32) && pz == a.NZ - 1);
 #pragma unroll
-    for (int r = 0; r < K; ++r) {
-      const int gy = Y0 + K * s + r;
-      if (gy >= a.NY) break;
-      const bool m = zm || xm || ((bm & 4) && gy == 0) || ((bm & 8) && gy == a.NY - 1);
-      epilogue(obase + (int64_t)a.NX * r + NXY * pz, out[r][q], m);
-    }
+    for (int r = 0; r < K; ++r)
+      if ((rvalid >> r) & 1u)
+        epilogue((int64_t)a.NX * r + NXY * pz, a.cy * out[r][q], zm || ((rcons >> r) & 1u));
   };
 
-  // ---- pipeline: one barrier per plane; iteration i runs the x-stage of plane i+1
-  // (A/B buffer (i+1)&1) and the y/z stages of plane i (buffer i&1)
+  // ---- pipeline (mbarriers: a warp may run up to one plane ahead of the slowest one).
+  // Iteration i: x-stage of plane i+1 into A/B buffer (i+1)&1, then the y/z stages of
+  // plane i from buffer i&1; plane i+NB is copied into the x~ buffer plane i used.
 #pragma unroll
-  for (int i = 0; i < NB - 1; ++i) load_plane(i);
-  st_cp_wait<NB - 2>();
-  __syncthreads();
-  load_plane(NB - 1);
+  for (int i = 0; i < NB; ++i) load_plane(i);
+  mbar_wait(landed, 0);
   x_stage(0);
-  st_cp_wait<NB - 2>();
-  __syncthreads();
-  load_plane(NB);
+  mbar_arrive(full);
+  double P[K], Q[K];
   int i = 0;
-  auto step = [&](double (&P)[K], double (&Q)[K]) {
-    if (i + 1 < NP) x_stage(i + 1);
-    plane_pq(i, P, Q);
-    st_cp_wait<NB - 2>();
-    __syncthreads();
-    load_plane(i + 1 + NB);
+  auto step = [&]() {
+    if (i + 1 < NP) {
+      if (i >= 1) mbar_wait(empty + ((i + 1) & 1), ((i - 1) >> 1) & 1);   // y/z of plane i-1 done
+      mbar_wait(landed + (i + 1) % NB, ((i + 1) / NB) & 1);
+      x_stage(i + 1);
+      mbar_arrive(full + ((i + 1) & 1));
+    }
+    mbar_wait(full + (i & 1), (i >> 1) & 1);       // x-stage of plane i done (x~ buffer i % NB free)
+    load_plane(i + NB);
+    double av[2 * K + 1], bv[2 * K + 1];
+    {
+      const double* Ab = AB + (i & 1) * 2 * LR * ABP + (K * s) * ABP + c;
+      const double* Bb = Ab + LR * ABP;
+#pragma unroll
+      for (int j = 0; j <= 2 * K; ++j) {
+        av[j] = Ab[j * ABP];
+        bv[j] = Bb[j * ABP];
+      }
+    }
+    mbar_arrive(empty + (i & 1));
+    y_stage(av, bv, P, Q);
     ++i;
   };
-  double P[K], Q[K];
-  step(P, Q);
+  step();
   accumulate(0, P, Q);
   for (int ez = ezs; ez < ez1; ++ez) {
 #pragma unroll
     for (int rp = 1; rp <= K; ++rp) {
-      step(P, Q);
+      step();
       accumulate(rp, P, Q);
     }
     // planes K ez .. K ez + K - 1 are complete; the vertex plane carries
@@ -418,7 +465,6 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     if (ez + 1 < ez1) accumulate(0, P, Q);   // the same plane is r' = 0 of the next element
   }
   if (ez1 == a.nz) write_plane(K * a.nz, 0);
-  st_cp_wait<0>();
 }
 
 // ---------------------------------------------------------------- launcher
@@ -437,7 +483,14 @@ void stencil_k(fem_ctx* h, const Level& L, const StArgs& a0) {
     if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
   a.bcmask = mask;
   const int gx = (a.NX + C::TX - 1) / C::TX, gy = (a.NY + C::TY - 1) / C::TY;
-  int ez = h->stencil_ez > 0 ? h->stencil_ez : 16;
+  // z-element layers per block: about 8 waves of 2 blocks per SM (wave quantisation,
+  // small levels) without making the recomputed halo layer (1/ez of the work) large
+  int ez = h->stencil_ez;
+  if (ez <= 0) {
+    const long tiles = (long)gx * gy;
+    ez = (int)std::lround((double)a.nz * tiles / (8.0 * 2 * 148));
+    ez = std::max(2, std::min(ez, 32));
+  }
   ez = std::max(1, std::min(ez, a.nz));
   a.ez_per_block = ez;
   const int gz = (a.nz + ez - 1) / ez;
@@ -445,8 +498,10 @@ void stencil_k(fem_ctx* h, const Level& L, const StArgs& a0) {
   a.cy = L.cart[1];
   a.cz = L.cart[2];
   const size_t sm = sizeof(double) * C::SMEM;
-  smem_attr(reinterpret_cast<const void*>(cg_stencil2_kernel<K, MODE>), sm);
-  launch_pdl(h, cg_stencil2_kernel<K, MODE>, dim3(gx, gy, gz), dim3(C::THREADS), sm, a);
+  const bool iso = L.cart[0] == L.cart[1] && L.cart[1] == L.cart[2];
+  auto kern = iso ? cg_stencil2_kernel<K, MODE, true> : cg_stencil2_kernel<K, MODE, false>;
+  smem_attr(reinterpret_cast<const void*>(kern), sm);
+  launch_pdl(h, kern, dim3(gx, gy, gz), dim3(C::THREADS), sm, a);
   count_launch();
   check_launch("cg_stencil2_kernel");
 }

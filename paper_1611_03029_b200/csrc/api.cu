@@ -883,6 +883,26 @@ void level_geometry_and_diagonal(fem_ctx* h, Level& L) {
     launch_set_constrained(h, L, nullptr, L.diag);     // diag = 1 on constrained rows
     launch_dinv(h, L);
     launch_set_constrained_value(h, L, 0.0, L.dinv);   // D^-1 = 0 on constrained rows
+    if (use_stencil2(h, L)) {
+      // Cartesian CG: D^-1 depends on a node only through its class per direction,
+      // 0 (first node), r = 1..k-1 (inside an element), k (interior vertex), k+1 (last
+      // node); the fused stencil epilogue reads it from this (k+2)^3 table, copied from
+      // the computed D^-1 at one representative node per class
+      const int K = h->k, nc = K + 2;
+      L.dinv_cls = dalloc((int64_t)nc * nc * nc);
+      auto rep = [&](int d, int cl) {
+        if (cl == 0) return 0;
+        if (cl == K + 1) return L.nn[d] - 1;
+        return (cl == K && L.n[d] < 2) ? 0 : cl;
+      };
+      for (int c2 = 0; c2 < nc; ++c2)
+        for (int c1 = 0; c1 < nc; ++c1)
+          for (int c0 = 0; c0 < nc; ++c0) {
+            const int64_t node = rep(0, c0) + (int64_t)L.nn[0] * (rep(1, c1) + (int64_t)L.nn[1] * rep(2, c2));
+            FEM_CUDA_TRY(cudaMemcpyAsync(L.dinv_cls + c0 + nc * (c1 + nc * c2), L.dinv + node, sizeof(double),
+                                         cudaMemcpyDeviceToDevice, h->stream));
+          }
+    }
   } else {
     launch_dg_diagonal(h, L);
     launch_dinv(h, L);

@@ -165,7 +165,8 @@ struct StArgs {
   double* __restrict__ y;          // MODE 0: A x;  MODE 1: x_new
   const double* __restrict__ xo;   // MODE 1: x_old (nullptr: none)
   const double* __restrict__ b;    // MODE 1
-  const double* __restrict__ dinv; // MODE 1
+  const double* __restrict__ dinv; // MODE 1 (unused when dcls is set)
+  const double* __restrict__ dcls; // MODE 1: D^-1 per node class, (K+2)^3 (api.cu), or nullptr
   double c1, c2;                   // MODE 1
   double c0, cy, cz;               // Cartesian metric det J (2/h_d)^2 of x, y, z
   int nx, ny, nz;                  // cells
@@ -402,12 +403,71 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
       for (int r = 0; r < K; ++r)
         out[r][q] = fma(ST_TAB(K).S[q][rp], P[r], fma(ST_TAB(K).M[q][rp], Q[r], out[r][q]));
   };
-  auto write_plane = [&](int pz, int q) {   // c_y out[.][q] -> global plane pz
+  auto write_plane = [&](int pz, int q) {   // MODE 0: c_y out[.][q] -> global plane pz
     const bool zm = ((bm & 16) && pz == 0) || ((bm & 32) && pz == a.NZ - 1);
 #pragma unroll
     for (int r = 0; r < K; ++r)
       if ((rvalid >> r) & 1u)
         epilogue((int64_t)a.NX * r + NXY * pz, a.cy * out[r][q], zm || ((rcons >> r) & 1u));
+  };
+  // MODE 1: node classes of D^-1 (see api.cu): 0 first node, r inside an element, K interior
+  // vertex, K+1 last node
+  auto ncls = [&](int g, int nn) { return g == 0 ? 0 : g == nn - 1 ? K + 1 : (g % K == 0 ? K : g % K); };
+  int clxy[K];   // x and y class part of the D^-1 class index
+#pragma unroll
+  for (int r = 0; r < K; ++r)
+    clxy[r] = ncls(min(gx, a.NX - 1), a.NX) + (K + 2) * ncls(min(Y0 + K * s + r, a.NY - 1), a.NY);
+  // MODE 1: the element's K output planes (plus the top plane at the domain end): all
+  // operand loads of a pair of planes are issued before any store (a store may alias them,
+  // so the compiler would otherwise serialise one DRAM round trip per output)
+  const int64_t yoff = ybase - a.y;
+  auto write_element = [&](int ez, int nq) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      if (q >= nq) break;
+      const int pz = K * ez + q;
+      const int clz = (K + 2) * (K + 2) * ncls(pz, a.NZ);
+      const int64_t po = yoff + NXY * pz;
+      const double* xp = a.x + po;
+      const double* bp = a.b + po;
+      const double* op = a.xo ? a.xo + po : nullptr;
+      double xv[K], xov[K], bv2[K];
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const bool ok = (rvalid >> r) & 1u;
+        xv[r] = ok ? xp[a.NX * r] : 0.0;
+        xov[r] = ok && op ? op[a.NX * r] : 0.0;
+        bv2[r] = ok ? bp[a.NX * r] : 0.0;
+      }
+      double* yp = a.y + po;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        if (!((rvalid >> r) & 1u)) continue;
+        const double dv = a.dcls ? __ldg(a.dcls + clxy[r] + clz) : a.dinv[po + a.NX * r];
+        const double v = a.cy * out[r][q];
+        yp[a.NX * r] = fma(a.c2 * dv, bv2[r] - v, fma(a.c1, xv[r] - xov[r], xv[r]));
+      }
+    }
+  };
+
+  // MODE 1: the epilogue reads x, x_old, b, D^-1 of the element's output planes; a burst of
+  // 16 x 4 dependent loads at the element end stalls the warps for a DRAM round trip, so
+  // the warp bulk-prefetches its 4 rows x (K planes) x 4 arrays into L2 when the element
+  // starts (one 256-byte range per lane-task, two per lane).
+  auto prefetch_epilogue = [&](int ez) {
+    if constexpr (MODE == 1) {
+      if (ez < ez0) return;
+      const int nq = K + (ez + 1 == a.nz ? 1 : 0);
+      const int ncol = min(C::TX, a.NX - X0);
+      for (int t = c; t < 4 * K * nq; t += 32) {
+        const int arr = t & 3, rq = t >> 2, r = rq % K, q = rq / K;
+        const int gy = Y0 + K * s + r;
+        if (gy >= a.NY) continue;
+        const double* base = arr == 0 ? a.x : arr == 1 ? a.xo : arr == 2 ? a.b : (a.dcls ? nullptr : a.dinv);
+        if (!base) continue;
+        prefetch_l2_range(base + X0 + (int64_t)a.NX * gy + NXY * (K * ez + q), sizeof(double) * ncol);
+      }
+    }
   };
 
   // ---- pipeline (mbarriers: a warp may run up to one plane ahead of the slowest one).
@@ -445,7 +505,9 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   };
   step();
   accumulate(0, P, Q);
+  prefetch_epilogue(ez0);
   for (int ez = ezs; ez < ez1; ++ez) {
+    if (ez + 1 < ez1) prefetch_epilogue(ez + 1);   // one element ahead
 #pragma unroll
     for (int rp = 1; rp <= K; ++rp) {
       step();
@@ -453,8 +515,12 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     }
     // planes K ez .. K ez + K - 1 are complete; the vertex plane carries
     if (ez >= ez0) {
+      if constexpr (MODE == 0) {
 #pragma unroll
-      for (int q = 0; q < K; ++q) write_plane(K * ez + q, q);
+        for (int q = 0; q < K; ++q) write_plane(K * ez + q, q);
+      } else {
+        write_element(ez, ez + 1 == a.nz ? K + 1 : K);   // the top plane (q = K) too at the end
+      }
     }
 #pragma unroll
     for (int r = 0; r < K; ++r) {
@@ -464,7 +530,9 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     }
     if (ez + 1 < ez1) accumulate(0, P, Q);   // the same plane is r' = 0 of the next element
   }
-  if (ez1 == a.nz) write_plane(K * a.nz, 0);
+  if constexpr (MODE == 0) {
+    if (ez1 == a.nz) write_plane(K * a.nz, 0);
+  }
 }
 
 // ---------------------------------------------------------------- launcher
@@ -489,7 +557,7 @@ void stencil_k(fem_ctx* h, const Level& L, const StArgs& a0) {
   if (ez <= 0) {
     const long tiles = (long)gx * gy;
     ez = (int)std::lround((double)a.nz * tiles / (8.0 * 2 * 148));
-    ez = std::max(2, std::min(ez, 32));
+    ez = std::max(4, std::min(ez, 32));
   }
   ez = std::max(1, std::min(ez, a.nz));
   a.ez_per_block = ez;
@@ -529,6 +597,7 @@ void launch_cg_stencil_cheb(fem_ctx* h, const Level& L, const double* x, const d
   a.xo = xo;
   a.b = b;
   a.dinv = L.dinv;
+  a.dcls = L.dinv_cls;
   a.c1 = c1;
   a.c2 = c2;
   switch (h->k) {

@@ -81,6 +81,15 @@ def element_apply_G(G, xe, quad):
     return flux.reshape(len(xe), nq * 3) @ B
 
 
+def cell_diagonals(G, quad):
+    """K^e_ii = sum_q sum_de grad_d phi_i(q) G_q,de grad_e phi_i(q) for a batch of cells,
+    G [C, q, 3, 3]: the same sum as einsum('qdi,cqde,qei->ci'), evaluated as one matrix
+    product with H[q, de, i] = grad_d phi_i(q) grad_e phi_i(q)."""
+    g = quad.grad
+    H = (g[:, :, None, :] * g[:, None, :, :]).reshape(-1, g.shape[2])     # [(q, d, e), i]
+    return np.ascontiguousarray(G).reshape(len(G), -1) @ H
+
+
 def element_apply(mesh, cells, xe, quad):
     return element_apply_G(metric(mesh, cells, quad), xe, quad)
 
@@ -153,7 +162,10 @@ class Operator:
         """sum over cells of K^e_ii = sum_q w det J |J^-T grad phi_i|^2; 1 on constrained rows."""
         d = np.zeros(self.mesh.cg_n_dofs())
         for cells, G in self._chunks():
-            de = np.einsum('qdi,cqde,qei->ci', self.quad.grad, G, self.quad.grad)
+            if self.uniform:   # mode O3-ii: K^e_ii of the one stored element matrix
+                de = np.broadcast_to(np.diag(self.Ke), (len(cells), self.Ke.shape[0]))
+            else:
+                de = cell_diagonals(G, self.quad)
             dm = self.mesh.cg_dofmap(cells)
             _scatter_add(d, dm, de)
         return np.where(self.mask, 1.0, d)

@@ -27,7 +27,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from .basis import Basis1D
-from .cg import CellQuadrature, cell_geometry, metric, element_matrix, element_apply_G
+from .cg import CellQuadrature, cell_geometry, metric, element_matrix, element_apply_G, cell_diagonals
 from .mesh import Mesh, eval_basis_3d, DIRICHLET
 
 
@@ -189,7 +189,7 @@ class Operator:
         sum_q JxW (-2 phi_i d_n phi_i + 2 sigma phi_i^2)."""
         D = np.zeros((self.mesh.n_cells, self.m))
         for cells, G in self._cell_chunks():
-            D[cells] += np.einsum('qdi,cqde,qei->ci', self.quad.grad, G, self.quad.grad)
+            D[cells] += cell_diagonals(G, self.quad)
         for fd in self.faces:
             for cells, ref, Jn, sg in ((fd.cm, fd.rm, fd.Jn_m, 1.0), (fd.cp, fd.rp, fd.Jn_p, -1.0)):
                 phidn = sum((fd.JxW * Jn[..., e]) @ (ref.val * ref.grad[:, e, :]) for e in range(3))

@@ -1462,13 +1462,22 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     double *r = L.pcg_r, *p = L.pcg_p, *q = L.pcg_q, *z = L.pcg_z;
     // CG Dirichlet rows are identity rows: x_c = b_c, r_c = 0 (the system decouples)
     if (is_cg(h)) launch_set_constrained(h, L, db, dx);
-    launch_copy(h, p, dx, n);                 // level vector (ghosts) for the first apply
-    apply_level(h, L, p, q, true);
-    launch_sub(h, r, db, q, n);
+    // r_0 = b - A x_0; a zero start (the usual call) skips the operator apply
     dot(h, L, db, db, 6);
-    dot(h, L, r, r, 2);
+    dot(h, L, dx, dx, 7);
     FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, h->stream));
     FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (h->hscal[7] == 0.0) {
+      launch_copy(h, r, db, n);
+      h->hscal[2] = h->hscal[6];
+    } else {
+      launch_copy(h, p, dx, n);                 // level vector (ghosts) for the first apply
+      apply_level(h, L, p, q, true);
+      launch_sub(h, r, db, q, n);
+      dot(h, L, r, r, 2);
+      FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal + 2, h->scal + 2, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+      FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
     const double bnorm = std::sqrt(h->hscal[6]);
     double rnorm = std::sqrt(h->hscal[2]);
     int it = 0;
@@ -1519,6 +1528,7 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
           prof_graph(h, h->sg.ev_upd);
         }
         ++it;
+        if (h->comm) h->comm->check();
         const double pq = h->hscal[1];
         rnorm = std::sqrt(h->hscal[2]);
         h->hist.push_back(bnorm > 0 ? rnorm / bnorm : rnorm);
@@ -1551,6 +1561,7 @@ int fem_sync(fem_handle h) {
   return guarded([&] {
     check_handle(h);
     FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (h->comm) h->comm->check();
   });
 }
 

@@ -40,6 +40,7 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -61,6 +62,7 @@ NcclApi& nccl() {
     FEM_NCCL_SYM(GroupStart);
     FEM_NCCL_SYM(GroupEnd);
     FEM_NCCL_SYM(GetErrorString);
+    FEM_NCCL_SYM(CommGetAsyncError);
 #undef FEM_NCCL_SYM
   });
   if (!api.so || !api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.AllReduce ||
@@ -99,6 +101,14 @@ class NcclComm : public Comm {
     nccl_try(nccl().AllReduce(p, p, (size_t)n, ncclFloat64, ncclSum, comm_, s), "ncclAllReduce");
   }
   bool graph_capturable() const override { return true; }
+  // a peer that died or a network fault surfaces here instead of as a hang in the next
+  // synchronisation (polled after every PCG iteration and in fem_sync)
+  void check() override {
+    if (!nccl().CommGetAsyncError) return;
+    ncclResult_t st = ncclSuccess;
+    nccl_try(nccl().CommGetAsyncError(comm_, &st), "ncclCommGetAsyncError");
+    if (st != ncclSuccess && st != ncclInProgress) nccl_try(st, "NCCL asynchronous error");
+  }
 
  private:
   ncclComm_t comm_ = nullptr;

@@ -76,6 +76,8 @@ class Comm {
   virtual void exchange(const std::vector<Msg>& sends, const std::vector<Msg>& recvs, cudaStream_t s) = 0;
   virtual void allreduce_sum(double* p, int64_t n, cudaStream_t s) = 0;
   virtual bool graph_capturable() const = 0;
+  // asynchronous transport errors (NCCL: ncclCommGetAsyncError); throws FEM_E_NCCL
+  virtual void check() {}
 };
 std::unique_ptr<Comm> make_nccl_comm(const void* id, int rank, int nranks);
 std::unique_ptr<Comm> make_local_comm(void* group, int rank, int nranks);

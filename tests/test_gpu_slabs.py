@@ -84,6 +84,9 @@ CASES = [
     ("sipg", 2, (2, 2, 6), 0.05, MIXED, 2, 1),
     ("sipg", 3, (4, 4, 8), 0.0, (DIRICHLET,) * 6, 4, 1),
     ("sipg", 4, (2, 2, 4), 0.05, (DIRICHLET,) * 6, 2, 2),
+    # eight ranks (one z-layer each on the finest level, the box's GPU count)
+    ("cg", 2, (2, 2, 8), 0.05, MIXED, 8, 1),
+    ("sipg", 2, (2, 2, 8), 0.0, (DIRICHLET,) * 6, 8, 1),
 ]
 
 

@@ -38,22 +38,22 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
   const int zi = ta + B * tb;   // Z-pattern word of the thread's line
   double g[N], w[N];
   // Z: interpolate in z
-  mv<N>(T.val, u, v);
+  MV_VAL(T, u, v);
 #pragma unroll
   for (int l = 0; l < N; ++l) s0[zi + S * l] = v[l];
   __syncthreads();
   // Y: interpolate in y
 #pragma unroll
   for (int l = 0; l < N; ++l) w[l] = s0[ta + B * l + S * tb];
-  mv<N>(T.val, w, v);
+  MV_VAL(T, w, v);
 #pragma unroll
   for (int l = 0; l < N; ++l) s0[ta + B * l + S * tb] = v[l];
   __syncthreads();
   // X: interpolate in x, d/dxi_x by collocation
 #pragma unroll
   for (int l = 0; l < N; ++l) w[l] = s0[l + B * ta + S * tb];
-  mv<N>(T.val, w, v);
-  mv<N>(T.colloc, v, g);
+  MV_VAL(T, w, v);
+  MV_COL(T, v, g);
 #pragma unroll
   for (int l = 0; l < N; ++l) {
     s0[l + B * ta + S * tb] = v[l];
@@ -63,14 +63,14 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
   // Y: d/dxi_y
 #pragma unroll
   for (int l = 0; l < N; ++l) w[l] = s0[ta + B * l + S * tb];
-  mv<N>(T.colloc, w, g);
+  MV_COL(T, w, g);
 #pragma unroll
   for (int l = 0; l < N; ++l) s1[ta + B * l + S * tb] = g[l];
   __syncthreads();
   // Z: d/dxi_z, quadrature-point operation, transposed d/dxi_z
 #pragma unroll
   for (int l = 0; l < N; ++l) w[l] = s0[zi + S * l];
-  mv<N>(T.colloc, w, g);
+  MV_COL(T, w, g);
   if (DEFORMED && geo.bar) mbar_wait(geo.bar, 0);
 #pragma unroll
   for (int l = 0; l < N; ++l) {
@@ -103,7 +103,7 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
     s1[zq] = fy;
     v[l] = fz;
   }
-  mvt<N>(T.colloc, v, w);
+  MVT_COL(T, v, w);
 #pragma unroll
   for (int l = 0; l < N; ++l) s0[zi + S * l] = w[l];
   __syncthreads();
@@ -113,7 +113,7 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
     v[l] = s1[ta + B * l + S * tb];
     w[l] = s0[ta + B * l + S * tb];
   }
-  mvt_add<N>(T.colloc, v, w);
+  MVT_ADD_COL(T, v, w);
 #pragma unroll
   for (int l = 0; l < N; ++l) s0[ta + B * l + S * tb] = w[l];
   __syncthreads();
@@ -123,22 +123,22 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
     v[l] = s2[l + B * ta + S * tb];
     w[l] = s0[l + B * ta + S * tb];
   }
-  mvt_add<N>(T.colloc, v, w);
-  mvt<N>(T.val, w, v);
+  MVT_ADD_COL(T, v, w);
+  MVT_VAL(T, w, v);
 #pragma unroll
   for (int l = 0; l < N; ++l) s0[l + B * ta + S * tb] = v[l];
   __syncthreads();
   // Y: interpolate back in y
 #pragma unroll
   for (int l = 0; l < N; ++l) w[l] = s0[ta + B * l + S * tb];
-  mvt<N>(T.val, w, v);
+  MVT_VAL(T, w, v);
 #pragma unroll
   for (int l = 0; l < N; ++l) s0[ta + B * l + S * tb] = v[l];
   __syncthreads();
   // Z: interpolate back in z
 #pragma unroll
   for (int l = 0; l < N; ++l) w[l] = s0[zi + S * l];
-  mvt<N>(T.val, w, v);
+  MVT_VAL(T, w, v);
 }
 
 }  // namespace fem

@@ -220,10 +220,10 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
     double in[N], out[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) in[i] = fld[i];
-    mv<N>(T.val, in, out);
+    MV_VAL(T, in, out);
     if (DEFORMED && (f == 0 || f == 2)) {
       double dd[N];
-      mv<N>(T.colloc, out, dd);
+      MV_COL(T, out, dd);
       double* fd = F + (s * 8 + (f == 0 ? 4 : 6)) * FS + N * row;
 #pragma unroll
       for (int i = 0; i < N; ++i) fd[i] = dd[i];
@@ -242,10 +242,10 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
       double in[N], out[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) in[i] = fld[N * i];
-      mv<N>(T.val, in, out);
+      MV_VAL(T, in, out);
       if (DEFORMED && (f == 0 || f == 2)) {
         double dd[N];
-        mv<N>(T.colloc, out, dd);
+        MV_COL(T, out, dd);
         double* fd = F + (s * 8 + (f == 0 ? 5 : 7)) * FS + col;
 #pragma unroll
         for (int i = 0; i < N; ++i) fd[N * i] = dd[i];
@@ -324,14 +324,14 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
           double b2[N];
 #pragma unroll
           for (int i = 0; i < N; ++i) b2[i] = Bs[3 * FS + N * i + col];
-          mvt_add<N>(T.colloc, b2, in);
+          MVT_ADD_COL(T, b2, in);
         }
       } else {
         const int f = (g == 1) ? 1 : 2;
 #pragma unroll
         for (int i = 0; i < N; ++i) in[i] = Bs[f * FS + N * i + col];
       }
-      mvt<N>(T.val, in, out);
+      MVT_VAL(T, in, out);
       const int f = (g == 0) ? 0 : (g == 1 ? 1 : 2);
 #pragma unroll
       for (int i = 0; i < N; ++i) Bs[f * FS + N * i + col] = out[i];
@@ -349,9 +349,9 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
       double q[N];
 #pragma unroll
       for (int i = 0; i < N; ++i) q[i] = Bs[2 * FS + N * row + i];
-      mvt_add<N>(T.colloc, q, in);
+      MVT_ADD_COL(T, q, in);
     }
-    mvt<N>(T.val, in, out);
+    MVT_VAL(T, in, out);
 #pragma unroll
     for (int i = 0; i < N; ++i) Bs[g * FS + N * row + i] = out[i];
   }

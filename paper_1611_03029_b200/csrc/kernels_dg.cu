@@ -119,6 +119,14 @@ struct DgArgs {
   double c[3];      // Cartesian metric det J (2/h_d)^2
   double h[3];
   double sigma[3];  // Cartesian penalty c (k+1)^2 / h_d
+  // deformed box with the analytic map (reading R2; not the general N3 geometries):
+  // FEM_DG_FGEO_FLY=1 recomputes the face quadrature data (JxW, J^-1 n) from the map at
+  // each face point instead of reading the 7 x (k+1)^2 face records (the penalty sigma_F,
+  // one double per face, is still read).  By the flop/byte balance (~5.7 flop/B) ~100
+  // flops should beat 56 bytes, but the three sincospi, the divide and the square root
+  // per point measured slower (C5 apply 7.28 vs 5.35 ms): off by default, parity-tested.
+  int fgeo_fly;
+  MapArgs map;
 };
 
 // result v = (A x)_i of DoF i: stored, or consumed by the fused Chebyshev epilogue
@@ -267,15 +275,41 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
       double dn_own, dn_nb = 0.0, JxW, sig, Jn[3];
       if (DEFORMED) {
         const int64_t fr = face_record(A, D, c, c[D] + s);
-        const double* rec = A.faceq + fr * 7 * N2;
-        JxW = __ldg(rec + t);
         sig = __ldg(A.fsigma + fr);
-        const int own = s ? 1 : 4, oth = s ? 4 : 1;  // own cell is the minus side iff s == 1
         double Jo[3];
+        if (A.fgeo_fly) {
+          // the face point in the own cell's reference coordinates; J (hence J^-1 n and
+          // JxW) is the same from both sides: one global map, equal cell sizes
+          double xi[3];
+          xi[D] = s ? 1.0 : -1.0;
+          xi[t1] = T.qp[a];
+          xi[t2] = T.qp[b];
+          const PointGeo g = map_point(A.map, c[0], c[1], c[2], xi[0], xi[1], xi[2]);
+          double v[3], nrm = 0.0;
 #pragma unroll
-        for (int e = 0; e < 3; ++e) {
-          Jn[e] = nsgn * __ldg(rec + (own + e) * N2 + t);
-          Jo[e] = nsgn * __ldg(rec + (oth + e) * N2 + t);
+          for (int e = 0; e < 3; ++e) {
+            v[e] = jinv(A.map, g, D, e);   // (J^-T e_D)_e: the minus side's normal direction
+            nrm = fma(v[e], v[e], nrm);
+          }
+          nrm = sqrt(nrm);
+          JxW = T.w[a] * T.w[b] * g.det * nrm;
+          const double inv = 1.0 / nrm;
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            const double jm = (jinv(A.map, g, e, 0) * v[0] + jinv(A.map, g, e, 1) * v[1] +
+                               jinv(A.map, g, e, 2) * v[2]) * inv;
+            Jn[e] = nsgn * jm;
+            Jo[e] = nsgn * jm;
+          }
+        } else {
+          const double* rec = A.faceq + fr * 7 * N2;
+          JxW = __ldg(rec + t);
+          const int own = s ? 1 : 4, oth = s ? 4 : 1;  // own cell is the minus side iff s == 1
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            Jn[e] = nsgn * __ldg(rec + (own + e) * N2 + t);
+            Jo[e] = nsgn * __ldg(rec + (oth + e) * N2 + t);
+          }
         }
         dn_own = Jn[t1] * Fs[4 * FS + t] + Jn[t2] * Fs[5 * FS + t] + Jn[D] * Fs[1 * FS + t];
         if (kind[s] == 0)
@@ -398,7 +432,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgQCPB<K>::value, dgq_minb
     c[1] = (int)(r % A.n[1]);
     c[2] = (int)(r / A.n[1]);
   }
-  if (FEM_DG_FACE_PREFETCH && DEFORMED && t == 0 && active) {
+  if (FEM_DG_FACE_PREFETCH && DEFORMED && !A.fgeo_fly && t == 0 && active) {
     // the cell's y- and z-face records (static; x-faces of the block's cells are one run)
 #pragma unroll
     for (int D = 1; D < 3; ++D)
@@ -875,6 +909,7 @@ __global__ void dg_face_kappa_kernel(double* faceq, const double* kap, int64_t n
 // ---------------------------------------------------------------- launchers
 namespace {
 
+MapArgs dg_map_args(const fem_ctx* h, const Level& L);
 DgArgs dg_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
   DgArgs A;
   A.x = x;
@@ -905,6 +940,11 @@ DgArgs dg_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
   for (int s = 0; s < 6; ++s)
     if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
   A.bcmask = mask;
+  A.fgeo_fly = 0;
+  if (!L.cartesian && !mesh_general(h->mesh) && h->dg_fgeo_fly) {
+    A.fgeo_fly = 1;
+    A.map = dg_map_args(h, L);
+  }
   return A;
 }
 

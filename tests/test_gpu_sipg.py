@@ -188,3 +188,16 @@ def test_c5_full_size_sampled_apply_and_solve_properties():
     bh, xh = b.cpu().numpy(), xsol.cpu().numpy()
     r_cells = bh.reshape(-1, m3)[cells] - osipg.apply_cells(m, xh, cells)
     assert np.abs(r_cells).max() <= 1e-7 * np.abs(bh).max()
+
+
+@pytest.mark.parametrize("k,cells,bc", [(2, (3, 4, 5), MIXED), (4, (5, 3, 4), MIXED), (6, (3, 2, 2), (DIRICHLET,) * 6)])
+def test_face_geometry_recomputed_on_the_fly_matches_oracle(k, cells, bc, monkeypatch):
+    """FEM_DG_FGEO_FLY=1: the deformed kernel recomputes JxW and J^-1 n at the face points
+    from the analytic map instead of reading the face records (same operator)."""
+    monkeypatch.setenv("FEM_DG_FGEO_FLY", "1")
+    F, m = make(cells, k, 0.05, bc)
+    x = fem_inputs.uniform_pm1(2, m.dg_n_dofs())
+    y = np.zeros_like(x)
+    F.fem_apply(x, y)
+    assert relmax(y, osipg.apply(m, x)) <= 1e-12
+    F.close()

@@ -151,6 +151,9 @@ __device__ constexpr RefTab<K> kRef{};
 // loaded two doubles per LDCU.128 (compile-time literals cost two UMOVs per use)
 template <int K>
 __constant__ RefTab<K> cRef = RefTab<K>();
+#ifndef FEM_ST_SUSPEND_NS
+#define FEM_ST_SUSPEND_NS 100000
+#endif
 #ifndef FEM_ST_CBANK
 #define FEM_ST_CBANK 0
 #endif
@@ -218,6 +221,21 @@ __device__ __forceinline__ double band_row(const double* v, int r, bool both, bo
     for (int j = 0; j <= K; ++j) s = fma(STIFF ? ST_TAB(K).S[r][j] : ST_TAB(K).M[r][j], v[K + j], s);
   }
   return s;
+}
+
+// wait for the phase with the given parity; the suspend-time hint lets the warp sleep in
+// the barrier unit until the phase completes instead of spinning on try_wait (the spin
+// loop cost ~10% of the issue slots of this issue-bound kernel)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(FEM_ST_SUSPEND_NS)
+      : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -475,19 +493,19 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   // plane i from buffer i&1; plane i+NB is copied into the x~ buffer plane i used.
 #pragma unroll
   for (int i = 0; i < NB; ++i) load_plane(i);
-  mbar_wait(landed, 0);
+  mbar_wait_sleep(landed, 0);
   x_stage(0);
   mbar_arrive(full);
   double P[K], Q[K];
   int i = 0;
   auto step = [&]() {
     if (i + 1 < NP) {
-      if (i >= 1) mbar_wait(empty + ((i + 1) & 1), ((i - 1) >> 1) & 1);   // y/z of plane i-1 done
-      mbar_wait(landed + (i + 1) % NB, ((i + 1) / NB) & 1);
+      if (i >= 1) mbar_wait_sleep(empty + ((i + 1) & 1), ((i - 1) >> 1) & 1);   // y/z of plane i-1 done
+      mbar_wait_sleep(landed + (i + 1) % NB, ((i + 1) / NB) & 1);
       x_stage(i + 1);
       mbar_arrive(full + ((i + 1) & 1));
     }
-    mbar_wait(full + (i & 1), (i >> 1) & 1);       // x-stage of plane i done (x~ buffer i % NB free)
+    mbar_wait_sleep(full + (i & 1), (i >> 1) & 1);       // x-stage of plane i done (x~ buffer i % NB free)
     load_plane(i + NB);
     double av[2 * K + 1], bv[2 * K + 1];
     {

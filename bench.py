@@ -231,8 +231,9 @@ def run_reference(args, w):
         "value": value, "unit": "DoF/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(w), "rtol": args.rtol, "sample_cells": list(ws.cells),
-                   "sample_n_dofs": n, "iterations": its},
+        "config": {"workload": workload_desc(w), "n_dofs_global": w.n_dofs(), "cells": list(w.cells),
+                   "rtol": args.rtol, "parallelism": "CPU oracle (numpy, host cores)",
+                   "sample_cells": list(ws.cells), "sample_n_dofs": n, "iterations": its},
         "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cpu_threads(), "kind": "oracle",
                          "sample": f"each step = one full oracle GMG-PCG solve of {what} ({n} DoFs, "
                                    f"{its} iterations, setup untimed); value = sample DoFs / mean step time"},
@@ -402,7 +403,7 @@ def run_ours(args, w):
         "metric": METRIC,
         "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak",
+        "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(w), "n_dofs_global": F.n_global, "n_dofs_local": n,
                    "rtol": args.rtol, "iterations": its, "cells": list(cells),

@@ -27,6 +27,7 @@ METRICS = [
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "smsp__pcsamp_sample_count",
     "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_barrier",
     "smsp__pcsamp_warps_issue_stalled_mio_throttle", "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
@@ -72,11 +73,11 @@ def main():
     tag = sys.argv[1]
     d = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
     res = {}
-    for p in sorted(glob.glob(os.path.join(d, f"{tag}_apply_*.ncu-rep"))):
+    for p in sorted(glob.glob(os.path.join(d, f"{tag}_*.ncu-rep"))):
         res[os.path.basename(p)[len(tag) + 1:-8]] = rep_metrics(p)
-    lp = os.path.join(d, f"{tag}_launches_bench_c2.csv")
-    if os.path.exists(lp):
-        res["bench_C2_launch_shares"] = launch_shares(lp)
+    for lp in sorted(glob.glob(os.path.join(d, f"{tag}_launches_bench_*.csv"))):
+        cfg = os.path.basename(lp)[len(tag) + len("_launches_bench_"):-4].upper()
+        res[f"bench_{cfg}_launch_shares"] = launch_shares(lp)
     os.makedirs("profiles", exist_ok=True)
     with open(os.path.join("profiles", f"{tag}_summary.json"), "w") as f:
         json.dump(res, f, indent=1)

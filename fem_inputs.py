@@ -4,7 +4,7 @@ This module holds NO arithmetic of the method (no basis, quadrature, geometry
 or operator); it only defines the workload presets of BASELINE.json and the
 counter-based random generator both sides draw from (SURVEY.md §8c reading
 R14).  The CUDA path implements the same generator independently (splitmix64
-in `csrc/kernels.cu`) for the random start vector of the eigenvalue estimate
+in `paper_1611_03029_b200/csrc/kernels_mg.cu`, `u01_splitmix`) for the random start vector of the eigenvalue estimate
 (SURVEY.md §8c O6); the oracle uses `uniform_pm1` below.
 
 Generator (R14): x_i = 2 * ((z_i >> 11) * 2^-53) - 1, z_i = splitmix64 output

@@ -192,10 +192,15 @@ FEM_API int fem_info(fem_handle h, int64_t* n_local, int64_t* n_global, int64_t*
  * nx, ny must equal n_local.  x and y must not alias. */
 FEM_API int fem_apply(fem_handle h, const double* x, int64_t nx, double* y, int64_t ny);
 
-/* d = diag(A) on the finest level (1 on constrained CG rows). */
+/* d = diag(A) on the finest level (1 on constrained CG rows): "the matrix diagonal that
+ * is pre-computed and stored" for the Jacobi part of the smoother, the
+ * diagonal of the operator of eq:poisson_fem / eq:poisson_dgsip (cell and face terms). */
 FEM_API int fem_diagonal(fem_handle h, double* d, int64_t nd);
 
-/* z = V(r): one multigrid V-cycle, z overwritten. */
+/* z = V(r): one multigrid V-cycle, z overwritten: Chebyshev-Jacobi pre-smoothing from
+ * zero, residual, restriction, the coarser V-cycle, prolongation, post-smoothing
+ * (P:L1159-1170 smoother, P:L1181-1185 transfer and coarse solve; the V-cycle of
+ * P:L1144-1146's preconditioner).  Linear in r and symmetric. */
 FEM_API int mg_vcycle(fem_handle h, const double* r, int64_t nr, double* z, int64_t nz);
 
 /* Preconditioned CG from the caller's x (pass zeros) until

@@ -37,8 +37,8 @@ struct Tab {
   EO<N> coleo;          // even-odd form of colloc (anti-centro-symmetric)
 };
 
-template <int N>
-inline void make_eo(const double (&M)[kMaxN][kMaxN], EO<N>& t) {
+template <int N, int LD>
+inline void make_eo(const double (&M)[LD][LD], EO<N>& t) {
   constexpr int h = N / 2;
   for (int q = 0; q < N; ++q)
     for (int j = 0; j < N; ++j) {

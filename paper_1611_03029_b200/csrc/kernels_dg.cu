@@ -61,9 +61,15 @@ template <int K>
 struct DgQCPB {
   static constexpr int value = K == 5 ? 2 : (K == 6 ? 1 : (K >= 7 ? FEM_DGQ_C78 : (K == 4 ? FEM_DGQ_C4 : (K == 3 ? FEM_DGQ_C3 : (K == 2 ? FEM_DGQ_C2 : DgCPB<K>::value)))));
 };
+// k = 6 (C5): with the even-odd sweeps the kernel fits 79 registers without spilling;
+// 11 blocks/SM (the shared-memory limit, 20.5 KB per cell) measured 4.75 ms per C5 apply
+// against 5.39 ms at the round-1 bound of 6 blocks (144 registers), 4.91 at 8, 4.81 at 10
+#ifndef FEM_DGQ_MINB6
+#define FEM_DGQ_MINB6 11
+#endif
 template <int K>
 __host__ __device__ constexpr int dgq_minb() {
-  return K == 5 ? 3 : (K == 6 ? 6 : (K >= 7 ? FEM_DG_MINB : (K == 4 ? FEM_DGQ_MINB4 : (K == 3 ? FEM_DGQ_MINB3 : (K == 2 ? FEM_DGQ_MINB2 : 1)))));
+  return K == 5 ? 3 : (K == 6 ? FEM_DGQ_MINB6 : (K >= 7 ? FEM_DG_MINB : (K == 4 ? FEM_DGQ_MINB4 : (K == 3 ? FEM_DGQ_MINB3 : (K == 2 ? FEM_DGQ_MINB2 : 1)))));
 }
 
 #ifndef FEM_DGQ_PAD

@@ -47,7 +47,7 @@ struct DgCPB {
 #define FEM_DGQ_C4 2
 #endif
 #ifndef FEM_DGQ_MINB4
-#define FEM_DGQ_MINB4 6
+#define FEM_DGQ_MINB4 10
 #endif
 #ifndef FEM_DG_MINB
 #define FEM_DG_MINB 4
@@ -67,9 +67,18 @@ struct DgQCPB {
 #ifndef FEM_DGQ_MINB6
 #define FEM_DGQ_MINB6 11
 #endif
+// round 2, after the even-odd register drop (SIPG deformed apply at ~16M DoFs, round-1
+// bound -> new): k = 4 6 -> 10 blocks/SM 949 -> 926 us, k = 5 3 -> 6 832 -> 788 us,
+// k = 7 4 -> 8 886 -> 868 us; k = 8 stays at 4 (8: 798 -> 940 us)
+#ifndef FEM_DGQ_MINB5
+#define FEM_DGQ_MINB5 6
+#endif
+#ifndef FEM_DGQ_MINB7
+#define FEM_DGQ_MINB7 8
+#endif
 template <int K>
 __host__ __device__ constexpr int dgq_minb() {
-  return K == 5 ? 3 : (K == 6 ? FEM_DGQ_MINB6 : (K >= 7 ? FEM_DG_MINB : (K == 4 ? FEM_DGQ_MINB4 : (K == 3 ? FEM_DGQ_MINB3 : (K == 2 ? FEM_DGQ_MINB2 : 1)))));
+  return K == 5 ? FEM_DGQ_MINB5 : (K == 6 ? FEM_DGQ_MINB6 : (K == 7 ? FEM_DGQ_MINB7 : (K == 8 ? FEM_DG_MINB : (K == 4 ? FEM_DGQ_MINB4 : (K == 3 ? FEM_DGQ_MINB3 : (K == 2 ? FEM_DGQ_MINB2 : 1))))));
 }
 
 #ifndef FEM_DGQ_PAD

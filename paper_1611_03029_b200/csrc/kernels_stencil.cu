@@ -598,10 +598,11 @@ void launch_cg_stencil_apply(fem_ctx* h, const Level& L, const double* x, double
   a.x = x;
   a.y = y;
   switch (h->k) {
+    case 1: stencil_k<1, 0>(h, L, a); break;
     case 2: stencil_k<2, 0>(h, L, a); break;
     case 3: stencil_k<3, 0>(h, L, a); break;
     case 4: stencil_k<4, 0>(h, L, a); break;
-    default: throw Error{FEM_E_ARG, "stencil kernel: k in 2..4"};
+    default: throw Error{FEM_E_ARG, "stencil kernel: k in 1..4"};
   }
   if (setc) launch_set_constrained(h, L, x, y);   // boundary rows only
 }
@@ -619,10 +620,11 @@ void launch_cg_stencil_cheb(fem_ctx* h, const Level& L, const double* x, const d
   a.c1 = c1;
   a.c2 = c2;
   switch (h->k) {
+    case 1: stencil_k<1, 1>(h, L, a); break;
     case 2: stencil_k<2, 1>(h, L, a); break;
     case 3: stencil_k<3, 1>(h, L, a); break;
     case 4: stencil_k<4, 1>(h, L, a); break;
-    default: throw Error{FEM_E_ARG, "stencil kernel: k in 2..4"};
+    default: throw Error{FEM_E_ARG, "stencil kernel: k in 1..4"};
   }
 }
 

@@ -51,6 +51,8 @@ def st_env(monkeypatch):
     (3, (11, 9, 4), DIRI, 32),
     (2, (16, 8, 6), MIXED, 5),     # k = 2: 16 x slots per tile
     (2, (17, 9, 2), NEUM, 1),
+    (1, (33, 17, 5), MIXED, 2),    # k = 1: 32 x slots, 8 rows per tile
+    (1, (40, 9, 3), NEUM, 1),
 ])
 def test_stencil2_apply_matches_oracle(k, cells, bc, ez, st_env):
     st_env.setenv("FEM_ST_EZ", str(ez))
@@ -71,7 +73,8 @@ def test_stencil2_apply_matches_oracle(k, cells, bc, ez, st_env):
     F.close()
 
 
-@pytest.mark.parametrize("k,cells,bc", [(4, (16, 8, 8), MIXED), (3, (12, 8, 8), DIRI), (2, (16, 16, 8), MIXED)])
+@pytest.mark.parametrize("k,cells,bc", [(4, (16, 8, 8), MIXED), (3, (12, 8, 8), DIRI), (2, (16, 16, 8), MIXED),
+                                        (1, (32, 16, 16), MIXED)])
 def test_stencil2_fused_chebyshev_and_vcycle(k, cells, bc, st_env):
     st_env.setenv("FEM_ST_EZ", "3")
     m = Mesh(cells, k, bc=bc)

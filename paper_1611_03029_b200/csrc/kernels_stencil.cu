@@ -151,6 +151,15 @@ __device__ constexpr RefTab<K> kRef{};
 // loaded two doubles per LDCU.128 (compile-time literals cost two UMOVs per use)
 template <int K>
 __constant__ RefTab<K> cRef = RefTab<K>();
+// MODE 1 epilogue operands: prefetch.global.L2 per 128-byte line, two z-elements ahead
+// (C4 solve, 5 its: bulk cp.async.bulk.prefetch.L2 one element ahead 141.2 ms, none
+// 132.5, per line one ahead 131.8, two ahead 125.1, three 133.1, four 135.3)
+#ifndef FEM_ST_PF_AHEAD
+#define FEM_ST_PF_AHEAD 2
+#endif
+#ifndef FEM_ST_PF_LINES
+#define FEM_ST_PF_LINES 1
+#endif
 #ifndef FEM_ST_SUSPEND_NS
 #define FEM_ST_SUSPEND_NS 100000
 #endif
@@ -468,10 +477,10 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     }
   };
 
-  // MODE 1: the epilogue reads x, x_old, b, D^-1 of the element's output planes; a burst of
-  // 16 x 4 dependent loads at the element end stalls the warps for a DRAM round trip, so
-  // the warp bulk-prefetches its 4 rows x (K planes) x 4 arrays into L2 when the element
-  // starts (one 256-byte range per lane-task, two per lane).
+  // MODE 1: the epilogue reads x, x_old, b (D^-1 from the class table) of the element's
+  // output planes; a burst of dependent loads at the element end stalls the warps for a
+  // DRAM round trip, so the warp prefetches its 4 rows x (K planes) x the arrays into L2
+  // FEM_ST_PF_AHEAD elements ahead (lanes split the 256-byte row ranges).
   auto prefetch_epilogue = [&](int ez) {
     if constexpr (MODE == 1) {
       if (ez < ez0) return;
@@ -483,7 +492,14 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
         if (gy >= a.NY) continue;
         const double* base = arr == 0 ? a.x : arr == 1 ? a.xo : arr == 2 ? a.b : (a.dcls ? nullptr : a.dinv);
         if (!base) continue;
+#if FEM_ST_PF_LINES
+        {   // per 128-byte line
+          const double* p0 = base + X0 + (int64_t)a.NX * gy + NXY * (K * ez + q);
+          for (int o = 0; o < ncol; o += 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + o));
+        }
+#else
         prefetch_l2_range(base + X0 + (int64_t)a.NX * gy + NXY * (K * ez + q), sizeof(double) * ncol);
+#endif
       }
     }
   };
@@ -523,9 +539,9 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   };
   step();
   accumulate(0, P, Q);
-  prefetch_epilogue(ez0);
+  for (int d = 0; d < FEM_ST_PF_AHEAD; ++d) prefetch_epilogue(ez0 + d);
   for (int ez = ezs; ez < ez1; ++ez) {
-    if (ez + 1 < ez1) prefetch_epilogue(ez + 1);   // one element ahead
+    if (ez + FEM_ST_PF_AHEAD < ez1) prefetch_epilogue(ez + FEM_ST_PF_AHEAD);   // elements ahead
 #pragma unroll
     for (int rp = 1; rp <= K; ++rp) {
       step();

@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rtol", type=float, default=1e-10)
+    ap.add_argument("--others", default="C2,C3,C5",
+                    help="single GPU: also time these configs' solves and applies (extra key other_configs)")
     return ap.parse_args()
 
 
@@ -82,9 +84,14 @@ def workload_desc(w):
 
 def algorithmic_apply_bytes(w, n_dofs):
     """read x once + write y once (16 B/DoF) plus the streamed geometry
-    table on deformed meshes (6 doubles per quadrature point per cell)."""
+    table on deformed meshes (6 doubles per quadrature point per cell) and, for SIPG on
+    deformed meshes, the face records (7 doubles per face quadrature point)."""
     n_cells = int(np.prod(w.cells))
     geo = 48 * (w.degree + 1) ** 3 * n_cells if w.deform_eps else 0
+    if w.deform_eps and w.method == fem_inputs.SIPG:
+        nx, ny, nz = w.cells
+        n_faces = (nx + 1) * ny * nz + nx * (ny + 1) * nz + nx * ny * (nz + 1)
+        geo += 56 * (w.degree + 1) ** 2 * n_faces
     return 16 * n_dofs + geo
 
 
@@ -267,6 +274,65 @@ def apply_flops_per_dof(w):
     return None
 
 
+# ---------------------------------------------------------------- other configs
+def other_configs(names, rtol, reps=5):
+    """BASELINE.json's other solve configs measured in the same run (single GPU): time to
+    solution (median of `reps` solves from x = 0, CUDA events, L2 flushed between them),
+    iterations, and the finest-level apply (20 back to back between two events; the
+    algorithmic bytes of algorithmic_apply_bytes)."""
+    import torch
+    from paper_1611_03029_b200 import fem
+    hbm, _ = peaks()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    out = {}
+    for name in names:
+        w = fem_inputs.CONFIGS[name]
+        t0 = time.perf_counter()
+        F = fem.Fem(w.cells, w.degree, w.method, deform_eps=w.deform_eps, bc=w.bc,
+                    penalty_factor=w.penalty_factor)
+        torch.cuda.synchronize()
+        setup = time.perf_counter() - t0
+        n = F.n_local
+        b = torch.zeros(n, dtype=torch.float64, device="cuda")
+        F.fem_rhs(b)
+        x = torch.zeros_like(b)
+        F.cg_solve(b, x, rtol=rtol)
+        ts, its = [], 0
+        for i in range(reps):
+            flush.fill_(float(i))
+            x.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            its, rr, ok = F.cg_solve(b, x, rtol=rtol)
+            e.record()
+            torch.cuda.synchronize()
+            assert ok and rr <= rtol
+            ts.append(s.elapsed_time(e))
+        xa = torch.from_numpy(fem_inputs.uniform_pm1(w.seed, n)).cuda()
+        ya = torch.empty_like(xa)
+        F.fem_apply(xa, ya)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(20):
+            F.fem_apply(xa, ya)
+        e.record()
+        torch.cuda.synchronize()
+        t_apply = s.elapsed_time(e) * 1e-3 / 20
+        t_solve = statistics.median(ts) * 1e-3
+        n_cells = int(np.prod(w.cells))
+        out[name] = {"workload": workload_desc(w), "n_dofs": n, "iterations": its,
+                     "time_to_solution_ms": t_solve * 1e3, "dofs_per_s": n / t_solve,
+                     "apply_us": t_apply * 1e6, "apply_dofs_per_s": n / t_apply,
+                     "apply_equivalent_dofs_per_s": n_cells * w.degree ** 3 / t_apply,
+                     "apply_hbm_frac": algorithmic_apply_bytes(w, n) / t_apply / 1e9 / hbm,
+                     "setup_s": round(setup, 3), "solve_ms_samples": [round(t, 4) for t in ts]}
+        F.close()
+        del b, x, xa, ya
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args, w):
     import torch
@@ -436,12 +502,16 @@ def run_ours(args, w):
                                     "frac": fl / avg_apply_s / 1e12 / FP64_PEAK_TFLOPS,
                                     "peak_source": "profiles/fp64_peak.json (measured DFMA chains)"}
         line["apply"]["fp64_frac"] = fpd * F.n_global / apply_s / 1e12 / FP64_PEAK_TFLOPS
+    F.close()
+    if world == 1 and args.others:
+        del b, x, flush
+        torch.cuda.empty_cache()
+        line["other_configs"] = other_configs([c for c in args.others.split(",") if c != w.name], args.rtol)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(w, args.rtol)
         line["cpu_baseline"].pop("seconds", None)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    F.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

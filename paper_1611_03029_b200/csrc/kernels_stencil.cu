@@ -339,12 +339,19 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     const bool zm = ((bm & 16) && gz == 0) || ((bm & 32) && gz == a.NZ - 1);
     const double* src = a.x + (int64_t)gz * NXY;
     double* dst = Xt + (i % NB) * LR * LP;
+    const uint32_t ok = zm ? 0u : ld_ok;   // source sizes of this plane's copies: 8 or 0 bytes
 #pragma unroll
     for (int j = 0; j < C::NLD; ++j) {
       const int idx = tid + j * C::THREADS;
       if (idx < LR * LC) {
         const int so = LP == LC ? idx : (idx / LC) * LP + idx % LC;
-        st_cp_async8(dst + so, src + ld_off[j], !zm && ((ld_ok >> j) & 1u));
+        if constexpr (MODE == 0) {   // source size 8 or 0 straight from the mask bit
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + so)),
+                       "l"(src + ld_off[j]), "r"(((ok >> j) & 1u) << 3)
+                       : "memory");
+        } else {   // (MODE 1: this form measured better, the register allocation differs)
+          st_cp_async8(dst + so, src + ld_off[j], !zm && ((ld_ok >> j) & 1u));
+        }
       }
     }
     mbar_arrive_cp_async(landed + i % NB);
@@ -359,6 +366,17 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   const int nitems = LR * nsl;
   const double rx = a.c0 / a.cy, rz = a.cz / a.cy;   // metric folded: y = c_y (M_z Q + r_z S_z P)
   static_assert(C::LR * C::SX <= 2 * C::THREADS, "x-stage items per thread");
+  // the thread's (at most two) items, loop-invariant: shared-memory read and write
+  // offsets packed into one word each (both < 2^16), the boundary halving in bit 31
+  // (MODE 0 only: in MODE 1 the two extra registers made the epilogue spill)
+  uint32_t xit[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int it = tid + u * C::THREADS;
+    const int row = it % LR, sl = it / LR;
+    const bool edge = e0 + sl == 0 || e0 + sl == a.nx;
+    xit[u] = (uint32_t)(row * LP + sl * K) | ((uint32_t)(row * ABP + sl * K) << 16) | (edge ? 0x80000000u : 0u);
+  }
   auto x_stage = [&](int i) {
     const double* xb = Xt + (i % NB) * LR * LP;
     double* Ab = AB + (i & 1) * 2 * LR * ABP;
@@ -366,14 +384,25 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     for (int u = 0; u < 2; ++u) {
       const int it = tid + u * C::THREADS;
       if (it >= nitems) break;
-      const int row = it % LR, sl = it / LR;
-      const double* v = xb + row * LP + sl * K;   // loaded column of node K (e-1)
+      const double* v;
+      double* ao;
+      bool edge;
+      if constexpr (MODE == 0) {
+        v = xb + (xit[u] & 0xffffu);
+        ao = Ab + ((xit[u] >> 16) & 0x7fffu);
+        edge = xit[u] >> 31;
+      } else {
+        const int row = it % LR, sl = it / LR;
+        v = xb + row * LP + sl * K;
+        ao = Ab + row * ABP + sl * K;
+        edge = e0 + sl == 0 || e0 + sl == a.nx;
+      }
+      // v: loaded column of node K (e-1)
       double w[2 * K + 1];
 #pragma unroll
       for (int j = 0; j <= 2 * K; ++j) w[j] = v[j];
       const double wk = w[K];
-      w[K] = (e0 + sl == 0 || e0 + sl == a.nx) ? 0.5 * wk : wk;
-      double* ao = Ab + row * ABP + sl * K;
+      w[K] = edge ? 0.5 * wk : wk;
       double* bo = ao + LR * ABP;
       ao[0] = band_row<K, false>(w, 0, true, false);
       bo[0] = ISO ? band_row<K, true>(w, 0, true, false) : rx * band_row<K, true>(w, 0, true, false);

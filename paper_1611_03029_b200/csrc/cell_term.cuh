@@ -14,6 +14,24 @@
 
 namespace fem {
 
+// Analytic geometry of the deformed box (reading R2) at the thread's z-line of quadrature
+// points: x = xhat + eps s(xhat) (1,1,1), s = prod_d sin(pi t_d).  With g = grad s,
+// fac = 1 + eps sum g, beta = eps / fac, J^-1 = diag(2/h) (I - beta 1 g^T), the metric is
+//   G_ab = w det J (4 / (h_a h_b)) (delta_ab - beta (g_a + g_b) + beta^2 |g|^2),
+// det J = fac prod(h/2) -- the geometry_kernel formula, evaluated in the q-point phase
+// instead of read from the 48-byte-per-point table.
+struct GeoFlyC {             // level constants (kernel parameter)
+  double pl[3];              // pi / L_d
+  double eps, hh;            // eps, prod(h/2)
+  double ih[6];              // 4 / (h_a h_b) for (00, 01, 02, 11, 12, 22)
+};
+template <int N>
+struct GeoFlyPt {
+  double sx, cx, sy, cy;     // sin / cos (pi t) of the thread's x and y quadrature coordinates
+  const double* scz;         // shared: sin (pi t_z) at [0, N), cos at [N, 2N) of the cell's z points
+  const GeoFlyC* c;
+};
+
 template <int N>
 struct CellGeo {
   const double* G;  // deformed: &G[cell][0][0] of layout [6][N^3] (global or shared)
@@ -22,6 +40,7 @@ struct CellGeo {
   uint64_t* bar;    // if set: mbarrier of a bulk copy that fills G, waited on before the q-point phase
   int gq = 1;       // G stride between quadrature points ([cell][comp][q]: 1)
   int gc = N * N * N;  // G stride between components
+  const GeoFlyPt<N>* fly = nullptr;   // analytic geometry instead of G (FLY kernels)
 };
 
 // RT_STRIDES: G strides from geo.gq / geo.gc (the Q4 line kernel's 8-cell block order);
@@ -80,7 +99,23 @@ __device__ __forceinline__ void cell_laplace(const Tab<N>& T, const CellGeo<N>& 
     double fx, fy, fz;
     if (DEFORMED) {
       double G00 = 0, G01 = 0, G02 = 0, G11 = 0, G12 = 0, G22 = 0;
-      if (geo.active) {
+      if (geo.fly) {
+        const GeoFlyPt<N>& f = *geo.fly;
+        const GeoFlyC& k = *f.c;
+        const double szl = f.scz[l], czl = f.scz[N + l];
+        const double g0 = k.pl[0] * f.cx * f.sy * szl, g1 = k.pl[1] * f.sx * f.cy * szl,
+                     g2 = k.pl[2] * f.sx * f.sy * czl;
+        const double fac = 1.0 + k.eps * (g0 + g1 + g2);
+        const double beta = k.eps / fac;
+        const double W = T.w[ta] * T.w[tb] * T.w[l] * fac * k.hh;
+        const double bb = beta * beta * (g0 * g0 + g1 * g1 + g2 * g2);
+        G00 = W * k.ih[0] * (1.0 - 2.0 * beta * g0 + bb);
+        G01 = W * k.ih[1] * (bb - beta * (g0 + g1));
+        G02 = W * k.ih[2] * (bb - beta * (g0 + g2));
+        G11 = W * k.ih[3] * (1.0 - 2.0 * beta * g1 + bb);
+        G12 = W * k.ih[4] * (bb - beta * (g1 + g2));
+        G22 = W * k.ih[5] * (1.0 - 2.0 * beta * g2 + bb);
+      } else if (geo.active) {
         const int gq = RT_STRIDES ? geo.gq : 1, gc = RT_STRIDES ? geo.gc : N3;
         const double* Gc = geo.G + q * gq;
         G00 = Gc[0];

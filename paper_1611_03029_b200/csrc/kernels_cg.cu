@@ -136,8 +136,16 @@ __host__ __device__ constexpr int line_minb() {
 // instead of apply + cheb_step (single-rank levels).
 // (The fused variant is its own __global__ with the CgFuse block as an extra parameter:
 // growing OpArgs itself slowed the plain kernel by 9%, C2 apply 66.6 -> 72.6 us.)
-template <int K, bool DEFORMED, bool FUSED>
-__device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>& T, const CgFuse& f) {
+// analytic map of the deformed box for the FLY kernel (reading R2; not the N3 geometries)
+struct GeoFly {
+  double lo[3], L[3], h[3];
+  int cz0;   // global z offset (cells) of the level's local layer 0
+  GeoFlyC c;
+};
+
+template <int K, bool DEFORMED, bool FUSED, bool FLY = false>
+__device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>& T, const CgFuse& f,
+                                              const GeoFly* gfly = nullptr) {
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
   constexpr int C = CPB<K>::value;
   extern __shared__ double smem[];
@@ -212,7 +220,21 @@ __device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>&
   // sweep phases run, and the q-point phase reads G from shared memory.
   const double* Gs = nullptr;
   __shared__ alignas(8) uint64_t gbar;
-  if (DEFORMED && a.g_direct) {
+  GeoFlyPt<N> fp;
+  __shared__ double scz[FLY ? C : 1][FLY ? 2 * N : 1];
+  if constexpr (FLY) {
+    // sin / cos (pi t) of the quadrature coordinates: the thread's x and y in registers, the
+    // cell's z points in shared memory (computed by N of its threads; the q-point phase
+    // comes after several barriers of the sweeps)
+    const GeoFly& m = *gfly;
+    const int c3[3] = {cx, cy, cz + m.cz0};
+    auto tq = [&](int d, int q) { return m.h[d] * (c3[d] + 0.5 * (T.qp[q] + 1.0)) / m.L[d]; };
+    sincospi(tq(0, ta), &fp.sx, &fp.cx);
+    sincospi(tq(1, tb), &fp.sy, &fp.cy);
+    if (real && t < N) sincospi(tq(2, t), &scz[ci][t], &scz[ci][N + t]);
+    fp.scz = scz[ci];
+    fp.c = &m.c;
+  } else if (DEFORMED && a.g_direct) {
     // G read straight from global memory in the q-point phase (each warp load is 256
     // contiguous bytes: q = t + N^2 l); the block's slice is bulk-prefetched into L2 now
     const int64_t c0 = a.cell0 + (int64_t)blockIdx.x * C;
@@ -243,7 +265,8 @@ __device__ __forceinline__ void cg_apply_body(const OpArgs& a, const Tab<K + 1>&
     __syncthreads();       // barrier initialisation visible to all threads
     Gs = c8 ? sG + ci : sG + ci * 6 * N3;
   }
-  CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, (DEFORMED && !a.g_direct) ? &gbar : nullptr};
+  CellGeo<N> geo{Gs, a.c0, a.c1, a.c2, active, (DEFORMED && !FLY && !a.g_direct) ? &gbar : nullptr};
+  if constexpr (FLY) geo.fly = &fp;
   if constexpr (line_cell_fast<K>()) {
     if (DEFORMED && a.glayout == kGLayoutCell8) {
       geo.gq = kCell8;
@@ -267,6 +290,15 @@ __global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
     cg_apply_kernel(OpArgs a, Tab<K + 1> T) {
   FEM_PDL_ENTRY();
   cg_apply_body<K, DEFORMED, false>(a, T, CgFuse{});
+}
+
+// deformed CG with the metric recomputed from the analytic map at every quadrature point
+// (no G traffic: C2's apply moves 16 instead of 108 bytes per DoF)
+template <int K>
+__global__ void __launch_bounds__(line_tpc<K>() * CPB<K>::value, line_minb<K>())
+    cg_apply_fly_kernel(OpArgs a, Tab<K + 1> T, GeoFly g) {
+  FEM_PDL_ENTRY();
+  cg_apply_body<K, true, false, true>(a, T, CgFuse{}, &g);
 }
 
 template <int K>
@@ -1403,6 +1435,22 @@ void apply_k(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0,
     const size_t sm = sizeof(double) * (line_g_offset<N, C>() + (a.g_direct ? 0 : 6 * N * N * N * C));
     smem_attr(reinterpret_cast<const void*>(cg_apply_fused_kernel<K>), (size_t)((int)(sizeof(double) * (line_g_offset<N, C>() + 6 * N * N * N * C))));
     launch_pdl(h, cg_apply_fused_kernel<K>, (unsigned)grid, lblock, sm, a, T, h->cgf);
+  } else if (h->cg_geo_fly && !mesh_general(h->mesh)) {
+    GeoFly g;
+    for (int d = 0; d < 3; ++d) {
+      g.lo[d] = h->mesh.lo[d];
+      g.L[d] = h->mesh.hi[d] - h->mesh.lo[d];
+      g.h[d] = L.h[d];
+      g.c.pl[d] = M_PI / g.L[d];
+    }
+    g.cz0 = L.cz0;
+    g.c.eps = h->mesh.deform_eps;
+    g.c.hh = (0.5 * L.h[0]) * (0.5 * L.h[1]) * (0.5 * L.h[2]);
+    const int ab[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+    for (int c = 0; c < 6; ++c) g.c.ih[c] = 4.0 / (L.h[ab[c][0]] * L.h[ab[c][1]]);
+    const size_t sm = sizeof(double) * line_g_offset<N, C>();
+    smem_attr(reinterpret_cast<const void*>(cg_apply_fly_kernel<K>), sm);
+    launch_pdl(h, cg_apply_fly_kernel<K>, (unsigned)grid, lblock, sm, a, T, g);
   } else {
     const size_t sm = sizeof(double) * (line_g_offset<N, C>() + (a.g_direct ? 0 : 6 * N * N * N * C));
     smem_attr(reinterpret_cast<const void*>(cg_apply_kernel<K, true>), (size_t)((int)(sizeof(double) * (line_g_offset<N, C>() + 6 * N * N * N * C))));

@@ -322,3 +322,16 @@ def test_layout_and_fusion_switches_keep_parity(env, val, monkeypatch):
     assert ok and abs(its - its_o) <= 1
     assert np.linalg.norm(b - mg.fine.apply(xs)) / np.linalg.norm(b) <= 1e-9
     F.close()
+
+
+@pytest.mark.parametrize("k,cells", [(2, (5, 3, 4)), (4, (6, 4, 3)), (7, (2, 2, 2))])
+def test_metric_recomputed_on_the_fly_matches_oracle(k, cells, monkeypatch):
+    """FEM_CG_GEO_FLY=1: the deformed line kernel evaluates G_q from the analytic map in its
+    q-point phase instead of reading the table (same operator)."""
+    monkeypatch.setenv("FEM_CG_GEO_FLY", "1")
+    F, m = make(cells, k, 0.05, MIXED)
+    x = fem_inputs.uniform_pm1(6, m.cg_n_dofs())
+    y = np.zeros_like(x)
+    F.fem_apply(x, y)
+    assert relmax(y, ocg.apply(m, x)) <= 1e-12
+    F.close()

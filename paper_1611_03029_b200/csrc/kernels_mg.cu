@@ -263,6 +263,52 @@ __global__ void prolongate_elem_kernel(TransferArgs a, Embed<K, DG> E, const dou
     s_in[i] = v;
   }
   __syncthreads();
+  if constexpr (!DG) {
+    // CG: one row of the embedding matrix per thread in registers (fixed fine index along
+    // the sweep direction): one shared-memory load per FMA instead of two
+    constexpr int TPR = kTransferThreads / M;
+    const int ri = threadIdx.x / TPR, rj = threadIdx.x % TPR;
+    const bool act = ri < M;
+    double e[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) e[i] = act ? sE[ri][i] : 0.0;
+    if (act) {   // x: s_1[r + M jl], r = ri
+      for (int jl = rj; jl < N * N; jl += TPR) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) s = fma(e[i], s_in[i + N * jl], s);
+        s_1[ri + M * jl] = s;
+      }
+    }
+    __syncthreads();
+    if (act) {   // y: s_2[r + M (sidx + M l)], sidx = ri
+      for (int it = rj; it < M * N; it += TPR) {
+        const int r = it % M, l = it / M;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) s = fma(e[j], s_1[r + M * (j + N * l)], s);
+        s_2[r + M * (ri + M * l)] = s;
+      }
+    }
+    __syncthreads();
+    if (act) {   // z + write: fine node (r, sidx, tt), tt = ri
+      const int tt = ri;
+      for (int it = rj; it < M * M; it += TPR) {
+        const int r = it % M, sidx = it / M;
+        double s = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) s = fma(e[l], s_2[r + M * (sidx + M * l)], s);
+        // owned: local fine index < 2K unless this is the last coarse cell
+        if ((r == 2 * K && cx != a.nc0 - 1) || (sidx == 2 * K && cy != a.nc1 - 1) ||
+            (tt == 2 * K && a.czc0 + cz != a.ncz - 1))
+          continue;
+        const int gx = 2 * K * cx + r, gy = 2 * K * cy + sidx, gz = 2 * K * cz + tt;
+        if (cg_constrained(a.bcmask, gx, gy, 2 * K * a.czc0 + gz, a.nnf0, a.nnf1, a.nnf2)) continue;
+        xf[cg_index(gx, gy, gz, a.nnf0, a.nnf1)] += s;
+      }
+    }
+    return;
+  }
   for (int o = threadIdx.x; o < M * N * N; o += blockDim.x) {  // x sweep: [l][j][r]
     const int r = o % M, jl = o / M;
     double s = 0.0;
@@ -363,6 +409,49 @@ __global__ void restrict_elem_kernel(TransferArgs a, Embed<K, DG> E, const doubl
     s_in[r + M * (sidx + M * tt)] = v;
   }
   __syncthreads();
+  if constexpr (!DG) {
+    // CG: each thread keeps one column of the embedding matrix in registers (the output's
+    // coarse index along the sweep direction is fixed per thread), so a sweep costs one
+    // shared-memory load per FMA instead of two (the transfer was issue-bound, ncu r02:
+    // 80% issue-active, 2 LDS per DFMA)
+    constexpr int TPC = kTransferThreads / N;   // threads per coarse index
+    const int ci = threadIdx.x / TPC, cj = threadIdx.x % TPC;
+    const bool act = ci < N;
+    double e[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) e[r] = act ? sE[r][ci] : 0.0;
+    if (act) {   // x: s_1[st N + i], i = ci
+      for (int st = cj; st < M * M; st += TPC) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < M; ++r) s = fma(e[r], s_in[r + M * st], s);
+        s_1[st * N + ci] = s;
+      }
+    }
+    __syncthreads();
+    if (act) {   // y: s_2[i + N (j + N tt)], j = ci
+      for (int it = cj; it < N * M; it += TPC) {
+        const int i = it % N, tt = it / N;
+        double s = 0.0;
+#pragma unroll
+        for (int sidx = 0; sidx < M; ++sidx) s = fma(e[sidx], s_1[i + N * (sidx + M * tt)], s);
+        s_2[i + N * (ci + N * tt)] = s;
+      }
+    }
+    __syncthreads();
+    if (act) {   // z: (i, j, l), l = ci
+      for (int it = cj; it < N * N; it += TPC) {
+        const int i = it % N, j = it / N;
+        double s = 0.0;
+#pragma unroll
+        for (int tt = 0; tt < M; ++tt) s = fma(e[tt], s_2[i + N * (j + N * tt)], s);
+        const int gx = K * cx + i, gy = K * cy + j, gz = K * cz + ci;
+        if (!cg_constrained(a.bcmask, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2))
+          atomicAdd(xc + cg_index(gx, gy, gz, a.nnc0, a.nnc1), s);
+      }
+    }
+    return;
+  }
   for (int o = threadIdx.x; o < N * M * M; o += blockDim.x) {  // x: [t][s][i]
     const int i = o % N, st = o / N;
     double s = 0.0;
@@ -384,13 +473,7 @@ __global__ void restrict_elem_kernel(TransferArgs a, Embed<K, DG> E, const doubl
     double s = 0.0;
 #pragma unroll
     for (int tt = 0; tt < M; ++tt) s = fma(sE[tt][l], s_2[i + N * (j + N * tt)], s);
-    if (DG) {
-      xc[cell * N * N * N + o] = s;
-    } else {
-      const int gx = K * cx + i, gy = K * cy + j, gz = K * cz + l;
-      if (!cg_constrained(a.bcmask, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2))
-        atomicAdd(xc + cg_index(gx, gy, gz, a.nnc0, a.nnc1), s);
-    }
+    xc[cell * N * N * N + o] = s;
   }
 }
 

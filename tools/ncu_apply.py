@@ -21,9 +21,14 @@ x = torch.from_numpy(fem_inputs.uniform_pm1(w.seed, F.n_local)).cuda()
 y = torch.zeros_like(x)
 F.fem_apply(x, y)
 torch.cuda.synchronize()
+smooth = os.environ.get("NCU_SMOOTH") == "1"   # finest-level smoother instead (fused Chebyshev)
+xs = torch.zeros_like(x)
 torch.cuda.cudart().cudaProfilerStart()
 for _ in range(reps):
-    F.fem_apply(x, y)
+    if smooth:
+        F.mg_smooth(F.n_levels - 1, y, xs, False)
+    else:
+        F.fem_apply(x, y)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()
 print(f"{w.name}: {reps} applies ok, |y|_max = {y.abs().max().item():.6e}")

@@ -35,6 +35,13 @@ def run(w, solve=True):
     n_cells = np.prod(w.cells)
     print(f"{w.name}: n={n} setup={setup:.2f}s apply={ms*1e3:.1f}us  {n/ms/1e6:.2f} GDoF/s "
           f"(equiv {n_cells*w.degree**3/ms/1e6:.2f})", flush=True)
+    if __import__("os").environ.get("PROBE_SMOOTH") == "1":   # finest-level smoother (fused Chebyshev launches)
+        L = F.n_levels - 1
+        b = torch.zeros_like(x)
+        F.fem_apply(x, b)
+        xs = torch.zeros_like(x)
+        ms_s = timeit(lambda: F.mg_smooth(L, b, xs, False), reps=10)
+        print(f"   smooth (5 steps from x != 0): {ms_s*1e3:.1f}us = {ms_s*1e3/5:.1f}us per step", flush=True)
     if solve:
         b = torch.zeros_like(x)
         F.fem_rhs(b) if w.rhs == "manufactured" else F.fem_apply(x, b)

@@ -45,7 +45,31 @@
 
 namespace fem {
 
-template <int K>
+// Pipeline depths per MODE (r02c A/B on C4, apply / smoother step): A/B planes in flight
+// (x-stage -> y-stage hand-off) 2 (3: 766 vs 754 us apply, 2044 vs 1706 us smoother);
+// x~ planes in flight 3 (4: 754 -> 748 us apply; smoother 1706 -> 1667 us with one element
+// of L2 prefetch; 2: 1863 us).  The LR * SX - THREADS extra x-stage items of a plane
+// rotate over the warps with the plane (FEM_ST_ROT; fixed on warps 0-1: 766 vs 754 us):
+// every plane's EMPTY / FULL hand-off otherwise waited on the same two slow warps.
+// Tried and dropped (MODE 1): parking an element's planes 1..K-1 in a 24 KB shared stash
+// and writing one plane per following step (2023 us; with the operands loaded one step
+// early 2517 us, spills) -- extra shared memory costs this kernel more than the burst.
+#ifndef FEM_ST_NAB0
+#define FEM_ST_NAB0 2
+#endif
+#ifndef FEM_ST_NAB1
+#define FEM_ST_NAB1 2
+#endif
+#ifndef FEM_ST_NB0
+#define FEM_ST_NB0 3
+#endif
+#ifndef FEM_ST_NB1
+#define FEM_ST_NB1 3
+#endif
+#ifndef FEM_ST_ROT
+#define FEM_ST_ROT 1
+#endif
+template <int K, int MODE = 0>
 struct StCfg {
   static constexpr int N = K + 1;
   static constexpr int SX = 32 / K;               // x slots per tile (<= 32 output columns)
@@ -56,9 +80,11 @@ struct StCfg {
   static constexpr int LP = LC | 1;               // odd row strides: conflict-free column walks
   static constexpr int ABP = TX | 1;
   static constexpr int THREADS = 32 * SY;         // thread = (output column, y slot)
-  static constexpr int NB = 4;                    // x~ planes in flight
+  static constexpr int NB = MODE == 0 ? FEM_ST_NB0 : FEM_ST_NB1;   // x~ planes in flight
   static constexpr int NLD = (LR * LC + THREADS - 1) / THREADS;
-  static constexpr int SMEM = NB * LR * LP + 2 * 2 * LR * ABP + 4 + NB + 8;   // doubles (+ mbarriers)
+  static constexpr int NAB = MODE == 0 ? FEM_ST_NAB0 : FEM_ST_NAB1;
+  static constexpr int NBAR = 2 * NAB + NB;
+  static constexpr int SMEM = NB * LR * LP + NAB * 2 * LR * ABP + NBAR + 8;   // doubles (+ mbarriers)
   // two blocks per SM: 16 warps, 4 per SM sub-partition (16K registers each)
   static constexpr int MAXREG = 128;
 };
@@ -151,11 +177,12 @@ __device__ constexpr RefTab<K> kRef{};
 // loaded two doubles per LDCU.128 (compile-time literals cost two UMOVs per use)
 template <int K>
 __constant__ RefTab<K> cRef = RefTab<K>();
-// MODE 1 epilogue operands: prefetch.global.L2 per 128-byte line, two z-elements ahead
-// (C4 solve, 5 its: bulk cp.async.bulk.prefetch.L2 one element ahead 141.2 ms, none
-// 132.5, per line one ahead 131.8, two ahead 125.1, three 133.1, four 135.3)
+// MODE 1 epilogue operands: prefetch.global.L2 per 128-byte line, one z-element ahead
+// (C4 solve, 5 its, NB 4: bulk cp.async.bulk.prefetch.L2 one element ahead 141.2 ms, none
+// 132.5, per line one ahead 131.8, two ahead 125.1, three 133.1, four 135.3; with NB 3:
+// one ahead 122.2 ms, two ahead 124.4)
 #ifndef FEM_ST_PF_AHEAD
-#define FEM_ST_PF_AHEAD 2
+#define FEM_ST_PF_AHEAD 1
 #endif
 #ifndef FEM_ST_PF_LINES
 #define FEM_ST_PF_LINES 1
@@ -259,15 +286,16 @@ template <int K, int MODE, bool ISO>
 __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXREG)
     cg_stencil2_kernel(StArgs a) {
   FEM_PDL_ENTRY();
-  using C = StCfg<K>;
+  using C = StCfg<K, MODE>;
   constexpr int N = K + 1, SX = C::SX, LR = C::LR, LC = C::LC, LP = C::LP, ABP = C::ABP, NB = C::NB;
+  constexpr int NAB = C::NAB;
   extern __shared__ double smem[];
   double* Xt = smem;                           // [NB][LR][LP]
   double* AB = smem + NB * LR * LP;            // [2 buffers][A, B][LR][ABP]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(AB + 2 * 2 * LR * ABP);
-  uint64_t* full = bars;                       // [2]  A/B buffer written by every thread
-  uint64_t* empty = bars + 2;                  // [2]  A/B buffer read by every thread
-  uint64_t* landed = bars + 4;                 // [NB] x~ plane copies of every thread landed
+  uint64_t* bars = reinterpret_cast<uint64_t*>(AB + NAB * 2 * LR * ABP);
+  uint64_t* full = bars;                       // [NAB] A/B buffer written by every thread
+  uint64_t* empty = bars + NAB;                // [NAB] A/B buffer read by every thread
+  uint64_t* landed = bars + 2 * NAB;           // [NB]  x~ plane copies of every thread landed
   const int tid = threadIdx.x;
   const int e0 = blockIdx.x * SX, f0 = blockIdx.y * C::SY;
   const int X0 = K * e0, Y0 = K * f0;
@@ -315,7 +343,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     return;
   }
   if (tid == 0) {
-    for (int b = 0; b < 4 + NB; ++b) mbar_init(bars + b, C::THREADS);
+    for (int b = 0; b < C::NBAR; ++b) mbar_init(bars + b, C::THREADS);
   }
   __syncthreads();
 
@@ -379,15 +407,17 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   }
   auto x_stage = [&](int i) {
     const double* xb = Xt + (i % NB) * LR * LP;
-    double* Ab = AB + (i & 1) * 2 * LR * ABP;
+    double* Ab = AB + (i % NAB) * 2 * LR * ABP;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const int it = tid + u * C::THREADS;
+      // the LR * SX - THREADS extra items of a plane go to two warps that rotate with the
+      // plane (FEM_ST_ROT), so that no warp is the slow one on every plane
+      const int it = u == 0 ? tid : C::THREADS + (FEM_ST_ROT ? ((tid - 64 * (i & 3)) & (C::THREADS - 1)) : tid);
       if (it >= nitems) break;
       const double* v;
       double* ao;
       bool edge;
-      if constexpr (MODE == 0) {
+      if (MODE == 0 && u == 0) {
         v = xb + (xit[u] & 0xffffu);
         ao = Ab + ((xit[u] >> 16) & 0x7fffu);
         edge = xit[u] >> 31;
@@ -545,16 +575,17 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   int i = 0;
   auto step = [&]() {
     if (i + 1 < NP) {
-      if (i >= 1) mbar_wait_sleep(empty + ((i + 1) & 1), ((i - 1) >> 1) & 1);   // y/z of plane i-1 done
+      if (i + 1 >= NAB)   // y/z stages of plane i + 1 - NAB done
+        mbar_wait_sleep(empty + (i + 1) % NAB, ((i + 1) / NAB - 1) & 1);
       mbar_wait_sleep(landed + (i + 1) % NB, ((i + 1) / NB) & 1);
       x_stage(i + 1);
-      mbar_arrive(full + ((i + 1) & 1));
+      mbar_arrive(full + (i + 1) % NAB);
     }
-    mbar_wait_sleep(full + (i & 1), (i >> 1) & 1);       // x-stage of plane i done (x~ buffer i % NB free)
+    mbar_wait_sleep(full + i % NAB, (i / NAB) & 1);       // x-stage of plane i done (x~ buffer i % NB free)
     load_plane(i + NB);
     double av[2 * K + 1], bv[2 * K + 1];
     {
-      const double* Ab = AB + (i & 1) * 2 * LR * ABP + (K * s) * ABP + c;
+      const double* Ab = AB + (i % NAB) * 2 * LR * ABP + (K * s) * ABP + c;
       const double* Bb = Ab + LR * ABP;
 #pragma unroll
       for (int j = 0; j <= 2 * K; ++j) {
@@ -562,7 +593,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
         bv[j] = Bb[j * ABP];
       }
     }
-    mbar_arrive(empty + (i & 1));
+    mbar_arrive(empty + i % NAB);
     y_stage(av, bv, P, Q);
     ++i;
   };
@@ -601,7 +632,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
 // ---------------------------------------------------------------- launcher
 template <int K, int MODE>
 void stencil_k(fem_ctx* h, const Level& L, const StArgs& a0) {
-  using C = StCfg<K>;
+  using C = StCfg<K, MODE>;
   StArgs a = a0;
   a.nx = L.n[0];
   a.ny = L.n[1];

@@ -17,6 +17,9 @@ with no sum factorization:
 * `transfer`   nodal-interpolation prolongation P and restriction P^T
 * `multigrid`  Chebyshev-Jacobi smoother, lambda_max estimate, V-cycle, PCG
 * `problem`    manufactured right-hand side and L2 error
+* `hdg`        HDG: quadrature-built local matrices, the statically
+               condensed trace operator K and its right-hand side (eq:hdg_matrix_condensed),
+               local recovery, the mixed (flux-substituted) operator, Jacobi-PCG
 
 Parity status of every function is listed in DESIGN.md ("Oracle pins").
 """

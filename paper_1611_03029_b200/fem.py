@@ -90,6 +90,16 @@ def _load():
         "fem_profile_read": (C.c_int, [P, C.POINTER(D), C.POINTER(I64), I32]),
         "fem_last_error": (C.c_char_p, []),
         "fem_destroy": (None, [P]),
+        # include/fem_hdg.h
+        "hdg_setup": (C.c_int, [C.POINTER(fem_mesh), I32, D, P, C.POINTER(P)]),
+        "hdg_info": (C.c_int, [P, C.POINTER(I64), C.POINTER(I64)]),
+        "hdg_apply": (C.c_int, [P, P, I64, P, I64]),
+        "hdg_diagonal": (C.c_int, [P, P, I64]),
+        "hdg_rhs": (C.c_int, [P, P, I64]),
+        "hdg_local_solve": (C.c_int, [P, P, I64, I32, P, I64, P, I64]),
+        "hdg_mixed_apply": (C.c_int, [P, P, I64, P, I64]),
+        "hdg_cg_solve": (C.c_int, [P, P, I64, P, I64, D, I32, C.POINTER(I32), C.POINTER(D)]),
+        "hdg_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -105,7 +115,8 @@ SYMBOLS = ("fem_default_options", "fem_setup", "fem_partition", "fem_nccl_unique
            "cg_solve", "cg_history", "fem_rhs", "fem_level_info", "fem_level_apply", "fem_level_diagonal",
            "fem_level_lambda", "fem_level_geometry", "mg_smooth", "mg_prolongate_add", "mg_restrict",
            "mg_coarse_solve", "fem_sync", "fem_kernel_launches", "fem_profile_read", "fem_last_error",
-           "fem_destroy")
+           "fem_destroy", "hdg_setup", "hdg_info", "hdg_apply", "hdg_diagonal", "hdg_rhs", "hdg_local_solve",
+           "hdg_mixed_apply", "hdg_cg_solve", "hdg_destroy")
 
 
 def lib():
@@ -361,3 +372,69 @@ class Fem:
         ms, n = C.c_double(), C.c_int64()
         _check(_lib.fem_profile_read(self.h, C.byref(ms), C.byref(n), 1 if reset else 0))
         return ms.value, n.value
+
+
+class Hdg:
+    """One HDG handle (include/fem_hdg.h: hdg_setup ... hdg_destroy), Cartesian box meshes.
+    Vectors are CUDA float64 tensors (device pointers only)."""
+
+    def __init__(self, cells, degree, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0), bc=(FEM_BC_DIRICHLET,) * 6,
+                 tau=5.0, stream=None):
+        m = _mesh(cells, lo, hi, 0.0, bc, 0, 1, None, None)
+        s = None if stream is None else C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+        h = C.c_void_p()
+        _check(_lib.hdg_setup(C.byref(m), degree, tau, s, C.byref(h)))
+        self.h = h
+        self.degree, self.cells = degree, tuple(cells)
+        nt, nc = C.c_int64(), C.c_int64()
+        _check(_lib.hdg_info(h, C.byref(nt), C.byref(nc)))
+        self.n_trace, self.n_cells = nt.value, nc.value
+        self.n_cell_dofs = self.n_cells * (degree + 1) ** 3
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.hdg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def hdg_apply(self, lam, y):
+        pl, nl = _vec(lam)
+        py, ny = _vec(y, True)
+        _check(_lib.hdg_apply(self.h, pl, nl, py, ny))
+        return y
+
+    def hdg_diagonal(self, d):
+        p, n = _vec(d, True)
+        _check(_lib.hdg_diagonal(self.h, p, n))
+        return d
+
+    def hdg_rhs(self, r):
+        p, n = _vec(r, True)
+        _check(_lib.hdg_rhs(self.h, p, n))
+        return r
+
+    def hdg_local_solve(self, lam, u, q=None, with_f=True):
+        pl, nl = _vec(lam)
+        pu, nu = _vec(u, True)
+        pq, nq = _vec(q, True) if q is not None else (None, 0)
+        _check(_lib.hdg_local_solve(self.h, pl, nl, 1 if with_f else 0, pu, nu, pq, nq))
+        return u
+
+    def hdg_mixed_apply(self, qu, y):
+        px, nx = _vec(qu)
+        py, ny = _vec(y, True)
+        _check(_lib.hdg_mixed_apply(self.h, px, nx, py, ny))
+        return y
+
+    def hdg_cg_solve(self, b, lam, rtol=1e-10, maxit=10000):
+        pb, nb = _vec(b)
+        px, nx = _vec(lam, True)
+        its, rel = C.c_int32(), C.c_double()
+        rc = _check(_lib.hdg_cg_solve(self.h, pb, nb, px, nx, rtol, maxit, C.byref(its), C.byref(rel)),
+                    (FEM_OK, FEM_NOT_CONVERGED))
+        return its.value, rel.value, rc == FEM_OK

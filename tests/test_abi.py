@@ -1,4 +1,5 @@
-"""The C-ABI library loads and exports every symbol include/fem.h declares (no GPU needed)."""
+"""The C-ABI library loads and exports every symbol include/fem.h and include/fem_hdg.h
+declare (no GPU needed)."""
 import ctypes
 import os
 import re
@@ -7,11 +8,11 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "fem.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("fem.h", "fem_hdg.h")]
 
 
 def declared_symbols():
-    src = open(HEADER).read()
+    src = "".join(open(h).read() for h in HEADERS)
     return sorted(set(re.findall(r"FEM_API\s+[\w\s\*]+?\b(\w+)\s*\(", src)))
 
 
@@ -24,7 +25,7 @@ def libpath():
 def test_header_declares_the_north_star_calls():
     syms = declared_symbols()
     for s in ("fem_setup", "fem_apply", "fem_diagonal", "mg_vcycle", "cg_solve", "fem_destroy",
-              "fem_last_error"):
+              "fem_last_error", "hdg_setup", "hdg_apply", "hdg_mixed_apply", "hdg_local_solve"):
         assert s in syms
 
 
@@ -36,7 +37,7 @@ def test_library_exports_every_declared_symbol(libpath):
     exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
     assert set(declared_symbols()) <= exported
     # nothing else leaks out of the library (visibility=hidden)
-    assert all(s in declared_symbols() or not s.startswith(("fem", "mg_", "cg_")) for s in exported)
+    assert all(s in declared_symbols() or not s.startswith(("fem", "mg_", "cg_", "hdg_")) for s in exported)
 
 
 def test_binding_symbol_list_matches_header(libpath):

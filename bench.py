@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rtol", type=float, default=1e-10)
+    ap.add_argument("--no-hdg", action="store_true", help="skip the N4 HDG operator measurement")
     ap.add_argument("--others", default="C2,C3,C5",
                     help="single GPU: also time these configs' solves and applies (extra key other_configs)")
     return ap.parse_args()
@@ -333,6 +334,74 @@ def other_configs(names, rtol, reps=5):
     return out
 
 
+def hdg_flops_per_cell(k):
+    """Algorithmic FMA x 2 of one HDG trace apply per cell (csrc/hdg.cu): face masses in and out
+    12 + 12 n^3, t-tensor 6 n^3, fast-diagonalization sweeps 6 n^4, face-layer reductions 6 n^3."""
+    n = k + 1
+    return 2 * (6 * n ** 4 + 36 * n ** 3)
+
+
+def hdg_mixed_flops_per_cell(k):
+    """Mixed apply per cell: per direction 3 n^4 (slot-d operators) + 4 n^4 (two tangential mass
+    sweeps of two fields): 21 n^4 FMA."""
+    return 2 * 21 * (k + 1) ** 4
+
+
+def hdg_config(cells=(32, 32, 32), k=4, rtol=1e-10, reps=20, solve=True):
+    """HDG Q_k on the C3 mesh (Cartesian, Dirichlet, manufactured u):
+    trace matrix-free and mixed matrix-free applies (reps back to back between CUDA events) with
+    their FP64 and HBM roofline fractions, and the Jacobi-PCG trace solve (iterations, time)."""
+    import torch
+    from paper_1611_03029_b200 import fem
+    hbm, _ = peaks()
+    H = fem.Hdg(cells, k)
+    nt, nc = H.n_trace, H.n_cells
+    x = torch.from_numpy(fem_inputs.uniform_pm1(0, nt)).cuda()
+    y = torch.empty_like(x)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) * 1e-3 / reps
+
+    t_tr = timed(lambda: H.hdg_apply(x, y))
+    m = (k + 1) ** 3
+    qu = torch.from_numpy(fem_inputs.uniform_pm1(1, 4 * nc * m)).cuda()
+    yq = torch.empty_like(qu)
+    t_mx = timed(lambda: H.hdg_mixed_apply(qu, yq))
+    its, rr, ok, ms = 0, None, None, None
+    if solve:
+        b = torch.zeros(nt, dtype=torch.float64, device="cuda")
+        H.hdg_rhs(b)
+        lam = torch.zeros_like(b)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        its, rr, ok = H.hdg_cg_solve(b, lam, rtol=rtol)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+    eq = nc * k ** 3
+    fl_tr, fl_mx = hdg_flops_per_cell(k) * nc, hdg_mixed_flops_per_cell(k) * nc
+    out = {"workload": f"N4: HDG Q{k} Cartesian {cells[0]}x{cells[1]}x{cells[2]} on [0,1]^3, Dirichlet, tau = 5",
+           "n_trace_dofs": nt, "n_cells": nc,
+           "trace_apply_us": t_tr * 1e6, "trace_dofs_per_s": nt / t_tr, "trace_equivalent_dofs_per_s": eq / t_tr,
+           "trace_fp64_frac": fl_tr / t_tr / 1e12 / FP64_PEAK_TFLOPS,
+           "trace_hbm_frac": 16.0 * nt / t_tr / 1e9 / hbm,
+           "mixed_apply_us": t_mx * 1e6, "mixed_dofs_per_s": 4 * nc * m / t_mx, "mixed_equivalent_dofs_per_s": eq / t_mx,
+           "mixed_fp64_frac": fl_mx / t_mx / 1e12 / FP64_PEAK_TFLOPS,
+           "mixed_hbm_frac": 64.0 * nc * m / t_mx / 1e9 / hbm,
+           "jacobi_pcg": {"iterations": its, "relres": rr, "converged": ok, "ms": ms},
+           "flops_per_cell": {"trace": hdg_flops_per_cell(k), "mixed": hdg_mixed_flops_per_cell(k)}}
+    H.close()
+    return out
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args, w):
     import torch
@@ -507,6 +576,8 @@ def run_ours(args, w):
         del b, x, flush
         torch.cuda.empty_cache()
         line["other_configs"] = other_configs([c for c in args.others.split(",") if c != w.name], args.rtol)
+        if not args.no_hdg:
+            line["other_configs"]["N4_HDG"] = hdg_config(rtol=args.rtol)
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(w, args.rtol)
         line["cpu_baseline"].pop("seconds", None)

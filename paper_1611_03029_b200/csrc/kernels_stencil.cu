@@ -177,12 +177,17 @@ __device__ constexpr RefTab<K> kRef{};
 // loaded two doubles per LDCU.128 (compile-time literals cost two UMOVs per use)
 template <int K>
 __constant__ RefTab<K> cRef = RefTab<K>();
-// MODE 1 epilogue operands: prefetch.global.L2 per 128-byte line, one z-element ahead
+// MODE 1 epilogue operands: prefetch.global.L2 per 128-byte line at the element's start
 // (C4 solve, 5 its, NB 4: bulk cp.async.bulk.prefetch.L2 one element ahead 141.2 ms, none
 // 132.5, per line one ahead 131.8, two ahead 125.1, three 133.1, four 135.3; with NB 3:
-// one ahead 122.2 ms, two ahead 124.4)
+// one ahead 122.2 ms, two ahead 124.4, at the element's start 118.4 ms: smoother step 1600 us,
+// DRAM 4.7 GB read vs 3.24 GB algorithmic.  Reading the epilogue's x from copies parked out of
+// the x~ tile brought DRAM reads to 3.39 GB but the step to 1712 us: not bandwidth-bound)
 #ifndef FEM_ST_PF_AHEAD
-#define FEM_ST_PF_AHEAD 1
+#define FEM_ST_PF_AHEAD 0
+#endif
+#ifndef FEM_ST_PF_X   // also prefetch x
+#define FEM_ST_PF_X 1
 #endif
 #ifndef FEM_ST_PF_LINES
 #define FEM_ST_PF_LINES 1
@@ -549,7 +554,8 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
         const int arr = t & 3, rq = t >> 2, r = rq % K, q = rq / K;
         const int gy = Y0 + K * s + r;
         if (gy >= a.NY) continue;
-        const double* base = arr == 0 ? a.x : arr == 1 ? a.xo : arr == 2 ? a.b : (a.dcls ? nullptr : a.dinv);
+        const double* base = arr == 0 ? (FEM_ST_PF_X ? a.x : nullptr) : arr == 1 ? a.xo : arr == 2 ? a.b
+                                                                                   : (a.dcls ? nullptr : a.dinv);
         if (!base) continue;
 #if FEM_ST_PF_LINES
         {   // per 128-byte line

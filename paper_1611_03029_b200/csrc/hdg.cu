@@ -35,6 +35,14 @@
 
 #pragma nv_diag_suppress 128   // code after the kRecover early return in the other modes
 
+// minimum resident blocks per SM requested from ptxas (register cap); 0 = none
+#ifndef FEM_HDG_MINB
+#define FEM_HDG_MINB 6
+#endif
+#ifndef FEM_HDG_MINB_MIX
+#define FEM_HDG_MINB_MIX 0
+#endif
+
 namespace fem {
 namespace {
 
@@ -75,7 +83,7 @@ struct HdgCfg {
 };
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1)) hdg_cell_kernel(HdgArgs a) {
+__global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HDG_MINB) hdg_cell_kernel(HdgArgs a) {
   constexpr int N = K + 1, NF = N * N, N3 = N * N * N;
   using Cfg = HdgCfg<N>;
   extern __shared__ double sm[];
@@ -321,7 +329,7 @@ __device__ __forceinline__ int tidx(int e, int i, int ta, int tb) {   // node i 
 }
 
 template <int K>
-__global__ void __launch_bounds__(MixCfg<K + 1>::CPB * (K + 1) * (K + 1)) hdg_mixed_kernel(
+__global__ void __launch_bounds__(MixCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HDG_MINB_MIX) hdg_mixed_kernel(
     const double* __restrict__ qu, double* __restrict__ y, const HdgTab* tab, int nx, int ny, int nz, int bc,
     int64_t ncells) {
   constexpr int N = K + 1, NF = N * N, N3 = N * N * N;
@@ -740,6 +748,8 @@ void launch_cells_k(hdg_ctx* h, HdgArgs a) {
   const size_t sm = sizeof(double) * Cfg::SMEM;
   auto kern = hdg_cell_kernel<K, MODE>;
   smem_attr(reinterpret_cast<const void*>(kern), sm);
+  FEM_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   a.tab = h->tab;
   a.nx = h->mesh.n[0];
   a.ny = h->mesh.n[1];
@@ -787,6 +797,8 @@ void launch_mixed_k(hdg_ctx* h, const double* qu, double* y) {
   const size_t sm = sizeof(double) * Cfg::SMEM;
   auto kern = hdg_mixed_kernel<K>;
   smem_attr(reinterpret_cast<const void*>(kern), sm);
+  FEM_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   const int64_t blocks = (h->n_cells + Cfg::CPB - 1) / Cfg::CPB;
   kern<<<(unsigned)blocks, dim3(N * N, Cfg::CPB), sm, h->stream>>>(qu, y, h->tab, h->mesh.n[0], h->mesh.n[1],
                                                                     h->mesh.n[2], h->bc, h->n_cells);

@@ -122,3 +122,11 @@ def test_jacobi_pcg_matches_direct_solve():
     x, its, hist = hdg.jacobi_pcg(op, op.rhs(hdg.load(mesh)), tol=1e-12)
     assert hist[-1] <= 1e-12 and its < 200
     assert np.abs(x - lam).max() <= 1e-9 * np.abs(lam).max()
+
+
+@pytest.mark.parametrize("eps", [0.0, 0.05])
+def test_diagonal_is_the_assembled_diagonal(eps):
+    # diag(K) gathered per face node == the diagonal of the assembled K (pinned above by
+    # symmetry, definiteness and the patch test); constrained rows 1
+    op = hdg.HdgOperator(Mesh((2, 3, 2), 2, eps=eps, bc=(D, N, N, D, D, N)))
+    assert np.abs(op.diagonal() - op.assemble().diagonal()).max() <= 1e-14 * np.abs(op.diagonal()).max()

@@ -27,6 +27,7 @@
 // stores, the second adds (no atomics, no zero fill, deterministic).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -687,6 +688,619 @@ void build_hdg_tab(int k, const double h[3], double tau, HdgTab& T) {
   }
 }
 
+
+// ================================================================ curved cells (the paper's design)
+// "HDG trace matrix-free" with the inner Schur complement's inverse STORED per cell (P:L449-460:
+// "Only the (k+1)^d x (k+1)^d matrix (D - B A^-1 B^T)^-1 needs to be explicitly stored"), on the
+// deformed box map x = xhat + eps s(xhat) (1,1,1) (reading R2), k <= 4 (the per-cell inversion
+// runs in shared memory).  With the GLL basis and the (k+1)-point Gauss rule the interpolation
+// B3 = val (x) val (x) val is square and invertible, so on every cell
+//   A^-1 = B3^-1 W^-1 B3^-T  (W = w det J at the Gauss points),   E_i = B3^T W sum_e Jinv_ei D_e,
+//   D_e B3^-1 = Dco_e (collocation derivative at the Gauss points, slot e),
+// and the inner Schur complement S = D + E A^-1 E^T = K_e + D: the cell's Laplace stiffness plus
+// tau times the face masses of its face layers (built by quadrature, inverted at setup).
+// Per cell and apply (R_q, R_u of step (1) are supported on the face layers):
+//   r_i(q) = sum_s (val^-T e_l)(q_d) g_si(q_t) / W(q),  g_si = -(w_F det J m_i) lambda_s(q_t)
+//   t = R_u - B3^T W sum_i sum_e Jinv_ei (Dco_e r_i)       (W^-1 B3^-T R_q,i = r_i)
+//   u = S^-1 t;  u_q = B3 u;  z_i = W^-1 sum_e Dco_e^T (Jinv_ei W u_q)
+//   at face points: q_i = sum_qd val^-1[l][qd] (r_i + z_i),  u = sum_qd val^-1[l][qd] u_q
+//   y_s = B_F^T [tau JxW (lambda - u) - sum_i (w_F det J m_i) q_i],
+// m = J^-T nhat (Nanson: JxW n = w_F det J m, JxW = w_F det J |m|).
+struct CurvTab {
+  double val[kMaxN][kMaxN];    // [q][i] GLL basis at the Gauss points
+  double vinv[kMaxN][kMaxN];   // [i][q] val^-1
+  double der[kMaxN][kMaxN];    // [q][i]
+  double dco[kMaxN][kMaxN];    // [q][p] collocation derivative at the Gauss points
+  double qw[kMaxN], qp[kMaxN];
+  double lo[3], len[3], h[3], eps, tau;
+};
+constexpr int kCurvDoubles = sizeof(CurvTab) / sizeof(double);
+
+template <int N>
+struct CurvCellGeo {                 // sin / cos of pi t_d at the Gauss points and the two faces
+  double sn[3][N], cs[3][N], sb[3][2], cb[3][2];
+};
+
+template <int N>
+__device__ void curv_cell_geo(const CurvTab& T, int cx, int cy, int cz, int t, CurvCellGeo<N>& G) {
+  const int c3[3] = {cx, cy, cz};
+  for (int i = t; i < 3 * (N + 2); i += N * N) {
+    const int d = i / (N + 2), j = i % (N + 2);
+    const double xr = j < N ? T.h[d] * (c3[d] + 0.5 * (T.qp[j] + 1.0)) : T.h[d] * (c3[d] + (j - N));
+    double sv, cv;
+    sincospi(xr / T.len[d], &sv, &cv);
+    if (j < N) {
+      G.sn[d][j] = sv;
+      G.cs[d][j] = cv;
+    } else {
+      G.sb[d][j - N] = sv;
+      G.cb[d][j - N] = cv;
+    }
+  }
+}
+
+// grad s at a point given sin / cos per direction; returns beta = eps / (1 + eps sum g), det J
+__device__ __forceinline__ void curv_point(const CurvTab& T, const double s[3], const double c[3], double g[3],
+                                           double& beta, double& detJ) {
+  g[0] = M_PI / T.len[0] * c[0] * s[1] * s[2];
+  g[1] = M_PI / T.len[1] * s[0] * c[1] * s[2];
+  g[2] = M_PI / T.len[2] * s[0] * s[1] * c[2];
+  const double sg = 1.0 + T.eps * (g[0] + g[1] + g[2]);
+  beta = T.eps / sg;
+  detJ = 0.125 * T.h[0] * T.h[1] * T.h[2] * sg;
+}
+// Jinv[e][d] = (2/h_e)(delta_ed - beta g_d)
+__device__ __forceinline__ double curv_jinv(const CurvTab& T, const double g[3], double beta, int e, int d) {
+  return (2.0 / T.h[e]) * ((e == d ? 1.0 : 0.0) - beta * g[d]);
+}
+
+template <int N>
+__device__ __forceinline__ int cidx(int e, int i, int ta, int tb) {   // node i on the e-line at (ta, tb)
+  return e == 0 ? i + N * ta + N * N * tb : e == 1 ? ta + N * i + N * N * tb : ta + N * tb + N * N * i;
+}
+
+// S_cell = D + E A^-1 E^T = D + sum_c P_c^T W P_c, P_c = W^-1 sum_e Dco_e^T (Jinv_ec W) B3, built
+// column by column with the apply's sum-factorized sweeps, then S^-1 by Gauss-Jordan in shared
+// memory (SPD: no pivoting); one block per cell, the first (k+1)^2 threads own the sweep lines.
+template <int K>
+__global__ void __launch_bounds__(128) hdg_curved_setup_kernel(const CurvTab* tab, double* __restrict__ Sinv,
+                                                               int nx, int ny, int64_t ncells) {
+  constexpr int N = K + 1, NF = N * N, M = N * N * N;
+  extern __shared__ double sm[];
+  CurvTab& T = *reinterpret_cast<CurvTab*>(sm);
+  double* A = sm + kCurvDoubles;   // [M][M]
+  double* Uq = A + M * M;          // [M]
+  double* P = Uq + M;              // [M]
+  double* T1 = P + M;              // [M]
+  double* T2 = T1 + M;             // [M]
+  double* Y = T2 + M;              // [M]
+  double* row = Y + M;             // [M]
+  __shared__ CurvCellGeo<N> geo;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int t = tid < NF ? tid : 0, ta = t % N, tb = t / N;
+  const bool ln = tid < NF;
+  for (int i = tid; i < kCurvDoubles; i += nt) sm[i] = reinterpret_cast<const double*>(tab)[i];
+  const int64_t cell = blockIdx.x;
+  const int cx = (int)(cell % nx), cy = (int)((cell / nx) % ny), cz = (int)(cell / ((int64_t)nx * ny));
+  __syncthreads();
+  if (ln) curv_cell_geo<N>(T, cx, cy, cz, t, geo);
+  __syncthreads();
+  auto cell_geo = [&](int q, double& W, double Ji[3][3]) {
+    const int q0 = q % N, q1 = (q / N) % N, q2 = q / NF;
+    const double s[3] = {geo.sn[0][q0], geo.sn[1][q1], geo.sn[2][q2]}, c[3] = {geo.cs[0][q0], geo.cs[1][q1], geo.cs[2][q2]};
+    double g[3], beta, detJ;
+    curv_point(T, s, c, g, beta, detJ);
+    W = T.qw[q0] * T.qw[q1] * T.qw[q2] * detJ;
+    for (int e = 0; e < 3; ++e)
+      for (int d = 0; d < 3; ++d) Ji[e][d] = curv_jinv(T, g, beta, e, d);
+  };
+  auto sweep = [&](int e, const double* src, double* dst, auto Mt) {   // lines of the first NF threads
+    if (!ln) return;
+    double g[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = src[cidx<N>(e, i, ta, tb)];
+#pragma unroll
+    for (int o = 0; o < N; ++o) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v = fma(Mt(o, i), g[i], v);
+      dst[cidx<N>(e, o, ta, tb)] = v;
+    }
+  };
+  for (int jc = 0; jc < M; ++jc) {
+    const int j0 = jc % N, j1 = (jc / N) % N, j2 = jc / NF;
+    for (int q = tid; q < M; q += nt) {   // u_q = B3 e_j (a tensor product of basis columns)
+      Uq[q] = T.val[q % N][j0] * T.val[(q / N) % N][j1] * T.val[q / NF][j2];
+      Y[q] = 0.0;
+    }
+    __syncthreads();
+    for (int c = 0; c < 3; ++c) {
+      // P_c e_j = W^-1 sum_e Dco_e^T (Jinv_ec W u_q)
+      for (int q = tid; q < M; q += nt) P[q] = 0.0;
+      __syncthreads();
+      for (int e = 0; e < 3; ++e) {
+        for (int q = tid; q < M; q += nt) {
+          double W, Ji[3][3];
+          cell_geo(q, W, Ji);
+          T1[q] = Ji[e][c] * W * Uq[q];
+        }
+        __syncthreads();
+        sweep(e, T1, T2, [&](int o, int i) { return T.dco[i][o]; });
+        __syncthreads();
+        for (int q = tid; q < M; q += nt) P[q] += T2[q];
+        __syncthreads();
+      }
+      // p_c = P_c e_j = W^-1 X;  P_c^T W p_c = B3^T sum_e (Jinv_ec W) Dco_e p_c
+      for (int q = tid; q < M; q += nt) {
+        double W, Ji[3][3];
+        cell_geo(q, W, Ji);
+        P[q] /= W;
+      }
+      __syncthreads();
+      for (int e = 0; e < 3; ++e) {
+        sweep(e, P, T2, [&](int o, int i) { return T.dco[o][i]; });
+        __syncthreads();
+        for (int q = tid; q < M; q += nt) {
+          double W, Ji[3][3];
+          cell_geo(q, W, Ji);
+          Y[q] += Ji[e][c] * W * T2[q];
+        }
+        __syncthreads();
+      }
+    }
+    // the column of sum_c P_c^T W P_c is B3^T Y
+    sweep(0, Y, T1, [&](int o, int i) { return T.val[i][o]; });
+    __syncthreads();
+    sweep(1, T1, T2, [&](int o, int i) { return T.val[i][o]; });
+    __syncthreads();
+    sweep(2, T2, T1, [&](int o, int i) { return T.val[i][o]; });
+    __syncthreads();
+    for (int i = tid; i < M; i += nt) A[i * M + jc] = T1[i];
+    __syncthreads();
+  }
+  // + D: tau face masses on the face layers
+  for (int p = tid; p < M * M; p += nt) {
+    const int i = p / M, j = p % M;
+    const int ic[3] = {i % N, (i / N) % N, i / NF}, jcc[3] = {j % N, (j / N) % N, j / NF};
+    double add = 0.0;
+    for (int sd = 0; sd < 6; ++sd) {
+      const int d = sd / 2, hi = sd & 1, l = hi ? K : 0;
+      if (ic[d] != l || jcc[d] != l) continue;
+      const int t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
+      for (int b = 0; b < N; ++b)
+        for (int a2 = 0; a2 < N; ++a2) {
+          double sv[3], cv[3];
+          sv[d] = geo.sb[d][hi];
+          cv[d] = geo.cb[d][hi];
+          sv[t1] = geo.sn[t1][a2];
+          cv[t1] = geo.cs[t1][a2];
+          sv[t2] = geo.sn[t2][b];
+          cv[t2] = geo.cs[t2][b];
+          double g[3], beta, detJ;
+          curv_point(T, sv, cv, g, beta, detJ);
+          double m2 = 0.0;
+          for (int e = 0; e < 3; ++e) {
+            const double me = curv_jinv(T, g, beta, d, e);
+            m2 += me * me;
+          }
+          add += T.tau * T.qw[a2] * T.qw[b] * detJ * sqrt(m2) * T.val[a2][ic[t1]] * T.val[b][ic[t2]] *
+                 T.val[a2][jcc[t1]] * T.val[b][jcc[t2]];
+        }
+    }
+    A[p] += add;
+  }
+  __syncthreads();
+  for (int p = tid; p < M * M; p += nt) {   // symmetrize (rounding)
+    const int i = p / M, j = p % M;
+    if (i < j) {
+      const double v = 0.5 * (A[i * M + j] + A[j * M + i]);
+      A[i * M + j] = v;
+      A[j * M + i] = v;
+    }
+  }
+  __syncthreads();
+  // in-place Gauss-Jordan inverse (SPD: no pivoting)
+  for (int k = 0; k < M; ++k) {
+    const double piv = A[k * M + k];
+    for (int j = tid; j < M; j += nt) {
+      row[j] = (j == k ? 1.0 : A[k * M + j]) / piv;
+      P[j] = A[j * M + k];   // the pivot column, read before any thread overwrites it
+    }
+    __syncthreads();
+    for (int p = tid; p < M * M; p += nt) {
+      const int i = p / M, j = p % M;
+      if (i == k) continue;
+      A[p] = (j == k ? 0.0 : A[p]) - P[i] * row[j];
+    }
+    __syncthreads();
+    for (int j = tid; j < M; j += nt) A[k * M + j] = row[j];
+    __syncthreads();
+  }
+  double* out = Sinv + cell * (int64_t)M * M;
+  for (int p = tid; p < M * M; p += nt) out[p] = A[p];
+}
+
+template <int N>
+struct CurvCfg {
+  static constexpr int NF = N * N, M = N * N * N;
+  static constexpr int PER_CELL = 10 * M + 3 * 6 * NF;   // r[3], z[3], T1, T2, U, Uq; lam, lq, fo
+  static constexpr int SMEM = kCurvDoubles + PER_CELL;
+};
+
+// MODE kApply / kRhs / kRecover (see hdg_cell_kernel), one cell per block of (k+1)^2 threads.
+// kDiag here: blockIdx = cell; the 6 (k+1)^2 unit traces of that cell in turn, output the
+// diagonal entry of the cell's trace matrix (a.y[cell * 6 NF + s NF + a]).
+template <int K, int MODE>
+__global__ void __launch_bounds__((K + 1) * (K + 1)) hdg_curved_kernel(HdgArgs a, const CurvTab* tab,
+                                                                      const double* __restrict__ Sinv) {
+  constexpr int N = K + 1, NF = N * N, M = N * N * N;
+  extern __shared__ double sm[];
+  CurvTab& T = *reinterpret_cast<CurvTab*>(sm);
+  __shared__ CurvCellGeo<N> geo;
+  const int t = threadIdx.x, ta = t % N, tb = t / N;
+  for (int i = t; i < kCurvDoubles; i += NF) sm[i] = reinterpret_cast<const double*>(tab)[i];
+  double* R = sm + kCurvDoubles;   // [3][M]
+  double* Z = R + 3 * M;           // [3][M]
+  double* T1 = Z + 3 * M;
+  double* T2 = T1 + M;
+  double* U = T2 + M;
+  double* Uq = U + M;
+  double* lam = Uq + M;            // [6][NF]
+  double* lq = lam + 6 * NF;       // [6][NF] lambda at the face points
+  double* fo = lq + 6 * NF;        // [6][NF]
+  const int64_t j = blockIdx.x;
+  int cx, cy, cz;
+  bool active = true;
+  if (MODE != kDiag && a.color >= 0) {
+    const int cpr = (a.nx + 1) / 2;
+    const int64_t rowi = j / cpr;
+    cy = (int)(rowi % a.ny);
+    cz = (int)(rowi / a.ny);
+    cx = 2 * (int)(j % cpr) + ((cy + cz + a.color) & 1);
+    active = cz < a.nz && cx < a.nx;
+    if (!active) return;   // block-uniform
+  } else {
+    cx = (int)(j % a.nx);
+    cy = (int)((j / a.nx) % a.ny);
+    cz = (int)(j / ((int64_t)a.nx * a.ny));
+  }
+  const int64_t cell = cx + (int64_t)a.nx * (cy + (int64_t)a.ny * cz);
+  int64_t fid[6];
+  bool inter[6], dir[6];
+  {
+    const int c3[3] = {cx, cy, cz}, n3[3] = {a.nx, a.ny, a.nz};
+    for (int s = 0; s < 6; ++s) {
+      const int d = s / 2, hi = s & 1;
+      fid[s] = d == 0 ? (cx + hi) + (int64_t)(a.nx + 1) * (cy + (int64_t)a.ny * cz)
+             : d == 1 ? a.fx + cx + (int64_t)a.nx * ((cy + hi) + (int64_t)(a.ny + 1) * cz)
+                      : a.fx + a.fy + cx + (int64_t)a.nx * (cy + (int64_t)a.ny * (cz + hi));
+      inter[s] = hi ? c3[d] < n3[d] - 1 : c3[d] > 0;
+      dir[s] = !inter[s] && ((a.bc >> s) & 1);
+    }
+  }
+  __syncthreads();
+  curv_cell_geo<N>(T, cx, cy, cz, t, geo);
+  __syncthreads();
+  const double* Sc = Sinv + cell * (int64_t)M * M;
+
+  // face-point geometry of face s at the thread's face point (a, b) = (ta, tb)
+  auto face_geo = [&](int s, double wm[3], double& jxw) {
+    const int d = s / 2, hi = s & 1, t1 = d == 0 ? 1 : 0, t2 = d == 2 ? 1 : 2;
+    double sv[3], cv[3];
+    sv[d] = geo.sb[d][hi];
+    cv[d] = geo.cb[d][hi];
+    sv[t1] = geo.sn[t1][ta];
+    cv[t1] = geo.cs[t1][ta];
+    sv[t2] = geo.sn[t2][tb];
+    cv[t2] = geo.cs[t2][tb];
+    double g[3], beta, detJ;
+    curv_point(T, sv, cv, g, beta, detJ);
+    const double sg = hi ? 1.0 : -1.0, wf = T.qw[ta] * T.qw[tb] * detJ;
+    double m2 = 0.0;
+    for (int e = 0; e < 3; ++e) {
+      const double me = sg * curv_jinv(T, g, beta, d, e);
+      wm[e] = wf * me;
+      m2 += me * me;
+    }
+    jxw = wf * sqrt(m2);
+  };
+  // the cell's q-point metric at q-point (q0, q1, q2)
+  auto cell_geo = [&](int q0, int q1, int q2, double& W, double Ji[3][3]) {
+    const double s[3] = {geo.sn[0][q0], geo.sn[1][q1], geo.sn[2][q2]}, c[3] = {geo.cs[0][q0], geo.cs[1][q1], geo.cs[2][q2]};
+    double g[3], beta, detJ;
+    curv_point(T, s, c, g, beta, detJ);
+    W = T.qw[q0] * T.qw[q1] * T.qw[q2] * detJ;
+    for (int e = 0; e < 3; ++e)
+      for (int d = 0; d < 3; ++d) Ji[e][d] = curv_jinv(T, g, beta, e, d);
+  };
+  // sweep along direction e with the 1-D matrix Mt (out[o] = sum_i Mt(o, i) in[i])
+  auto sweep = [&](int e, const double* src, double* dst, auto Mt) {
+    double g[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) g[i] = src[cidx<N>(e, i, ta, tb)];
+#pragma unroll
+    for (int o = 0; o < N; ++o) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v = fma(Mt(o, i), g[i], v);
+      dst[cidx<N>(e, o, ta, tb)] = v;
+    }
+  };
+
+  const int nrep = MODE == kDiag ? 6 * NF : 1;
+  for (int rep = 0; rep < nrep; ++rep) {
+    // ---- inputs
+    for (int s = 0; s < 6; ++s) {
+      double v = 0.0;
+      if (MODE == kDiag) v = (rep == s * NF + t) ? 1.0 : 0.0;
+      else if ((MODE == kApply || MODE == kRecover) && !dir[s]) v = a.lam[fid[s] * NF + t];
+      lam[s * NF + t] = v;
+    }
+    __syncthreads();
+    // lambda at the face points (B_F: val in both tangential directions)
+    for (int s = 0; s < 6; ++s) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v = fma(T.val[ta][i], lam[s * NF + i + N * tb], v);
+      fo[s * NF + t] = v;
+    }
+    __syncthreads();
+    for (int s = 0; s < 6; ++s) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v = fma(T.val[tb][i], fo[s * NF + ta + N * i], v);
+      lq[s * NF + t] = v;
+    }
+    __syncthreads();
+    // ---- r_i(q) = sum_s vinv[l][q_d] g_si(q_t) / W(q), g_si = -wm_i lambda_q; R_u on the face layers
+    for (int i = t; i < 3 * M + M; i += NF) (i < 3 * M ? R : T1)[i < 3 * M ? i : i - 3 * M] = 0.0;
+    __syncthreads();
+    for (int s = 0; s < 6; ++s) {   // thread = face point (ta, tb) of face s: its normal line
+      const int d = s / 2, l = (s & 1) ? K : 0;
+      double wm[3], jxw;
+      face_geo(s, wm, jxw);
+      const double lv = lq[s * NF + t];
+      fo[s * NF + t] = T.tau * jxw * lv;   // gu_s at the face point
+#pragma unroll
+      for (int qd = 0; qd < N; ++qd) {
+        const int q = cidx<N>(d, qd, ta, tb);
+        const double vl = T.vinv[l][qd];
+        for (int c = 0; c < 3; ++c) R[c * M + q] += vl * (-wm[c] * lv);   // / W below
+      }
+      __syncthreads();   // faces of the same direction touch the same lines
+    }
+    for (int q = t; q < M; q += NF) {
+      double W, Ji[3][3];
+      cell_geo(q % N, (q / N) % N, q / NF, W, Ji);
+      for (int c = 0; c < 3; ++c) R[c * M + q] /= W;
+    }
+    // R_u = sum_s e_l (x) B_F^T gu_s  (two tangential sweeps, then onto the layer)
+    for (int s = 0; s < 6; ++s) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v = fma(T.val[i][ta], fo[s * NF + i + N * tb], v);
+      lq[s * NF + t] = lq[s * NF + t];   // keep lambda_q
+      Z[s * NF + t] = v;                 // scratch (Z is free until step z)
+    }
+    __syncthreads();
+    for (int s = 0; s < 6; ++s) {
+      const int d = s / 2, l = (s & 1) ? K : 0;
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v = fma(T.val[i][tb], Z[s * NF + ta + N * i], v);
+      __syncthreads();
+      T1[cidx<N>(d, l, ta, tb)] += v;
+      __syncthreads();
+    }
+    if (MODE != kDiag && a.F && (MODE == kRhs || MODE == kRecover))
+      for (int i = t; i < M; i += NF) T1[i] += a.F[cell * M + i];
+    __syncthreads();
+    // ---- h = sum_i sum_e Jinv_ei Dco_e r_i at the q-points -> U (scratch), then t = R_u - B3^T W h
+    for (int q = t; q < M; q += NF) U[q] = 0.0;
+    __syncthreads();
+    for (int e = 0; e < 3; ++e) {
+      for (int c = 0; c < 3; ++c) {
+        sweep(e, R + c * M, T2, [&](int o, int i) { return T.dco[o][i]; });
+        __syncthreads();
+        for (int q = t; q < M; q += NF) {
+          double W, Ji[3][3];
+          cell_geo(q % N, (q / N) % N, q / NF, W, Ji);
+          U[q] += Ji[e][c] * T2[q];
+        }
+        __syncthreads();
+      }
+    }
+    for (int q = t; q < M; q += NF) {
+      double W, Ji[3][3];
+      cell_geo(q % N, (q / N) % N, q / NF, W, Ji);
+      U[q] *= W;
+    }
+    __syncthreads();
+    sweep(0, U, T2, [&](int o, int i) { return T.val[i][o]; });   // B3^T = val^T per direction
+    __syncthreads();
+    sweep(1, T2, U, [&](int o, int i) { return T.val[i][o]; });
+    __syncthreads();
+    sweep(2, U, T2, [&](int o, int i) { return T.val[i][o]; });
+    __syncthreads();
+    for (int i = t; i < M; i += NF) T1[i] -= T2[i];   // t
+    __syncthreads();
+    // ---- u = S^-1 t (dense, the stored inverse)
+    for (int i = t; i < M; i += NF) {
+      double v = 0.0;
+      for (int jj = 0; jj < M; ++jj) v = fma(Sc[(int64_t)jj * M + i], T1[jj], v);
+      U[i] = v;
+    }
+    __syncthreads();
+    if (MODE == kRecover)
+      for (int i = t; i < M; i += NF) a.u[cell * M + i] = U[i];
+    // ---- u_q = B3 u
+    sweep(0, U, T2, [&](int o, int i) { return T.val[o][i]; });
+    __syncthreads();
+    sweep(1, T2, Uq, [&](int o, int i) { return T.val[o][i]; });
+    __syncthreads();
+    sweep(2, Uq, T2, [&](int o, int i) { return T.val[o][i]; });
+    __syncthreads();
+    for (int i = t; i < M; i += NF) Uq[i] = T2[i];
+    __syncthreads();
+    // ---- z_i = W^-1 sum_e Dco_e^T (Jinv_ei W u_q)
+    for (int i = t; i < 3 * M; i += NF) Z[i] = 0.0;
+    __syncthreads();
+    for (int e = 0; e < 3; ++e) {
+      for (int c = 0; c < 3; ++c) {
+        for (int q = t; q < M; q += NF) {
+          double W, Ji[3][3];
+          cell_geo(q % N, (q / N) % N, q / NF, W, Ji);
+          T2[q] = Ji[e][c] * W * Uq[q];
+        }
+        __syncthreads();
+        sweep(e, T2, T1, [&](int o, int i) { return T.dco[i][o]; });
+        __syncthreads();
+        for (int q = t; q < M; q += NF) Z[c * M + q] += T1[q];
+        __syncthreads();
+      }
+    }
+    for (int q = t; q < M; q += NF) {
+      double W, Ji[3][3];
+      cell_geo(q % N, (q / N) % N, q / NF, W, Ji);
+      for (int c = 0; c < 3; ++c) Z[c * M + q] = Z[c * M + q] / W + R[c * M + q];   // r_i + z_i
+    }
+    __syncthreads();
+    if (MODE == kRecover) {
+      if (a.q) {   // q_i nodal = B3^-1 (r_i + z_i)
+        for (int c = 0; c < 3; ++c) {
+          sweep(0, Z + c * M, T1, [&](int o, int i) { return T.vinv[o][i]; });
+          __syncthreads();
+          sweep(1, T1, T2, [&](int o, int i) { return T.vinv[o][i]; });
+          __syncthreads();
+          sweep(2, T2, T1, [&](int o, int i) { return T.vinv[o][i]; });
+          __syncthreads();
+          for (int i = t; i < M; i += NF) a.q[(int64_t)c * a.n_work * M + cell * M + i] = T1[i];
+          __syncthreads();
+        }
+      }
+      return;
+    }
+    // ---- face outputs: out = tau JxW (lambda - u) - sum_i wm_i q_i at the face points, then B_F^T
+    for (int s = 0; s < 6; ++s) {
+      const int d = s / 2, l = (s & 1) ? K : 0;
+      double wm[3], jxw;
+      face_geo(s, wm, jxw);
+      double qv[3] = {0, 0, 0}, uv = 0.0;
+#pragma unroll
+      for (int qd = 0; qd < N; ++qd) {
+        const int q = cidx<N>(d, qd, ta, tb);
+        const double vl = T.vinv[l][qd];
+        uv = fma(vl, Uq[q], uv);
+        for (int c = 0; c < 3; ++c) qv[c] = fma(vl, Z[c * M + q], qv[c]);
+      }
+      fo[s * NF + t] = T.tau * jxw * (lq[s * NF + t] - uv) - (wm[0] * qv[0] + wm[1] * qv[1] + wm[2] * qv[2]);
+    }
+    __syncthreads();
+    for (int s = 0; s < 6; ++s) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v = fma(T.val[i][ta], fo[s * NF + i + N * tb], v);
+      lq[s * NF + t] = v;
+    }
+    __syncthreads();
+    for (int s = 0; s < 6; ++s) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) v = fma(T.val[i][tb], lq[s * NF + ta + N * i], v);
+      if (MODE == kDiag) {
+        if (rep == s * NF + t) a.y[cell * 6 * NF + rep] = v;
+        continue;
+      }
+      double* yp = a.y + fid[s] * NF + t;
+      if (dir[s]) {
+        *yp = MODE == kApply ? a.lam[fid[s] * NF + t] : 0.0;
+      } else {
+        if (MODE == kRhs) v = -v;
+        if (a.color == 1 && inter[s]) *yp += v;
+        else *yp = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// diag(K) from the per-cell element diagonals dc[cell][6][NF] (curved meshes)
+__global__ void hdg_curved_diag_kernel(double* d, const double* dc, int N, int nx, int ny, int nz, int64_t fx,
+                                       int64_t fy, int bc, int64_t n) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  const int NF = N * N;
+  const int64_t f = g / NF;
+  const int t = (int)(g % NF);
+  int dd, i, nn;
+  int64_t c_above;   // the cell whose lo side the face is (index with i)
+  int64_t step;
+  if (f < fx) {
+    dd = 0;
+    i = (int)(f % (nx + 1));
+    const int64_t r = f / (nx + 1);
+    c_above = i + (int64_t)nx * r;
+    step = 1;
+    nn = nx;
+  } else if (f < fx + fy) {
+    const int64_t ff = f - fx;
+    dd = 1;
+    const int cx = (int)(ff % nx);
+    i = (int)((ff / nx) % (ny + 1));
+    const int cz = (int)(ff / ((int64_t)nx * (ny + 1)));
+    c_above = cx + (int64_t)nx * (i + (int64_t)ny * cz);
+    step = nx;
+    nn = ny;
+  } else {
+    const int64_t ff = f - fx - fy;
+    dd = 2;
+    i = (int)(ff / ((int64_t)nx * ny));
+    c_above = ff % ((int64_t)nx * ny) + (int64_t)nx * ny * i;
+    step = (int64_t)nx * ny;
+    nn = nz;
+  }
+  const bool has_hi = i < nn, has_lo = i > 0;
+  if ((!has_lo && ((bc >> (2 * dd)) & 1)) || (!has_hi && ((bc >> (2 * dd + 1)) & 1))) {
+    d[g] = 1.0;
+    return;
+  }
+  double v = 0.0;
+  if (has_hi) v += dc[c_above * 6 * NF + (2 * dd) * NF + t];
+  if (has_lo) v += dc[(c_above - step) * 6 * NF + (2 * dd + 1) * NF + t];
+  d[g] = v;
+}
+
+// manufactured load on the deformed map: F_v = sum_q f(x(q)) phi_v(q) w det J(q)
+__global__ void hdg_curved_load_kernel(double* F, const CurvTab* tab, int N, int nx, int ny, int64_t total) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= total) return;
+  const CurvTab& T = *tab;
+  const int M = N * N * N;
+  const int64_t cell = g / M;
+  const int v = (int)(g % M);
+  const int v0 = v % N, v1 = (v / N) % N, v2 = v / (N * N);
+  const int c3[3] = {(int)(cell % nx), (int)((cell / nx) % ny), (int)(cell / ((int64_t)nx * ny))};
+  const double cf = M_PI * M_PI * (1.0 / (T.len[0] * T.len[0]) + 1.0 / (T.len[1] * T.len[1]) + 1.0 / (T.len[2] * T.len[2]));
+  double acc = 0.0;
+  for (int q2 = 0; q2 < N; ++q2)
+    for (int q1 = 0; q1 < N; ++q1)
+      for (int q0 = 0; q0 < N; ++q0) {
+        const int qq[3] = {q0, q1, q2};
+        double s[3], c[3], xh[3];
+        for (int d = 0; d < 3; ++d) {
+          xh[d] = T.h[d] * (c3[d] + 0.5 * (T.qp[qq[d]] + 1.0));
+          sincospi(xh[d] / T.len[d], &s[d], &c[d]);
+        }
+        double g3[3], beta, detJ;
+        curv_point(T, s, c, g3, beta, detJ);
+        const double sx = s[0] * s[1] * s[2];
+        double f = cf;
+        for (int d = 0; d < 3; ++d) f *= sinpi((xh[d] + T.eps * sx) / T.len[d]);
+        acc += f * T.val[q0][v0] * T.val[q1][v1] * T.val[q2][v2] * T.qw[q0] * T.qw[q1] * T.qw[q2] * detJ;
+      }
+  F[g] = acc;
+}
+
 }  // namespace
 }  // namespace fem
 
@@ -707,6 +1321,11 @@ struct hdg_ctx {
   double* ydiag = nullptr;         // scratch
   double *r = nullptr, *p = nullptr, *q = nullptr, *z = nullptr, *part = nullptr, *scal = nullptr;
   double* d1d = nullptr;           // qp, qw, val for the load kernel
+  // curved meshes (deform_eps != 0) or FEM_HDG_DENSE=1: the paper's design, S^-1 stored per cell
+  bool curved = false;
+  fem::CurvTab* ctab = nullptr;    // device
+  double* Sinv = nullptr;          // [n_cells][M][M]
+  double* dc = nullptr;            // [n_cells][6][NF] element diagonals
 };
 
 namespace fem {
@@ -820,12 +1439,79 @@ void launch_mixed(hdg_ctx* h, const double* qu, double* y) {
   }
 }
 
+template <int K, int MODE>
+void launch_curved_k(hdg_ctx* h, HdgArgs a) {
+  constexpr int N = K + 1;
+  using Cfg = CurvCfg<N>;
+  const size_t sm = sizeof(double) * Cfg::SMEM;
+  auto kern = hdg_curved_kernel<K, MODE>;
+  smem_attr(reinterpret_cast<const void*>(kern), sm);
+  a.tab = h->tab;
+  a.nx = h->mesh.n[0];
+  a.ny = h->mesh.n[1];
+  a.nz = h->mesh.n[2];
+  a.fx = h->fx;
+  a.fy = h->fy;
+  a.bc = h->bc;
+  auto go = [&](int color) {
+    a.color = color;
+    const int64_t blocks = color >= 0 ? (int64_t)((a.nx + 1) / 2) * a.ny * a.nz : h->n_cells;
+    a.n_work = h->n_cells;
+    kern<<<(unsigned)blocks, N * N, sm, h->stream>>>(a, h->ctab, h->Sinv);
+    count_launch();
+    check_launch("hdg_curved_kernel");
+  };
+  if (MODE == kApply || MODE == kRhs) {
+    go(0);
+    go(1);
+  } else {
+    go(-1);
+  }
+}
+
+template <int MODE>
+void launch_curved(hdg_ctx* h, const HdgArgs& a) {
+  switch (h->k) {
+    case 1: launch_curved_k<1, MODE>(h, a); break;
+    case 2: launch_curved_k<2, MODE>(h, a); break;
+    case 3: launch_curved_k<3, MODE>(h, a); break;
+    case 4: launch_curved_k<4, MODE>(h, a); break;
+    default: throw Error{FEM_E_ARG, "curved HDG: degree 1..4"};
+  }
+}
+
+template <int K>
+void curved_setup_k(hdg_ctx* h) {
+  constexpr int N = K + 1, M = N * N * N;
+  const size_t sm = sizeof(double) * (kCurvDoubles + M * M + 6 * M);
+  auto kern = hdg_curved_setup_kernel<K>;
+  smem_attr(reinterpret_cast<const void*>(kern), sm);
+  kern<<<(unsigned)h->n_cells, 128, sm, h->stream>>>(h->ctab, h->Sinv, h->mesh.n[0], h->mesh.n[1], h->n_cells);
+  count_launch();
+  check_launch("hdg_curved_setup_kernel");
+}
+
+// dispatch: the fast-diagonalization kernels on Cartesian meshes, the stored-inverse ones otherwise
+template <int MODE>
+void launch_any(hdg_ctx* h, const HdgArgs& a) {
+  if (h->curved) launch_curved<MODE>(h, a);
+  else launch_cells<MODE>(h, a);
+}
+
 unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8); }
 
 void ensure_load(hdg_ctx* h) {
   if (h->F) return;
   const int N = h->n;
   h->F = hdg_alloc(h->n_cells * N * N * N);
+  if (h->curved) {
+    const int64_t tot = h->n_cells * N * N * N;
+    hdg_curved_load_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, h->stream>>>(h->F, h->ctab, N, h->mesh.n[0],
+                                                                               h->mesh.n[1], tot);
+    count_launch();
+    check_launch("hdg_curved_load_kernel");
+    return;
+  }
   const double len[3] = {h->mesh.hi[0] - h->mesh.lo[0], h->mesh.hi[1] - h->mesh.lo[1], h->mesh.hi[2] - h->mesh.lo[2]};
   const double c = M_PI * M_PI * (1.0 / (len[0] * len[0]) + 1.0 / (len[1] * len[1]) + 1.0 / (len[2] * len[2]));
   const int64_t total = h->n_cells * N * N * N;
@@ -861,9 +1547,8 @@ int hdg_setup(const fem_mesh* mesh, int32_t degree, double tau, void* stream, hd
     *out = nullptr;
     if (degree < 1 || degree > kMaxDeg) throw Error{FEM_E_ARG, "degree must be 1..8"};
     if (!(tau > 0.0)) throw Error{FEM_E_ARG, "tau must be positive"};
-    if (mesh->deform_eps != 0.0 || mesh->geometry != FEM_GEOM_BOX || mesh->mapping_degree != 0 ||
-        mesh->kappa_amplitude != 0.0)
-      throw Error{FEM_E_ARG, "HDG: Cartesian box meshes only"};
+    if (mesh->geometry != FEM_GEOM_BOX || mesh->mapping_degree != 0 || mesh->kappa_amplitude != 0.0)
+      throw Error{FEM_E_ARG, "HDG: box meshes (Cartesian or the deformed map) only"};
     if (mesh->nranks > 1) throw Error{FEM_E_ARG, "HDG: single rank"};
     for (int d = 0; d < 3; ++d)
       if (mesh->n[d] < 1 || !(mesh->hi[d] > mesh->lo[d])) throw Error{FEM_E_ARG, "bad mesh"};
@@ -883,10 +1568,10 @@ int hdg_setup(const fem_mesh* mesh, int32_t degree, double tau, void* stream, hd
     for (int s = 0; s < 6; ++s)
       if (mesh->bc[s] == FEM_BC_DIRICHLET) h->bc |= 1 << s;
     build_hdg_tab(degree, h->h, tau, h->tab_host);
-    h->tab = reinterpret_cast<HdgTab*>(hdg_alloc(kTabDoubles));
-    FEM_CUDA_TRY(cudaMemcpyAsync(h->tab, &h->tab_host, sizeof(HdgTab), cudaMemcpyHostToDevice, h->stream));
     Tables1D t1;
     build_tables(degree, t1);
+    h->tab = reinterpret_cast<HdgTab*>(hdg_alloc(kTabDoubles));
+    FEM_CUDA_TRY(cudaMemcpyAsync(h->tab, &h->tab_host, sizeof(HdgTab), cudaMemcpyHostToDevice, h->stream));
     std::vector<double> d1(3 * kMaxN + kMaxN * kMaxN, 0.0);
     for (int q = 0; q < h->n; ++q) {
       d1[q] = t1.qp[q];
@@ -897,14 +1582,55 @@ int hdg_setup(const fem_mesh* mesh, int32_t degree, double tau, void* stream, hd
     FEM_CUDA_TRY(cudaMemcpyAsync(h->d1d, d1.data(), sizeof(double) * d1.size(), cudaMemcpyHostToDevice, h->stream));
     // element diagonal by the cell kernel on unit traces, then diag(K) and its inverse
     const int NF = h->n * h->n;
-    h->de = hdg_alloc(6 * NF);
-    HdgArgs a{};
-    a.y = h->de;
-    launch_cells<kDiag>(h.get(), a);
+    const char* dense = std::getenv("FEM_HDG_DENSE");
+    h->curved = mesh->deform_eps != 0.0 || (dense && std::atoi(dense) != 0);
     h->diag = hdg_alloc(h->n_trace);
     h->dinv = hdg_alloc(h->n_trace);
-    hdg_diag_kernel<<<(unsigned)((h->n_trace + 255) / 256), 256, 0, h->stream>>>(
-        h->diag, h->de, h->n, mesh->n[0], mesh->n[1], mesh->n[2], h->fx, h->fy, h->bc, h->n_trace);
+    if (h->curved) {
+      if (degree > 4) throw Error{FEM_E_ARG, "HDG on deformed meshes (stored local inverses): degree 1..4"};
+      CurvTab ct{};
+      const int n = h->n;
+      for (int q = 0; q < n; ++q) {
+        ct.qw[q] = t1.qw[q];
+        ct.qp[q] = t1.qp[q];
+        for (int i = 0; i < n; ++i) {
+          ct.val[q][i] = t1.val[q][i];
+          ct.der[q][i] = t1.der[q][i];
+          ct.dco[q][i] = t1.colloc[q][i];
+        }
+      }
+      invert(n, ct.val, ct.vinv);
+      for (int d = 0; d < 3; ++d) {
+        ct.lo[d] = mesh->lo[d];
+        ct.len[d] = mesh->hi[d] - mesh->lo[d];
+        ct.h[d] = h->h[d];
+      }
+      ct.eps = mesh->deform_eps;
+      ct.tau = tau;
+      h->ctab = reinterpret_cast<CurvTab*>(hdg_alloc(kCurvDoubles));
+      FEM_CUDA_TRY(cudaMemcpyAsync(h->ctab, &ct, sizeof(CurvTab), cudaMemcpyHostToDevice, h->stream));
+      const int64_t M = (int64_t)n * n * n;
+      h->Sinv = hdg_alloc(h->n_cells * M * M);
+      switch (degree) {
+        case 1: curved_setup_k<1>(h.get()); break;
+        case 2: curved_setup_k<2>(h.get()); break;
+        case 3: curved_setup_k<3>(h.get()); break;
+        default: curved_setup_k<4>(h.get()); break;
+      }
+      h->dc = hdg_alloc(h->n_cells * 6 * NF);
+      HdgArgs a{};
+      a.y = h->dc;
+      launch_curved<kDiag>(h.get(), a);
+      hdg_curved_diag_kernel<<<(unsigned)((h->n_trace + 255) / 256), 256, 0, h->stream>>>(
+          h->diag, h->dc, h->n, mesh->n[0], mesh->n[1], mesh->n[2], h->fx, h->fy, h->bc, h->n_trace);
+    } else {
+      h->de = hdg_alloc(6 * NF);
+      HdgArgs a{};
+      a.y = h->de;
+      launch_cells<kDiag>(h.get(), a);
+      hdg_diag_kernel<<<(unsigned)((h->n_trace + 255) / 256), 256, 0, h->stream>>>(
+          h->diag, h->de, h->n, mesh->n[0], mesh->n[1], mesh->n[2], h->fx, h->fy, h->bc, h->n_trace);
+    }
     hdg_inv_kernel<<<grid_for(h->n_trace), 256, 0, h->stream>>>(h->dinv, h->diag, h->n_trace);
     count_launch(2);
     check_launch("hdg_diag");
@@ -931,7 +1657,7 @@ int hdg_apply(hdg_handle h, const double* lambda, int64_t n, double* y, int64_t 
     HdgArgs a{};
     a.lam = lambda;
     a.y = y;
-    launch_cells<kApply>(h, a);
+    launch_any<kApply>(h, a);
   });
 }
 
@@ -953,7 +1679,7 @@ int hdg_rhs(hdg_handle h, double* r, int64_t nr) {
     HdgArgs a{};
     a.F = h->F;
     a.y = r;
-    launch_cells<kRhs>(h, a);
+    launch_any<kRhs>(h, a);
   });
 }
 
@@ -972,7 +1698,7 @@ int hdg_local_solve(hdg_handle h, const double* lambda, int64_t n, int32_t with_
     a.F = with_f ? h->F : nullptr;
     a.u = u;
     a.q = q;
-    launch_cells<kRecover>(h, a);
+    launch_any<kRecover>(h, a);
   });
 }
 
@@ -984,6 +1710,7 @@ int hdg_mixed_apply(hdg_handle h, const double* qu, int64_t n, double* y, int64_
     check_dev(qu, "qu");
     check_dev(y, "y");
     if (qu == y) throw Error{FEM_E_ARG, "hdg_mixed_apply: y must not alias qu"};
+    if (h->mesh.deform_eps != 0.0) throw Error{FEM_E_ARG, "hdg_mixed_apply: Cartesian meshes only"};
     launch_mixed(h, qu, y);
   });
 }
@@ -1009,7 +1736,7 @@ int hdg_cg_solve(hdg_handle h, const double* b, int64_t nb, double* x, int64_t n
     HdgArgs a{};
     a.lam = x;
     a.y = h->q;
-    launch_cells<kApply>(h, a);   // q = K x0
+    launch_any<kApply>(h, a);   // q = K x0
     hdg_res_kernel<<<g, 256, 0, h->stream>>>(h->r, h->z, b, h->q, h->dinv, n);
     hdg_axpy_kernel<<<g, 256, 0, h->stream>>>(h->p, h->z, 0.0, n);
     count_launch(2);
@@ -1020,7 +1747,7 @@ int hdg_cg_solve(hdg_handle h, const double* b, int64_t nb, double* x, int64_t n
     while (rel > rtol && it < maxit) {
       a.lam = h->p;
       a.y = h->q;
-      launch_cells<kApply>(h, a);
+      launch_any<kApply>(h, a);
       const double pq = dot(h, h->p, h->q);
       if (!(pq > 0.0)) throw Error{FEM_E_BREAKDOWN, "hdg_cg_solve: p^T K p <= 0 at iteration " + std::to_string(it)};
       const double alpha = rz / pq;
@@ -1045,7 +1772,7 @@ int hdg_cg_solve(hdg_handle h, const double* b, int64_t nb, double* x, int64_t n
 void hdg_destroy(hdg_handle h) {
   if (!h) return;
   for (double* p : {reinterpret_cast<double*>(h->tab), h->de, h->diag, h->dinv, h->F, h->ydiag, h->r, h->p, h->q,
-                    h->z, h->part, h->scal, h->d1d})
+                    h->z, h->part, h->scal, h->d1d, reinterpret_cast<double*>(h->ctab), h->Sinv, h->dc})
     if (p) cudaFree(p);
   delete h;
 }

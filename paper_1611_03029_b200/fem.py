@@ -375,12 +375,13 @@ class Fem:
 
 
 class Hdg:
-    """One HDG handle (include/fem_hdg.h: hdg_setup ... hdg_destroy), Cartesian box meshes.
-    Vectors are CUDA float64 tensors (device pointers only)."""
+    """One HDG handle (include/fem_hdg.h: hdg_setup ... hdg_destroy), box meshes: Cartesian (fast
+    diagonalization of the local inverse) or the deformed map (deform_eps != 0; the local inverse
+    stored per cell, k <= 4).  Vectors are CUDA float64 tensors (device pointers only)."""
 
     def __init__(self, cells, degree, lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0), bc=(FEM_BC_DIRICHLET,) * 6,
-                 tau=5.0, stream=None):
-        m = _mesh(cells, lo, hi, 0.0, bc, 0, 1, None, None)
+                 tau=5.0, stream=None, deform_eps=0.0):
+        m = _mesh(cells, lo, hi, deform_eps, bc, 0, 1, None, None)
         s = None if stream is None else C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
         h = C.c_void_p()
         _check(_lib.hdg_setup(C.byref(m), degree, tau, s, C.byref(h)))

@@ -159,3 +159,57 @@ def test_errors():
                     torch.zeros(H.n_trace, dtype=torch.float64, device="cuda"))
     assert e.value.code == -2
     H.close()
+
+
+# ---- the paper's design: inner Schur complement inverse stored per cell (deformed meshes, and
+# Cartesian ones with FEM_HDG_DENSE=1)
+CURVED = [((2, 2, 2), 1, 0.05, (D, N, D, N, N, D)),
+          ((2, 3, 2), 2, 0.05, (D,) * 6),
+          ((2, 2, 2), 3, 0.05, (N, D, D, N, D, N)),
+          ((2, 2, 2), 4, 0.05, (D, D, N, N, D, D)),
+          ((3, 2, 2), 2, 0.0, (D, N, D, D, N, D))]
+
+
+@pytest.mark.parametrize("cells,k,eps,bc", CURVED)
+def test_stored_inverse_path_matches_oracle(cells, k, eps, bc, monkeypatch):
+    monkeypatch.setenv("FEM_HDG_DENSE", "1")
+    mesh = Mesh(cells, k, eps=eps, bc=bc)
+    op = ohdg.HdgOperator(mesh)
+    H = fem.Hdg(cells, k, bc=bc, deform_eps=eps)
+    x = fem_inputs.uniform_pm1(0, op.n)
+    y = torch.zeros(op.n, dtype=torch.float64, device="cuda")
+    H.hdg_apply(cuda(x), y)
+    assert rel(y.cpu().numpy(), op.apply(x)) <= 1e-11
+    d = torch.zeros_like(y)
+    H.hdg_diagonal(d)
+    assert rel(d.cpu().numpy(), op.diagonal()) <= 1e-11
+    r = torch.zeros_like(y)
+    H.hdg_rhs(r)
+    F = ohdg.load(mesh)
+    assert rel(r.cpu().numpy(), op.rhs(F)) <= 1e-11
+    m = (k + 1) ** 3
+    Qo, Uo = op.local_solve(x, F)
+    u = torch.zeros(mesh.n_cells * m, dtype=torch.float64, device="cuda")
+    q = torch.zeros(3 * mesh.n_cells * m, dtype=torch.float64, device="cuda")
+    H.hdg_local_solve(cuda(x), u, q, with_f=True)
+    assert rel(u.cpu().numpy(), Uo.ravel()) <= 1e-11
+    assert rel(q.cpu().numpy().reshape(3, mesh.n_cells, m).transpose(1, 0, 2), Qo) <= 1e-11
+    H.close()
+
+
+def test_deformed_solve_converges_at_order_k_plus_1():
+    errs = []
+    for n in (2, 4, 8):
+        mesh = Mesh((n,) * 3, 2, eps=0.05)
+        H = fem.Hdg((n,) * 3, 2, deform_eps=0.05)
+        b = torch.zeros(H.n_trace, dtype=torch.float64, device="cuda")
+        H.hdg_rhs(b)
+        lam = torch.zeros_like(b)
+        its, rr, ok = H.hdg_cg_solve(b, lam, rtol=1e-12)
+        assert ok
+        u = torch.zeros(H.n_cell_dofs, dtype=torch.float64, device="cuda")
+        H.hdg_local_solve(lam, u, with_f=True)
+        errs.append(problem.l2_error(mesh, SIPG, u.cpu().numpy()))
+        H.close()
+    rate = np.log2(errs[-2] / errs[-1])
+    assert rate >= 3 - 0.3, errs

@@ -223,6 +223,7 @@ struct fem_ctx {
   bool line_cell_fast = FEM_LINE_CELL_FAST != 0;   // Q4 line kernel: cells-fastest layout, G in kGLayoutCell8
   bool dg_kron = true;                 // FEM_DG_KRON=0: quadrature cell+face kernel on Cartesian SIPG levels
   bool cg_geo_fly = false;              // FEM_CG_GEO_FLY=1: deformed CG recomputes G from the analytic box map (measured slower: C2 apply 62.6 vs 57.1 us)
+  bool dg_cgeo_fly = false;            // FEM_DG_CGEO_FLY=1: deformed SIPG cell metric from the analytic map
   bool dg_fgeo_fly = false;            // FEM_DG_FGEO_FLY=1: deformed SIPG recomputes the face geometry (measured slower: C5 7.28 vs 5.35 ms)
   bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels (K1s, study)
   bool stencil2 = true;                // FEM_STENCIL2=0: warp-specialised assembled stencil (K1t) off

@@ -142,6 +142,12 @@ struct DgArgs {
   // per point measured slower (C5 apply 7.28 vs 5.35 ms): off by default, parity-tested.
   int fgeo_fly;
   MapArgs map;
+  // FEM_DG_CGEO_FLY=1: the cell term's metric G from the analytic map (cell_term.cuh GeoFly)
+  // instead of the 48-byte-per-point table: sin / cos per thread line and per cell z-point
+  // (parity-tested; measured slower, C5 apply 4710 -> 4868 us, solve 850 -> 872 ms: off)
+  int cgeo_fly;
+  GeoFlyC gfc;
+  double hL[3];    // h_d / L_d (quadrature coordinates t = hL (c + (xi + 1) / 2))
 };
 
 // result v = (A x)_i of DoF i: stored, or consumed by the fused Chebyshev epilogue
@@ -423,7 +429,7 @@ __device__ __forceinline__ void dg_faces(const DgArgs& A, const Tab<K + 1>& T, d
   __syncthreads();
 }
 
-template <int K, bool DEFORMED>
+template <int K, bool DEFORMED, bool FLY = false>
 __global__ void __launch_bounds__((K + 1) * (K + 1) * DgQCPB<K>::value, dgq_minb<K>())   // measured: 1 beats none at k <= 4
     dg_apply_kernel(DgArgs A, Tab<K + 1> T) {
   constexpr int N = K + 1, N2 = N * N, N3 = N2 * N;
@@ -433,7 +439,7 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgQCPB<K>::value, dgq_minb
   const int t = threadIdx.x, ci = threadIdx.y;
   const int64_t cell = A.cell0 + (int64_t)blockIdx.x * C + ci;
   const bool active = cell < A.cell1;
-  if (DEFORMED && t == 0 && ci == 0) {
+  if (DEFORMED && t == 0 && ci == 0 && !FLY) {
     // static geometry of the block's cells: pull it into L2 before waiting on the
     // predecessor kernel
     const int64_t c0 = A.cell0 + (int64_t)blockIdx.x * C;
@@ -475,8 +481,21 @@ __global__ void __launch_bounds__((K + 1) * (K + 1) * DgQCPB<K>::value, dgq_minb
     u[l] = active ? __ldg(A.x + cell * N3 + t + N2 * l) : 0.0;
     sm[L::X + t + N2 * l] = u[l];
   }
-  const CellGeo<N> geo{DEFORMED ? A.G + (size_t)(active ? cell : 0) * 6 * N3 : nullptr, A.c[0], A.c[1],
-                       A.c[2], active, nullptr};
+  CellGeo<N> geo{DEFORMED ? A.G + (size_t)(active ? cell : 0) * 6 * N3 : nullptr, A.c[0], A.c[1],
+                 A.c[2], active, nullptr};
+  GeoFlyPt<N> fp;
+  __shared__ double scz[FLY ? C : 1][FLY ? 2 * N : 1];
+  if constexpr (DEFORMED && FLY) {
+    const int ta = t % N, tb = t / N;
+    const int c3[3] = {c[0], c[1], c[2] + A.cz0};
+    auto tq = [&](int d, int q) { return A.hL[d] * (c3[d] + 0.5 * (T.qp[q] + 1.0)); };
+    sincospi(tq(0, ta), &fp.sx, &fp.cx);
+    sincospi(tq(1, tb), &fp.sy, &fp.cy);
+    if (t < N) sincospi(tq(2, t), &scz[ci][t], &scz[ci][N + t]);
+    fp.scz = scz[ci];
+    fp.c = &A.gfc;
+    geo.fly = &fp;   // read in the q-point phase, after the sweep barriers
+  }
   double* s0 = sm + L::S0;
   cell_laplace<N, DEFORMED, false, L::B, L::S>(T, geo, s0, s0 + L::CF, s0 + 2 * L::CF, t, u, v);
   __syncthreads();
@@ -969,6 +988,19 @@ DgArgs dg_args(const fem_ctx* h, const Level& L, const double* x, double* y) {
   for (int s = 0; s < 6; ++s)
     if (h->mesh.bc[s] == FEM_BC_DIRICHLET) mask |= 1 << s;
   A.bcmask = mask;
+  A.cgeo_fly = 0;
+  if (!L.cartesian && !mesh_general(h->mesh) && h->dg_cgeo_fly) {
+    A.cgeo_fly = 1;
+    for (int d = 0; d < 3; ++d) {
+      const double len = h->mesh.hi[d] - h->mesh.lo[d];
+      A.gfc.pl[d] = M_PI / len;
+      A.hL[d] = L.h[d] / len;
+    }
+    A.gfc.eps = h->mesh.deform_eps;
+    A.gfc.hh = (0.5 * L.h[0]) * (0.5 * L.h[1]) * (0.5 * L.h[2]);
+    const int ab[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+    for (int cc = 0; cc < 6; ++cc) A.gfc.ih[cc] = 4.0 / (L.h[ab[cc][0]] * L.h[ab[cc][1]]);
+  }
   A.fgeo_fly = 0;
   if (!L.cartesian && !mesh_general(h->mesh) && h->dg_fgeo_fly) {
     A.fgeo_fly = 1;
@@ -1003,12 +1035,17 @@ template <int K, bool DEF>
 void dg_apply_kd(fem_ctx* h, const Level& L, const double* x, double* y, int64_t r0, int64_t r1) {
   constexpr int N = K + 1, C = DgQCPB<K>::value;
   const size_t sm = sizeof(double) * DgSmem<N>::SIZE * C;
-  smem_attr(reinterpret_cast<const void*>(dg_apply_kernel<K, DEF>), (size_t)((int)sm));
   const unsigned grid = (unsigned)((r1 - r0 + C - 1) / C);
   DgArgs A = dg_args(h, L, x, y);
   A.cell0 = r0;
   A.cell1 = r1;
-  launch_pdl(h, dg_apply_kernel<K, DEF>, grid, dim3(N * N, C), sm, A, make_tab<N>(h->tab));
+  if (DEF && A.cgeo_fly) {
+    smem_attr(reinterpret_cast<const void*>(dg_apply_kernel<K, DEF, true>), (size_t)((int)sm));
+    launch_pdl(h, dg_apply_kernel<K, DEF, true>, grid, dim3(N * N, C), sm, A, make_tab<N>(h->tab));
+  } else {
+    smem_attr(reinterpret_cast<const void*>(dg_apply_kernel<K, DEF>), (size_t)((int)sm));
+    launch_pdl(h, dg_apply_kernel<K, DEF>, grid, dim3(N * N, C), sm, A, make_tab<N>(h->tab));
+  }
   count_launch();
   check_launch("dg_apply_kernel");
 }

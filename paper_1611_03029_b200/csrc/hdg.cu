@@ -80,22 +80,28 @@ struct HdgCfg {
   static constexpr int NF = N * N, N3 = N * N * N;
   static constexpr int CPB = std::max(1, 128 / NF);          // cells per block
   static constexpr int PER_CELL = 3 * 6 * NF + 2 * N3;       // lam, fz, ell, T1, T2
-  static constexpr int SMEM = kTabDoubles + CPB * PER_CELL;  // doubles
+  static constexpr int SMEM = CPB * PER_CELL;  // doubles
 };
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HDG_MINB) hdg_cell_kernel(HdgArgs a) {
+__global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HDG_MINB)
+    hdg_cell_kernel(HdgArgs a, const __grid_constant__ HdgTab T) {
+  // T: kernel parameter (constant bank): every compile-time-indexed coefficient is a uniform
+  // operand, no shared-memory load; the thread-indexed rows are preloaded from a.tab below
   constexpr int N = K + 1, NF = N * N, N3 = N * N * N;
   using Cfg = HdgCfg<N>;
   extern __shared__ double sm[];
-  HdgTab& T = *reinterpret_cast<HdgTab*>(sm);
-  {
-    const double* src = reinterpret_cast<const double*>(a.tab);
-    const int nt = blockDim.x * blockDim.y, tid = threadIdx.x + blockDim.x * threadIdx.y;
-    for (int i = tid; i < kTabDoubles; i += nt) sm[i] = src[i];
-  }
   const int t = threadIdx.x, ta = t % N, tb = t / N;
-  double* base = sm + kTabDoubles + threadIdx.y * Cfg::PER_CELL;
+  double Ma[N], Mb[N];
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) {
+    Ma[jj] = __ldg(&a.tab->M[ta][jj]);
+    Mb[jj] = __ldg(&a.tab->M[tb][jj]);
+  }
+  const double w2a = __ldg(&a.tab->w[2][ta]), w3a = __ldg(&a.tab->w[3][ta]), w4b = __ldg(&a.tab->w[4][tb]),
+               w5b = __ldg(&a.tab->w[5][tb]);
+  const double lxy = __ldg(&a.tab->lam[0][ta]) + __ldg(&a.tab->lam[1][tb]);
+  double* base = sm + threadIdx.y * Cfg::PER_CELL;
   double* lam = base;              // [6][NF]
   double* fz = lam + 6 * NF;       // [6][NF]
   double* ell = fz + 6 * NF;       // [6][NF]
@@ -133,8 +139,6 @@ __global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
       dir[s] = !inter[s] && ((a.bc >> s) & 1);
     }
   }
-  __syncthreads();   // table in shared memory
-
   // ---- inputs: the six faces' traces (constrained faces read as 0) and the load vector
   for (int s = 0; s < 6; ++s) {
     double v = 0.0;
@@ -147,17 +151,19 @@ __global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
     for (int i = t; i < N3; i += NF) T2[i] = active ? a.F[cell * N3 + i] : 0.0;
   __syncthreads();
   // ---- (1) l_s = (M (x) M) lambda_s, then t = sum_s w_s (x) l_s (+ F) on x-lines
+#pragma unroll
   for (int s = 0; s < 6; ++s) {
     double v = 0.0;
 #pragma unroll
-    for (int jj = 0; jj < N; ++jj) v = fma(T.M[ta][jj], lam[s * NF + jj + N * tb], v);
+    for (int jj = 0; jj < N; ++jj) v = fma(Ma[jj], lam[s * NF + jj + N * tb], v);
     fz[s * NF + t] = v;
   }
   __syncthreads();
+#pragma unroll
   for (int s = 0; s < 6; ++s) {
     double v = 0.0;
 #pragma unroll
-    for (int jj = 0; jj < N; ++jj) v = fma(T.M[tb][jj], fz[s * NF + ta + N * jj], v);
+    for (int jj = 0; jj < N; ++jj) v = fma(Mb[jj], fz[s * NF + ta + N * jj], v);
     ell[s * NF + t] = v;
   }
   __syncthreads();
@@ -167,10 +173,10 @@ __global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
 #pragma unroll
     for (int i0 = 0; i0 < N; ++i0) {
       double v = T.w[0][i0] * l0 + T.w[1][i0] * l1;
-      v = fma(T.w[2][ta], ell[2 * NF + i0 + N * tb], v);
-      v = fma(T.w[3][ta], ell[3 * NF + i0 + N * tb], v);
-      v = fma(T.w[4][tb], ell[4 * NF + i0 + N * ta], v);
-      v = fma(T.w[5][tb], ell[5 * NF + i0 + N * ta], v);
+      v = fma(w2a, ell[2 * NF + i0 + N * tb], v);
+      v = fma(w3a, ell[3 * NF + i0 + N * tb], v);
+      v = fma(w4b, ell[4 * NF + i0 + N * ta], v);
+      v = fma(w5b, ell[5 * NF + i0 + N * ta], v);
       if (a.F && (MODE == kRhs || MODE == kRecover)) v += T2[i0 + N * ta + NF * tb];
       line[i0] = v;
     }
@@ -202,7 +208,6 @@ __global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
     double g[N], hh[N];
 #pragma unroll
     for (int jj = 0; jj < N; ++jj) g[jj] = T2[ta + N * tb + NF * jj];
-    const double lxy = T.lam[0][ta] + T.lam[1][tb];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double v = 0.0;
@@ -251,6 +256,7 @@ __global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
   };
   if (MODE == kRecover) {
     if (a.q && active) {   // q_d on every node of the thread's d-line
+#pragma unroll
       for (int d = 0; d < 3; ++d) {
         const double ad = T.a[d];
         double g[N];
@@ -271,6 +277,7 @@ __global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
     return;
   }
   // ---- (3) z_s = tau lambda_s - sg_s q_d(l_s) - tau u(l_s) at the face points
+#pragma unroll
   for (int s = 0; s < 6; ++s) {
     const int d = s / 2, ly = (s & 1) ? K : 0;
     const double sg = (s & 1) ? 1.0 : -1.0, ad = T.a[d];
@@ -282,17 +289,19 @@ __global__ void __launch_bounds__(HdgCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
     fz[s * NF + t] = T.tau * (lam[s * NF + t] - uat(d, ly)) - sg * qn;
   }
   __syncthreads();
+#pragma unroll
   for (int s = 0; s < 6; ++s) {
     double v = 0.0;
 #pragma unroll
-    for (int jj = 0; jj < N; ++jj) v = fma(T.M[ta][jj], fz[s * NF + jj + N * tb], v);
+    for (int jj = 0; jj < N; ++jj) v = fma(Ma[jj], fz[s * NF + jj + N * tb], v);
     ell[s * NF + t] = v;
   }
   __syncthreads();
+#pragma unroll
   for (int s = 0; s < 6; ++s) {
     double v = 0.0;
 #pragma unroll
-    for (int jj = 0; jj < N; ++jj) v = fma(T.M[tb][jj], ell[s * NF + ta + N * jj], v);
+    for (int jj = 0; jj < N; ++jj) v = fma(Mb[jj], ell[s * NF + ta + N * jj], v);
     v *= T.J * T.a[s / 2];
     if (MODE == kDiag) {
       if (active && s == s0 && t == t0) a.y[j] = v;
@@ -321,7 +330,7 @@ struct MixCfg {
   static constexpr int NF = N * N, N3 = N * N * N;
   static constexpr int CPB = std::max(1, 128 / NF);
   static constexpr int PER_CELL = 9 * N3 + 6 * NF;   // Q[3], U, W[2], X[2], Yu; lambda^[6]
-  static constexpr int SMEM = kTabDoubles + CPB * PER_CELL;
+  static constexpr int SMEM = CPB * PER_CELL;
 };
 
 template <int N>
@@ -331,19 +340,13 @@ __device__ __forceinline__ int tidx(int e, int i, int ta, int tb) {   // node i 
 
 template <int K>
 __global__ void __launch_bounds__(MixCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HDG_MINB_MIX) hdg_mixed_kernel(
-    const double* __restrict__ qu, double* __restrict__ y, const HdgTab* tab, int nx, int ny, int nz, int bc,
-    int64_t ncells) {
+    const double* __restrict__ qu, double* __restrict__ y, const __grid_constant__ HdgTab T, int nx, int ny, int nz,
+    int bc, int64_t ncells) {
   constexpr int N = K + 1, NF = N * N, N3 = N * N * N;
   using Cfg = MixCfg<N>;
   extern __shared__ double sm[];
-  HdgTab& T = *reinterpret_cast<HdgTab*>(sm);
-  {
-    const double* src = reinterpret_cast<const double*>(tab);
-    const int nt = blockDim.x * blockDim.y, tid = threadIdx.x + blockDim.x * threadIdx.y;
-    for (int i = tid; i < kTabDoubles; i += nt) sm[i] = src[i];
-  }
   const int t = threadIdx.x, ta = t % N, tb = t / N;
-  double* Q = sm + kTabDoubles + threadIdx.y * Cfg::PER_CELL;   // [3][N3]
+  double* Q = sm + threadIdx.y * Cfg::PER_CELL;   // [3][N3]
   double* U = Q + 3 * N3;
   double* W = U + N3;       // [2][N3]
   double* X = W + 2 * N3;   // [2][N3]
@@ -361,6 +364,7 @@ __global__ void __launch_bounds__(MixCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
   {   // lambda^ on the six faces at the thread's face point
     const int c3[3] = {cx, cy, cz}, n3[3] = {nx, ny, nz};
     const int64_t step[3] = {1, nx, (int64_t)nx * ny};
+#pragma unroll
     for (int s = 0; s < 6; ++s) {
       const int d = s / 2, hi = s & 1, l = hi ? K : 0;
       const double sg = hi ? 1.0 : -1.0;
@@ -380,6 +384,7 @@ __global__ void __launch_bounds__(MixCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
     }
   }
   __syncthreads();
+#pragma unroll
   for (int d = 0; d < 3; ++d) {
     const int e1 = d == 0 ? 1 : 0, e2 = d == 2 ? 1 : 2;   // tangential directions
     const double ad = T.a[d];
@@ -1382,7 +1387,7 @@ void launch_cells_k(hdg_ctx* h, HdgArgs a) {
     else if (color >= 0) a.n_work = (int64_t)((a.nx + 1) / 2) * a.ny * a.nz;
     else a.n_work = h->n_cells;
     const int64_t blocks = (a.n_work + Cfg::CPB - 1) / Cfg::CPB;
-    kern<<<(unsigned)blocks, dim3(N * N, Cfg::CPB), sm, h->stream>>>(a);
+    kern<<<(unsigned)blocks, dim3(N * N, Cfg::CPB), sm, h->stream>>>(a, h->tab_host);
     count_launch();
     check_launch("hdg_cell_kernel");
   };
@@ -1419,7 +1424,7 @@ void launch_mixed_k(hdg_ctx* h, const double* qu, double* y) {
   FEM_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   const int64_t blocks = (h->n_cells + Cfg::CPB - 1) / Cfg::CPB;
-  kern<<<(unsigned)blocks, dim3(N * N, Cfg::CPB), sm, h->stream>>>(qu, y, h->tab, h->mesh.n[0], h->mesh.n[1],
+  kern<<<(unsigned)blocks, dim3(N * N, Cfg::CPB), sm, h->stream>>>(qu, y, h->tab_host, h->mesh.n[0], h->mesh.n[1],
                                                                     h->mesh.n[2], h->bc, h->n_cells);
   count_launch();
   check_launch("hdg_mixed_kernel");

@@ -114,7 +114,8 @@ typedef struct {
   const double* lambda_override;  /* host array [n_levels] or NULL (tests)        */
   void* stream;                   /* cudaStream_t; NULL => legacy default stream  */
   int32_t device;                 /* CUDA device ordinal; -1 => current device    */
-  int32_t profile;                /* 1 => time the operator kernels with events   */
+  int32_t profile;                /* 1 => time the finest PCG applies with events,
+                                     2 => time the finest-level smoother steps  */
   int32_t slab_min_layers;        /* multi-rank: a level is split into z-slabs while
                                      every rank keeps >= this many cell layers     [1] */
   int64_t slab_min_dofs;          /* ... and >= this many DoFs per rank; coarser
@@ -260,6 +261,13 @@ FEM_API int64_t fem_kernel_launches(void);
  * are not bracketed, so that the events do not perturb the solve) and every
  * fem_apply / fem_level_apply on the finest level. */
 FEM_API int fem_profile_read(fem_handle h, double* ms, int64_t* launches, int32_t reset);
+/* profile = 2: every Chebyshev step of the finest level (the fused smoother launches of
+ * R7, reading R8) of mg_smooth / mg_vcycle / cg_solve is bracketed; *bytes = their
+ * algorithmic bytes (read x, x_old if present, b; write x_new: 24 or 32 B per DoF). */
+FEM_API int fem_profile_read_bytes(fem_handle h, double* ms, int64_t* launches, double* bytes, int32_t reset);
+/* Switch the profile mode (0, 1, 2) of an existing handle; the cached PCG graphs are dropped
+ * (re-captured with the new event nodes on the next cg_solve). */
+FEM_API int fem_profile_mode(fem_handle h, int32_t mode);
 
 FEM_API const char* fem_last_error(void);
 FEM_API void fem_destroy(fem_handle h);

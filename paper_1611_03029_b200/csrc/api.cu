@@ -93,12 +93,13 @@ cudaEvent_t new_event() {
   return e;
 }
 
-void prof_begin(fem_ctx* h, bool finest) {
+void prof_begin(fem_ctx* h, bool finest, double bytes = 0.0) {
   if (!h->prof.on || !finest) return;
   if (h->prof.capturing) {
     // external record nodes: the events are really recorded on every replay, so
     // cudaEventElapsedTime works on them after the graph has run
     h->prof.cap->push_back({new_event(), new_event()});
+    if (h->prof.capb) h->prof.capb->push_back(bytes);
     FEM_CUDA_TRY(cudaEventRecordWithFlags(h->prof.cap->back().first, h->stream, cudaEventRecordExternal));
     return;
   }
@@ -110,6 +111,8 @@ void prof_begin(fem_ctx* h, bool finest) {
     }
   }
   FEM_CUDA_TRY(cudaEventRecord(h->prof.ev[h->prof.used], h->stream));
+  if (h->prof.evb.size() < h->prof.ev.size() / 2) h->prof.evb.resize(h->prof.ev.size() / 2);
+  h->prof.evb[h->prof.used / 2] = bytes;
 }
 
 void prof_end(fem_ctx* h, bool finest) {
@@ -130,18 +133,21 @@ void prof_collect(fem_ctx* h) {
     float ms = 0;
     FEM_CUDA_TRY(cudaEventElapsedTime(&ms, h->prof.ev[i], h->prof.ev[i + 1]));
     h->prof.ms += ms;
+    h->prof.bytes += h->prof.evb[i / 2];
   }
   h->prof.used = 0;
 }
 
 // elapsed time of the event pairs of a graph that has completed (stream synchronised)
-void prof_graph(fem_ctx* h, const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& ev) {
+void prof_graph(fem_ctx* h, const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& ev,
+                const std::vector<double>& evb) {
   if (!h->prof.on) return;
-  for (const auto& p : ev) {
+  for (size_t i = 0; i < ev.size(); ++i) {
     float ms = 0;
-    FEM_CUDA_TRY(cudaEventElapsedTime(&ms, p.first, p.second));
+    FEM_CUDA_TRY(cudaEventElapsedTime(&ms, ev[i].first, ev[i].second));
     h->prof.ms += ms;
     h->prof.launches += 1;
+    if (i < evb.size()) h->prof.bytes += evb[i];
   }
 }
 
@@ -253,7 +259,7 @@ void apply_level_overlap(fem_ctx* h, const Level& L, const double* x, double* y)
 
 void apply_level(fem_ctx* h, const Level& L, const double* x, double* y, bool set_constrained = true,
                  bool timed = false) {
-  const bool finest = timed && (&L == &h->levels.back());
+  const bool finest = timed && h->prof.mode == 1 && (&L == &h->levels.back());
   if (h->prof.on && finest && !h->prof.capturing && h->prof.used + 2 > 4096) prof_collect(h);
   if (L.dist && h->comm && h->overlap) {
     if (is_cg(h)) {
@@ -443,7 +449,12 @@ void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double
   // memory bound, the four extra epilogue streams cost more than the saved pass, C5 +0.6%)
   const bool fused = !is_cg(h) && h->fuse_cheb && L.cartesian && h->dg_kron;
   const bool st2 = h->fuse_cheb && use_stencil2(h, L);
+  // profile mode 2: time every step on the finest level, algorithmic bytes = read x, x_old (if
+  // any), b, write x_new (D^-1 from a class table or read: counted as not read)
+  const bool tsm = h->prof.mode == 2 && (&L == &h->levels.back());
   auto step = [&](const double* xc, const double* xold, double* xnew, double c1, double c2) {
+    if (tsm && !h->prof.capturing && h->prof.used + 2 > 4096) prof_collect(h);
+    prof_begin(h, tsm, 8.0 * (double)L.n_dofs * (xold ? 4 : 3));
     if (st2) {   // Chebyshev step in the stencil's epilogue: no A x vector at all
       launch_cg_stencil_cheb(h, L, xc, xold, b, xnew, c1, c2);
     } else if (fused) {
@@ -454,6 +465,7 @@ void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double
       apply_level(h, L, xc, L.t, false);
       launch_cheb_step(h, L, xnew, xc, xold, b, L.t, c1, c2, xold != nullptr);
     }
+    prof_end(h, tsm);
   };
   // step 1
   double* xn = (p == 1) ? x_out : next(x_in, nullptr);
@@ -672,17 +684,20 @@ struct Captured {
 };
 
 template <typename F>
-Captured capture(fem_ctx* h, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& ev, F&& body) {
+Captured capture(fem_ctx* h, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& ev, std::vector<double>& evb,
+                  F&& body) {
   cudaStream_t user = h->stream;
   Captured c;
   h->stream = h->cap_stream;
   h->prof.capturing = true;
   h->prof.cap = &ev;
+  h->prof.capb = &evb;
   g_capture_count = &c.kernels;
   auto restore = [&] {
     h->stream = user;
     h->prof.capturing = false;
     h->prof.cap = nullptr;
+    h->prof.capb = nullptr;
     g_capture_count = nullptr;
   };
   // the graph must not rely on buffer state observed at capture time
@@ -725,6 +740,8 @@ void drop_solve_graphs(fem_ctx* h) {
     }
     v->clear();
   }
+  h->sg.evb_pre.clear();
+  h->sg.evb_upd.clear();
   h->sg.g_pre = h->sg.g_upd = nullptr;
   h->sg.b = nullptr;
   h->sg.x = nullptr;
@@ -1120,6 +1137,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_NO_GRAPHS")) h->use_graphs = h->use_graphs && std::atoi(e) == 0;
     FEM_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
     h->prof.on = h->opt.profile != 0;
+    h->prof.mode = h->opt.profile;
     if (const char* e = std::getenv("FEM_GENERAL_PATH")) h->general_path = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_CHUNK_LAYERS")) h->chunk_layers = std::atoi(e);
     if (const char* e = std::getenv("FEM_PLANE")) h->plane_kernel = std::atoi(e) != 0;
@@ -1502,8 +1520,8 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     if (rnorm > rtol * bnorm) {
       if (h->use_graphs && (!h->sg.g_pre || h->sg.b != db || h->sg.x != dx)) {
         drop_solve_graphs(h);
-        Captured cp = capture(h, h->sg.ev_pre, body_pre);
-        Captured cu = capture(h, h->sg.ev_upd, body_upd);
+        Captured cp = capture(h, h->sg.ev_pre, h->sg.evb_pre, body_pre);
+        Captured cu = capture(h, h->sg.ev_upd, h->sg.evb_upd, body_upd);
         h->sg.g_pre = cp.exec;
         h->sg.g_upd = cu.exec;
         h->sg.k_pre = cp.kernels;
@@ -1527,8 +1545,8 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
         }
         FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
         if (h->use_graphs) {
-          prof_graph(h, h->sg.ev_pre);
-          prof_graph(h, h->sg.ev_upd);
+          prof_graph(h, h->sg.ev_pre, h->sg.evb_pre);
+          prof_graph(h, h->sg.ev_upd, h->sg.evb_upd);
         }
         ++it;
         if (h->comm) h->comm->check();
@@ -1569,14 +1587,31 @@ int fem_sync(fem_handle h) {
 }
 
 int fem_profile_read(fem_handle h, double* ms, int64_t* launches, int32_t reset) {
+  return fem_profile_read_bytes(h, ms, launches, nullptr, reset);
+}
+
+int fem_profile_mode(fem_handle h, int32_t mode) {
+  return guarded([&] {
+    check_handle(h);
+    if (mode < 0 || mode > 2) throw Error{FEM_E_ARG, "profile mode must be 0, 1 or 2"};
+    prof_collect(h);
+    drop_solve_graphs(h);
+    h->prof.on = mode != 0;
+    h->prof.mode = mode;
+  });
+}
+
+int fem_profile_read_bytes(fem_handle h, double* ms, int64_t* launches, double* bytes, int32_t reset) {
   return guarded([&] {
     check_handle(h);
     prof_collect(h);
     if (ms) *ms = h->prof.ms;
     if (launches) *launches = h->prof.launches;
+    if (bytes) *bytes = h->prof.bytes;
     if (reset) {
       h->prof.ms = 0;
       h->prof.launches = 0;
+      h->prof.bytes = 0;
     }
   });
 }

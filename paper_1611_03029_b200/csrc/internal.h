@@ -155,13 +155,17 @@ struct CgFuse {
 
 struct Profile {
   bool on = false;
+  int mode = 0;                  // fem_options.profile: 1 PCG applies, 2 finest-level smoother steps
   std::vector<cudaEvent_t> ev;   // pairs (start, stop) recorded eagerly
+  std::vector<double> evb;       // algorithmic bytes of each eager pair
   size_t used = 0;
   double ms = 0.0;
+  double bytes = 0.0;            // algorithmic bytes of the timed launches (mode 2)
   int64_t launches = 0;
   // while a graph is being captured, event pairs go here (owned by the graph)
   bool capturing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap = nullptr;
+  std::vector<double>* capb = nullptr;   // bytes of each captured pair
 };
 
 // One PCG iteration as two CUDA graphs (P:L1144-1148 loop body):
@@ -173,6 +177,7 @@ struct SolveGraphs {
   const double* b = nullptr;
   double* x = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pre, ev_upd;
+  std::vector<double> evb_pre, evb_upd;   // algorithmic bytes per timed launch (profile mode 2)
 };
 
 }  // namespace fem

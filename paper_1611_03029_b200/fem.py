@@ -88,6 +88,8 @@ def _load():
         "fem_sync": (C.c_int, [P]),
         "fem_kernel_launches": (I64, []),
         "fem_profile_read": (C.c_int, [P, C.POINTER(D), C.POINTER(I64), I32]),
+        "fem_profile_read_bytes": (C.c_int, [P, C.POINTER(D), C.POINTER(I64), C.POINTER(D), I32]),
+        "fem_profile_mode": (C.c_int, [P, I32]),
         "fem_last_error": (C.c_char_p, []),
         "fem_destroy": (None, [P]),
         # include/fem_hdg.h
@@ -114,7 +116,8 @@ SYMBOLS = ("fem_default_options", "fem_setup", "fem_partition", "fem_nccl_unique
            "fem_local_group_create", "fem_local_group_destroy", "fem_info", "fem_apply", "fem_diagonal", "mg_vcycle",
            "cg_solve", "cg_history", "fem_rhs", "fem_level_info", "fem_level_apply", "fem_level_diagonal",
            "fem_level_lambda", "fem_level_geometry", "mg_smooth", "mg_prolongate_add", "mg_restrict",
-           "mg_coarse_solve", "fem_sync", "fem_kernel_launches", "fem_profile_read", "fem_last_error",
+           "mg_coarse_solve", "fem_sync", "fem_kernel_launches", "fem_profile_read", "fem_profile_read_bytes", "fem_profile_mode",
+           "fem_last_error",
            "fem_destroy", "hdg_setup", "hdg_info", "hdg_apply", "hdg_diagonal", "hdg_rhs", "hdg_local_solve",
            "hdg_mixed_apply", "hdg_cg_solve", "hdg_destroy")
 
@@ -247,7 +250,7 @@ class Fem:
             o.stream = C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
         if device is not None:
             o.device = device
-        o.profile = 1 if profile else 0
+        o.profile = int(profile) if profile else 0   # True / 1: PCG applies, 2: finest smoother steps
         h = C.c_void_p()
         _check(_lib.fem_setup(C.byref(m), degree, method, C.byref(o), C.byref(h)))
         self.h = h
@@ -372,6 +375,14 @@ class Fem:
         ms, n = C.c_double(), C.c_int64()
         _check(_lib.fem_profile_read(self.h, C.byref(ms), C.byref(n), 1 if reset else 0))
         return ms.value, n.value
+
+    def fem_profile_read_bytes(self, reset=False):
+        ms, n, b = C.c_double(), C.c_int64(), C.c_double()
+        _check(_lib.fem_profile_read_bytes(self.h, C.byref(ms), C.byref(n), C.byref(b), 1 if reset else 0))
+        return ms.value, n.value, b.value
+
+    def fem_profile_mode(self, mode):
+        _check(_lib.fem_profile_mode(self.h, int(mode)))
 
 
 class Hdg:

@@ -335,3 +335,22 @@ def test_metric_recomputed_on_the_fly_matches_oracle(k, cells, monkeypatch):
     F.fem_apply(x, y)
     assert relmax(y, ocg.apply(m, x)) <= 1e-12
     F.close()
+
+
+def test_profile_mode_2_times_the_finest_smoother_steps(monkeypatch):
+    # fem_options.profile = 2: every finest-level Chebyshev step is bracketed by events and
+    # carries its algorithmic bytes (x, x_old if any, b read; x_new written): one mg_smooth from
+    # x != 0 is p = 5 steps, the first without x_old -> 8 n (3 + 4 * 4) bytes
+    fem = fem_mod()
+    monkeypatch.setenv("FEM_ST_MIN_CELLS", "1")
+    F = fem.Fem((8, 8, 8), 4, fem.FEM_CG, profile=2)
+    n = F.n_local
+    b = torch.ones(n, dtype=torch.float64, device="cuda")
+    x = torch.zeros_like(b)
+    F.mg_smooth(F.n_levels - 1, b, x, False)
+    ms, launches, nbytes = F.fem_profile_read_bytes(reset=True)
+    assert launches == 5 and ms > 0 and nbytes == 8.0 * n * (3 + 4 * 4)
+    F.fem_profile_mode(1)                      # back to the PCG-apply channel: smoothing not timed
+    F.mg_smooth(F.n_levels - 1, b, x, False)
+    assert F.fem_profile_read_bytes(reset=True)[1] == 0
+    F.close()

@@ -656,7 +656,10 @@ void stencil_k(fem_ctx* h, const Level& L, const StArgs& a0) {
   int ez = h->stencil_ez;
   if (ez <= 0) {
     const long tiles = (long)gx * gy;
-    ez = (int)std::lround((double)a.nz * tiles / (8.0 * 2 * 148));
+    // MODE 0 (no epilogue burst) prefers longer z-chunks -- fewer recomputed halo layers --
+    // over wave balance: C4 apply ez 16 -> 32: 747 -> 724 us (solve 118.6 -> 116.4 ms at 5 its); the
+    // fused step does not (ez 32 for it: 1591 -> 1646 us)
+    ez = (int)std::lround((double)a.nz * tiles / ((MODE == 0 ? 4.0 : 8.0) * 2 * 148));
     ez = std::max(4, std::min(ez, 32));
   }
   ez = std::max(1, std::min(ez, a.nz));

@@ -374,3 +374,34 @@ def trace_node_points(mesh: Mesh):
         xi[:, t1], xi[:, t2] = nodes[a], nodes[b]
         pts[fid[:, side]] = mesh.points(cc, xi)
     return pts.reshape(-1, 3)
+
+
+def postprocess(mesh: Mesh, Q, U):
+    """Element-by-element post-processing ([cgl09]): u* in Q_{k+1}(K) with
+        (grad u*, grad w)_K = -(q, grad w)_K   for all w in Q_{k+1}(K),   (u*, 1)_K = (u, 1)_K,
+    q = -grad u in the HDG sense (Q [n_cells, 3, m], U [n_cells, m] from local_solve).  GLL-nodal
+    Q_{k+1} basis, Gauss (k+2)^3 quadrature, the singular Neumann system closed by the mean
+    condition (one row replaced).  Returns u* [n_cells, (k+2)^3] (DG layout of degree k+1)."""
+    from .cg import CellQuadrature as CQ
+    from .mesh import eval_basis_3d
+    k = mesh.k
+    quad = CQ(k + 1)                                        # Gauss (k+2)^3, basis degree k+1
+    lo_nodes = Basis1D(k).nodes
+    val_lo, _ = eval_basis_3d(lo_nodes, quad.pts)           # degree-k basis at the points [q, m]
+    ms = (k + 2) ** 3
+    out = np.zeros((mesh.n_cells, ms))
+    for c0 in range(0, mesh.n_cells, 256):
+        cells = np.arange(c0, min(c0 + 256, mesh.n_cells))
+        Jinv, detJ = cell_geometry(mesh, cells, quad)
+        W = quad.w[None, :] * detJ                                          # [C, q]
+        phys = np.einsum('cqed,qei->cqdi', Jinv, quad.grad)                 # grad w_i at q [C, q, 3, i]
+        Kst = np.einsum('cq,cqdi,cqdj->cij', W, phys, phys)
+        qq = np.einsum('qj,cdj->cqd', val_lo, Q[cells])                     # q at the points
+        rhs = -np.einsum('cq,cqd,cqdi->ci', W, qq, phys)
+        mean_w = np.einsum('cq,qi->ci', W, quad.val)                        # (w_i, 1)
+        mean_u = np.einsum('cq,qj,cj->c', W, val_lo, U[cells])              # (u, 1)
+        A = Kst.copy()
+        A[:, 0, :] = mean_w                                                 # replace row 0: the mean
+        rhs[:, 0] = mean_u
+        out[cells] = np.linalg.solve(A, rhs[..., None])[..., 0]
+    return out

@@ -130,3 +130,51 @@ def test_diagonal_is_the_assembled_diagonal(eps):
     # symmetry, definiteness and the patch test); constrained rows 1
     op = hdg.HdgOperator(Mesh((2, 3, 2), 2, eps=eps, bc=(D, N, N, D, D, N)))
     assert np.abs(op.diagonal() - op.assemble().diagonal()).max() <= 1e-14 * np.abs(op.diagonal()).max()
+
+
+@pytest.mark.parametrize("k,eps", [(1, 0.0), (2, 0.0), (2, 0.05)])
+def test_postprocessing_superconverges_at_order_k_plus_2(k, eps):
+    # the element-by-element post-processed u* converges at rate k+2 (observed on
+    # hexahedra by the paper, "superconvergence ... for all constant-coefficient elliptic test
+    # cases"); its cell means equal those of u_h
+    errs, errs_u = [], []
+    for n in (2, 4, 8):
+        mesh = Mesh((n,) * 3, k, eps=eps)
+        op, lam, F = _solve(mesh)
+        Q, U = op.local_solve(lam, F)
+        us = hdg.postprocess(mesh, Q, U)
+        errs.append(problem.l2_error(Mesh((n,) * 3, k + 1, eps=eps), SIPG, us.ravel()))
+        errs_u.append(problem.l2_error(mesh, SIPG, U.ravel()))
+    rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert rates[-1] >= k + 2 - 0.3, (errs, rates)
+    assert errs[-1] < errs_u[-1]
+
+
+def test_postprocessing_reproduces_linear_u_and_keeps_cell_means():
+    # u = a.x + c: q = -a, u_h = u, so u* = u exactly; and (u*, 1)_K = (u_h, 1)_K on every cell
+    from oracle.cg import CellQuadrature
+    k = 2
+    mesh = Mesh((2, 2, 3), k, hi=(1.0, 1.2, 0.9))
+    a, c = np.array([0.3, -1.1, 0.7]), 0.25
+    m = (k + 1) ** 3
+    nodes = gll_nodes(k)
+    xi = np.stack([nodes[np.arange(m) % (k + 1)], nodes[(np.arange(m) // (k + 1)) % (k + 1)],
+                   nodes[np.arange(m) // (k + 1) ** 2]], -1)
+    U = mesh.points(mesh.cell_coords(), xi) @ a + c
+    Q = np.broadcast_to(-a[None, :, None], (mesh.n_cells, 3, m)).copy()
+    us = hdg.postprocess(mesh, Q, U)
+    m2 = (k + 2) ** 3
+    n2 = gll_nodes(k + 1)
+    xi2 = np.stack([n2[np.arange(m2) % (k + 2)], n2[(np.arange(m2) // (k + 2)) % (k + 2)],
+                    n2[np.arange(m2) // (k + 2) ** 2]], -1)
+    assert np.abs(us - (mesh.points(mesh.cell_coords(), xi2) @ a + c)).max() <= 1e-12
+    # means with a random (non-linear) input
+    rng = np.random.default_rng(3)
+    U = rng.standard_normal((mesh.n_cells, m))
+    Q = rng.standard_normal((mesh.n_cells, 3, m))
+    us = hdg.postprocess(mesh, Q, U)
+    q1, q2 = CellQuadrature(k + 1), CellQuadrature(k + 1)
+    from oracle.mesh import eval_basis_3d
+    v_lo, _ = eval_basis_3d(gll_nodes(k), q1.pts)
+    W = q1.w * np.prod(mesh.h / 2)
+    assert np.allclose(us @ (q2.val.T @ W), U @ (v_lo.T @ W), rtol=1e-12, atol=1e-12)

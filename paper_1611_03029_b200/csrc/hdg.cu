@@ -450,6 +450,131 @@ __global__ void __launch_bounds__(MixCfg<K + 1>::CPB * (K + 1) * (K + 1), FEM_HD
     if (active) y[3 * ncells * N3 + cell * N3 + i] = T.J * Yu[i];
 }
 
+
+// ---- element-by-element post-processing on Cartesian cells: u* in Q_{k+1} with
+//   (grad u*, grad w)_K = -(q, grad w)_K,  (u*, 1)_K = (u, 1)_K.
+// With the degree-(k+1) GLL basis (P = k+2 points, Gauss P-point rule) the stiffness is the
+// Kronecker sum J sum_d a_d^2 S* (x) M* (x) M* and the right-hand side
+//   -sum_d J a_d (C in slot d, X elsewhere) q_d,  C_ij = int phi*_i' phi_j,  X_ij = int phi*_i phi_j
+// (phi_j the degree-k basis of q); S* V = M* V Lambda (V^T M* V = I, Lambda_z = 0 for the constant
+// mode) gives u* = J^-1 V^(3) (sum a_d^2 Lambda)^-1 V^(3)T rhs on the other modes, plus the
+// constant mode fixed by the cell mean.
+struct PostTab {
+  double V[kMaxN + 1][kMaxN + 1];     // [i][mode] generalized eigenvectors (degree k+1)
+  double lam[kMaxN + 1];
+  double C[kMaxN + 1][kMaxN];         // [i*][j]
+  double X[kMaxN + 1][kMaxN];
+  double mk[kMaxN];                   // int phi_j (degree k)
+  double a2[3], a[3], J;
+  double vzsum;                       // (1^T M* v_z) for the constant mode
+  int z;                              // index of the constant mode
+};
+
+template <int K>
+__global__ void __launch_bounds__((K + 2) * (K + 2)) hdg_post_kernel(const double* __restrict__ q,
+                                                                       const double* __restrict__ u,
+                                                                       double* __restrict__ us,
+                                                                       const __grid_constant__ PostTab T,
+                                                                       int64_t ncells) {
+  constexpr int N = K + 1, P = K + 2, N3 = N * N * N, P3 = P * P * P;
+  __shared__ double A[P3], B[P3], R[P3], Qs[N3];
+  const int t = threadIdx.x, ta = t % P, tb = t / P;
+  const int64_t cell = blockIdx.x;
+  for (int i = t; i < P3; i += P * P) R[i] = 0.0;
+  // mean of u
+  __shared__ double umean;
+  if (t == 0) umean = 0.0;
+  __syncthreads();
+  for (int d = 0; d < 3; ++d) {
+    for (int i = t; i < N3; i += P * P) Qs[i] = q[(int64_t)d * ncells * N3 + cell * N3 + i];
+    __syncthreads();
+    // x: n -> P (lines over (y, z) in n^2)
+    if (ta < N && tb < N) {
+      double g[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) g[j] = Qs[j + N * ta + N * N * tb];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) v = fma(d == 0 ? T.C[i][j] : T.X[i][j], g[j], v);
+        A[i + P * ta + P * N * tb] = v;   // [P][N][N]
+      }
+    }
+    __syncthreads();
+    // y: n -> P (lines over (x*, z) in P x n)
+    if (tb < N) {
+      double g[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) g[j] = A[ta + P * j + P * N * tb];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) v = fma(d == 1 ? T.C[i][j] : T.X[i][j], g[j], v);
+        B[ta + P * i + P * P * tb] = v;   // [P][P][N]
+      }
+    }
+    __syncthreads();
+    // z: n -> P (lines over (x*, y*))
+    {
+      double g[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) g[j] = B[ta + P * tb + P * P * j];
+      const double f = -T.J * T.a[d];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) v = fma(d == 2 ? T.C[i][j] : T.X[i][j], g[j], v);
+        R[ta + P * tb + P * P * i] += f * v;
+      }
+    }
+    __syncthreads();
+  }
+  {   // (u, 1)_K = J sum_j mk x mk x mk u_j
+    double s = 0.0;
+    for (int i = t; i < N3; i += P * P) s += T.mk[i % N] * T.mk[(i / N) % N] * T.mk[i / (N * N)] * u[cell * N3 + i];
+    atomicAdd(&umean, s);   // shared-memory atomic (one block)
+  }
+  // FD: V^T in x, y, z; scale; V in z, y, x
+  auto sweep = [&](int e, const double* src, double* dst, bool trans) {
+    double g[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      g[i] = src[e == 0 ? i + P * ta + P * P * tb : e == 1 ? ta + P * i + P * P * tb : ta + P * tb + P * P * i];
+#pragma unroll
+    for (int o = 0; o < P; ++o) {
+      double v = 0.0;
+#pragma unroll
+      for (int i = 0; i < P; ++i) v = fma(trans ? T.V[i][o] : T.V[o][i], g[i], v);
+      dst[e == 0 ? o + P * ta + P * P * tb : e == 1 ? ta + P * o + P * P * tb : ta + P * tb + P * P * o] = v;
+    }
+  };
+  sweep(0, R, A, true);
+  __syncthreads();
+  sweep(1, A, B, true);
+  __syncthreads();
+  sweep(2, B, A, true);
+  __syncthreads();
+  for (int i = t; i < P3; i += P * P) {
+    const int i0 = i % P, i1 = (i / P) % P, i2 = i / (P * P);
+    if (i0 == T.z && i1 == T.z && i2 == T.z) {
+      A[i] = umean / (T.vzsum * T.vzsum * T.vzsum);   // the constant mode: (u*, 1)_K = (u, 1)_K (J cancels)
+    } else {
+      A[i] /= T.J * (T.a2[0] * T.lam[i0] + T.a2[1] * T.lam[i1] + T.a2[2] * T.lam[i2]);
+    }
+  }
+  __syncthreads();
+  sweep(2, A, B, false);
+  __syncthreads();
+  sweep(1, B, A, false);
+  __syncthreads();
+  sweep(0, A, B, false);
+  __syncthreads();
+  for (int i = t; i < P3; i += P * P) us[cell * P3 + i] = B[i];
+}
+
 // manufactured load F = (f, v), f = pi^2 sum_d (hi_d - lo_d)^-2 prod_d sin(pi t_d)
 __global__ void hdg_load_kernel(double* F, const double* qp, const double* qw, const double* val, int N,
                                 int nx, int ny, int nz, double lx, double ly, double lz, double hx, double hy,
@@ -1503,6 +1628,109 @@ void launch_any(hdg_ctx* h, const HdgArgs& a) {
   else launch_cells<MODE>(h, a);
 }
 
+double lagr1(const double* nodes, int n, int i, double z) {
+  double v = 1.0;
+  for (int j = 0; j < n; ++j)
+    if (j != i) v *= (z - nodes[j]) / (nodes[i] - nodes[j]);
+  return v;
+}
+double lagr1_d(const double* nodes, int n, int i, double z) {
+  double s = 0.0;
+  for (int m = 0; m < n; ++m) {
+    if (m == i) continue;
+    double t = 1.0 / (nodes[i] - nodes[m]);
+    for (int j = 0; j < n; ++j)
+      if (j != i && j != m) t *= (z - nodes[j]) / (nodes[i] - nodes[j]);
+    s += t;
+  }
+  return s;
+}
+
+void build_post_tab(int k, const double h[3], PostTab& T) {
+  Tables1D tk, tp;
+  build_tables(k, tk);
+  build_tables(k + 1, tp);   // degree k+1 basis, (k+2)-point Gauss rule
+  const int n = k + 1, p = k + 2;
+  T = PostTab{};
+  double Ms[kMaxN][kMaxN] = {}, Ss[kMaxN][kMaxN] = {};
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) {
+      double m = 0.0, st = 0.0;
+      for (int q = 0; q < p; ++q) {
+        m += tp.qw[q] * tp.val[q][i] * tp.val[q][j];
+        st += tp.qw[q] * tp.der[q][i] * tp.der[q][j];
+      }
+      Ms[i][j] = m;
+      Ss[i][j] = st;
+    }
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < n; ++j) {
+      double c = 0.0, x = 0.0;
+      for (int q = 0; q < p; ++q) {
+        const double pk = lagr1(tk.gll, n, j, tp.qp[q]);
+        c += tp.qw[q] * tp.der[q][i] * pk;
+        x += tp.qw[q] * tp.val[q][i] * pk;
+      }
+      T.C[i][j] = c;
+      T.X[i][j] = x;
+    }
+  for (int j = 0; j < n; ++j) {
+    double m = 0.0;
+    for (int q = 0; q < n; ++q) m += tk.qw[q] * tk.val[q][j];
+    T.mk[j] = m;
+  }
+  // S* V = M* V Lambda: Cholesky M* = R R^T, eig of R^-1 S* R^-T
+  double R[kMaxN][kMaxN] = {}, Ri[kMaxN][kMaxN] = {}, Cm[kMaxN][kMaxN] = {}, Q[kMaxN][kMaxN] = {};
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = Ms[i][j];
+      for (int m = 0; m < j; ++m) s -= R[i][m] * R[j][m];
+      R[i][j] = i == j ? std::sqrt(s) : s / R[j][j];
+    }
+  invert(p, R, Ri);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) {
+      double s = 0.0;
+      for (int a2 = 0; a2 < p; ++a2)
+        for (int b = 0; b < p; ++b) s += Ri[i][a2] * Ss[a2][b] * Ri[j][b];
+      Cm[i][j] = s;
+    }
+  for (int i = 0; i < p; ++i)
+    for (int j = i + 1; j < p; ++j) Cm[i][j] = Cm[j][i] = 0.5 * (Cm[i][j] + Cm[j][i]);
+  double lam[kMaxN];
+  sym_eig(p, Cm, Q, lam);
+  int z = 0;
+  for (int i = 1; i < p; ++i)
+    if (std::fabs(lam[i]) < std::fabs(lam[z])) z = i;
+  for (int i = 0; i < p; ++i) {
+    T.lam[i] = i == z ? 0.0 : lam[i];
+    for (int j = 0; j < p; ++j) {
+      double s = 0.0;
+      for (int m = 0; m < p; ++m) s += Ri[m][i] * Q[m][j];
+      T.V[i][j] = s;
+    }
+  }
+  T.z = z;
+  double vs = 0.0;   // 1^T M* v_z
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) vs += Ms[i][j] * T.V[j][z];
+  T.vzsum = vs;
+  T.J = h[0] * h[1] * h[2] / 8.0;
+  for (int d = 0; d < 3; ++d) {
+    T.a[d] = 2.0 / h[d];
+    T.a2[d] = T.a[d] * T.a[d];
+  }
+}
+
+template <int K>
+void post_k(hdg_ctx* h, const double* q, const double* u, double* us) {
+  PostTab T;
+  build_post_tab(K, h->h, T);
+  hdg_post_kernel<K><<<(unsigned)h->n_cells, (K + 2) * (K + 2), 0, h->stream>>>(q, u, us, T, h->n_cells);
+  count_launch();
+  check_launch("hdg_post_kernel");
+}
+
 unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8); }
 
 void ensure_load(hdg_ctx* h) {
@@ -1717,6 +1945,30 @@ int hdg_mixed_apply(hdg_handle h, const double* qu, int64_t n, double* y, int64_
     if (qu == y) throw Error{FEM_E_ARG, "hdg_mixed_apply: y must not alias qu"};
     if (h->mesh.deform_eps != 0.0) throw Error{FEM_E_ARG, "hdg_mixed_apply: Cartesian meshes only"};
     launch_mixed(h, qu, y);
+  });
+}
+
+int hdg_postprocess(hdg_handle h, const double* q, int64_t nq, const double* u, int64_t nu, double* ustar,
+                    int64_t nus) {
+  return hdg_guard([&] {
+    if (!h) throw Error{FEM_E_ARG, "null handle"};
+    if (h->mesh.deform_eps != 0.0) throw Error{FEM_E_ARG, "hdg_postprocess: Cartesian meshes only"};
+    if (h->k > kMaxDeg - 1) throw Error{FEM_E_ARG, "hdg_postprocess: degree 1..7 (u* has degree k+1)"};
+    const int64_t n3 = (int64_t)h->n * h->n * h->n, p3 = (int64_t)(h->n + 1) * (h->n + 1) * (h->n + 1);
+    if (nq != 3 * h->n_cells * n3 || nu != h->n_cells * n3 || nus != h->n_cells * p3)
+      throw Error{FEM_E_SIZE, "postprocess lengths"};
+    check_dev(q, "q");
+    check_dev(u, "u");
+    check_dev(ustar, "ustar");
+    switch (h->k) {
+      case 1: post_k<1>(h, q, u, ustar); break;
+      case 2: post_k<2>(h, q, u, ustar); break;
+      case 3: post_k<3>(h, q, u, ustar); break;
+      case 4: post_k<4>(h, q, u, ustar); break;
+      case 5: post_k<5>(h, q, u, ustar); break;
+      case 6: post_k<6>(h, q, u, ustar); break;
+      default: post_k<7>(h, q, u, ustar); break;
+    }
   });
 }
 

@@ -100,6 +100,7 @@ def _load():
         "hdg_rhs": (C.c_int, [P, P, I64]),
         "hdg_local_solve": (C.c_int, [P, P, I64, I32, P, I64, P, I64]),
         "hdg_mixed_apply": (C.c_int, [P, P, I64, P, I64]),
+        "hdg_postprocess": (C.c_int, [P, P, I64, P, I64, P, I64]),
         "hdg_cg_solve": (C.c_int, [P, P, I64, P, I64, D, I32, C.POINTER(I32), C.POINTER(D)]),
         "hdg_destroy": (None, [P]),
     }
@@ -119,7 +120,7 @@ SYMBOLS = ("fem_default_options", "fem_setup", "fem_partition", "fem_nccl_unique
            "mg_coarse_solve", "fem_sync", "fem_kernel_launches", "fem_profile_read", "fem_profile_read_bytes", "fem_profile_mode",
            "fem_last_error",
            "fem_destroy", "hdg_setup", "hdg_info", "hdg_apply", "hdg_diagonal", "hdg_rhs", "hdg_local_solve",
-           "hdg_mixed_apply", "hdg_cg_solve", "hdg_destroy")
+           "hdg_mixed_apply", "hdg_postprocess", "hdg_cg_solve", "hdg_destroy")
 
 
 def lib():
@@ -442,6 +443,13 @@ class Hdg:
         py, ny = _vec(y, True)
         _check(_lib.hdg_mixed_apply(self.h, px, nx, py, ny))
         return y
+
+    def hdg_postprocess(self, q, u, ustar):
+        pq, nq = _vec(q)
+        pu, nu = _vec(u)
+        ps, ns = _vec(ustar, True)
+        _check(_lib.hdg_postprocess(self.h, pq, nq, pu, nu, ps, ns))
+        return ustar
 
     def hdg_cg_solve(self, b, lam, rtol=1e-10, maxit=10000):
         pb, nb = _vec(b)

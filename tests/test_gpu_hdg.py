@@ -213,3 +213,39 @@ def test_deformed_solve_converges_at_order_k_plus_1():
         H.close()
     rate = np.log2(errs[-2] / errs[-1])
     assert rate >= 3 - 0.3, errs
+
+
+@pytest.mark.parametrize("cells,k,hi,bc", CASES[:4])
+def test_postprocessing_matches_oracle(cells, k, hi, bc):
+    mesh = Mesh(cells, k, hi=hi, bc=bc)
+    m = (k + 1) ** 3
+    rng = np.random.default_rng(k)
+    Q = rng.uniform(-1, 1, (mesh.n_cells, 3, m))
+    U = rng.uniform(-1, 1, (mesh.n_cells, m))
+    ref = ohdg.postprocess(mesh, Q, U)
+    H = fem.Hdg(cells, k, hi=hi, bc=bc)
+    us = torch.zeros(mesh.n_cells * (k + 2) ** 3, dtype=torch.float64, device="cuda")
+    H.hdg_postprocess(cuda(Q.transpose(1, 0, 2).ravel()), cuda(U.ravel()), us)
+    assert rel(us.cpu().numpy(), ref.ravel()) <= 1e-11
+    H.close()
+
+
+def test_postprocessed_solution_superconverges():
+    # GPU solve -> local recovery -> post-processing: order k + 2
+    k, errs = 2, []
+    for n in (4, 8, 16):
+        H = fem.Hdg((n,) * 3, k)
+        b = torch.zeros(H.n_trace, dtype=torch.float64, device="cuda")
+        H.hdg_rhs(b)
+        lam = torch.zeros_like(b)
+        its, rr, ok = H.hdg_cg_solve(b, lam, rtol=1e-12)
+        assert ok
+        u = torch.zeros(H.n_cell_dofs, dtype=torch.float64, device="cuda")
+        q = torch.zeros(3 * H.n_cell_dofs, dtype=torch.float64, device="cuda")
+        H.hdg_local_solve(lam, u, q, with_f=True)
+        us = torch.zeros(H.n_cells * (k + 2) ** 3, dtype=torch.float64, device="cuda")
+        H.hdg_postprocess(q, u, us)
+        errs.append(problem.l2_error(Mesh((n,) * 3, k + 1), SIPG, us.cpu().numpy()))
+        H.close()
+    rate = np.log2(errs[-2] / errs[-1])
+    assert rate >= k + 2 - 0.3, errs

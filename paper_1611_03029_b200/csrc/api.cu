@@ -742,6 +742,8 @@ void drop_solve_graphs(fem_ctx* h) {
   }
   h->sg.evb_pre.clear();
   h->sg.evb_upd.clear();
+  if (h->sg.g_loop) cudaGraphExecDestroy(h->sg.g_loop);
+  h->sg.g_loop = nullptr;
   h->sg.g_pre = h->sg.g_upd = nullptr;
   h->sg.b = nullptr;
   h->sg.x = nullptr;
@@ -1046,6 +1048,7 @@ void destroy(fem_ctx* h) {
   dfree(h->coarse_inv);
   dfree(h->red);
   dfree(h->scal);
+  dfree(h->sg.hist_dev);
   if (h->hscal) cudaFreeHost(h->hscal);
   for (auto& s : h->stage) dfree(s);
   if (h->geom_err) cudaFree(h->geom_err);
@@ -1059,6 +1062,80 @@ void destroy(fem_ctx* h) {
 }  // namespace fem
 
 using namespace fem;
+
+// On-device stopping test of the conditional PCG loop (R11, reading R13): scal[1] = (p, q),
+// scal[2] = (r, r) of this iteration, scal[6] = (b, b); scal[8] counts iterations, scal[9] flags a
+// breakdown, scal[10] = rtol, scal[11] = maxit; the relative residual goes to hist[it].
+__global__ void pcg_cond_kernel(cudaGraphConditionalHandle hc, double* scal, double* hist) {
+  const double pq = scal[1], rn = sqrt(scal[2]), bn = sqrt(scal[6]);
+  const double it = scal[8] + 1.0;
+  scal[8] = it;
+  const double rel = bn > 0 ? rn / bn : rn;
+  hist[(int)it] = rel;
+  scal[12] = rel;
+  const bool bad = !(pq > 0) || !isfinite(rn);
+  if (bad) scal[9] = 1.0;
+  cudaGraphSetConditional(hc, (!bad && rel > scal[10] && it < scal[11]) ? 1u : 0u);
+}
+
+namespace fem {
+// Build g_loop (see SolveGraphs).  Returns false (and remembers it) if the driver rejects the
+// conditional body, so that the host loop runs instead.
+template <typename F1, typename F2>
+bool build_cond_loop(fem_ctx* h, F1&& body_pre, F2&& body_upd) {
+  if (h->sg.cond_failed) return false;
+  cudaGraph_t g = nullptr;
+  cudaStream_t user = h->stream;
+  auto fail = [&](cudaGraph_t gg) {
+    if (gg) cudaGraphDestroy(gg);
+    cudaGetLastError();
+    h->stream = user;
+    g_capture_count = nullptr;
+    h->sg.cond_failed = true;
+    return false;
+  };
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return fail(nullptr);
+  cudaGraphConditionalHandle hc;
+  if (cudaGraphConditionalHandleCreate(&hc, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return fail(g);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) return fail(g);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if (!h->sg.hist_dev) h->sg.hist_dev = dalloc(kCondHist);
+  int64_t kernels = 0;
+  g_capture_count = &kernels;
+  h->stream = h->cap_stream;
+  for (auto& L : h->levels) L.t_zero = false;
+  if (cudaStreamBeginCaptureToGraph(h->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+      cudaSuccess)
+    return fail(g);
+  bool ok = true;
+  try {
+    body_pre();
+    body_upd();
+    pcg_cond_kernel<<<1, 1, 0, h->cap_stream>>>(hc, h->scal, h->sg.hist_dev);
+    ++kernels;
+  } catch (...) {
+    ok = false;
+  }
+  cudaGraph_t out = body;
+  const cudaError_t e = cudaStreamEndCapture(h->cap_stream, &out);
+  h->stream = user;
+  g_capture_count = nullptr;
+  if (!ok || e != cudaSuccess) return fail(g);
+  if (cudaGraphInstantiate(&h->sg.g_loop, g, 0) != cudaSuccess) {
+    h->sg.g_loop = nullptr;
+    return fail(g);
+  }
+  cudaGraphDestroy(g);
+  h->sg.k_iter = kernels;
+  return true;
+}
+}  // namespace fem
 
 extern "C" {
 
@@ -1458,6 +1535,7 @@ int fem_rhs(fem_handle h, double* b, int64_t nb) {
   });
 }
 
+
 int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, double rtol,
              int32_t maxit, int32_t* iters, double* relres) {
   int result = FEM_OK;
@@ -1535,7 +1613,36 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
       // first iteration through the same code: p = 0 and s0 = 1 make p = z + 0
       launch_zero(h, p, n);
       launch_set_scalar(h, 0, 1.0);
-      while (it < maxit) {
+      // the whole loop on the device (conditional WHILE graph, no host round trip per
+      // iteration): single rank, no profiling events, FEM_COND_GRAPH != 0
+      const char* cge = std::getenv("FEM_COND_GRAPH");
+      const bool cond = h->use_graphs && !h->prof.on && !h->comm && maxit < kCondHist && !(cge && std::atoi(cge) == 0);
+      if (cond && !h->sg.g_loop) {
+        auto upd_nocopy = [&] {
+          apply_level(h, L, p, q, false, true);
+          dot(h, L, p, q, 1);
+          launch_pcg_update_xr(h, dx, r, p, q, n);
+        };
+        build_cond_loop(h, body_pre, upd_nocopy);
+      }
+      if (cond && h->sg.g_loop) {
+        launch_set_scalar(h, 8, 0.0);
+        launch_set_scalar(h, 9, 0.0);
+        launch_set_scalar(h, 10, rtol);
+        launch_set_scalar(h, 11, (double)maxit);
+        FEM_CUDA_TRY(cudaGraphLaunch(h->sg.g_loop, h->stream));
+        FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 16, cudaMemcpyDeviceToHost, h->stream));
+        FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
+        it = (int)h->hscal[8];
+        g_launches += h->sg.k_iter * it;
+        std::vector<double> hh(it + 1);
+        FEM_CUDA_TRY(cudaMemcpy(hh.data(), h->sg.hist_dev, sizeof(double) * (it + 1), cudaMemcpyDeviceToHost));
+        for (int i = 1; i <= it; ++i) h->hist.push_back(hh[i]);
+        rnorm = h->hscal[12] * (bnorm > 0 ? bnorm : 1.0);
+        if (h->hscal[9] != 0.0)
+          throw Error{FEM_E_BREAKDOWN, "PCG breakdown at iteration " + std::to_string(it)};
+      }
+      while (!(cond && h->sg.g_loop) && it < maxit) {
         if (h->use_graphs) {
           launch_graph(h, h->sg.g_pre, h->sg.k_pre);
           launch_graph(h, h->sg.g_upd, h->sg.k_upd);

@@ -178,7 +178,14 @@ struct SolveGraphs {
   double* x = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pre, ev_upd;
   std::vector<double> evb_pre, evb_upd;   // algorithmic bytes per timed launch (profile mode 2)
+  // the whole PCG loop as one graph: a conditional WHILE node around both parts and an
+  // on-device stopping test (single rank, no profiling); cond_failed: not supported, host loop
+  cudaGraphExec_t g_loop = nullptr;
+  bool cond_failed = false;
+  int64_t k_iter = 0;
+  double* hist_dev = nullptr;   // [kCondHist] relative residuals of the device loop
 };
+constexpr int kCondHist = 4096;
 
 }  // namespace fem
 

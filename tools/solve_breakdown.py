@@ -13,6 +13,10 @@ difference is launch latency / dependency gaps.
 import collections
 import csv
 import os
+
+# ncu profiles the kernels of the per-iteration graphs; the single conditional-loop graph of
+# the default path hides them, so the breakdown uses the host loop
+os.environ.setdefault("FEM_COND_GRAPH", "0")
 import re
 import sys
 import time

@@ -221,7 +221,9 @@ def run_reference(args, w):
     if world > 1 and rank != 0:
         return
     ws, what = oracle_sample(w)
+    t_setup = time.perf_counter()
     mg, b = oracle_solver(ws)
+    t_setup = time.perf_counter() - t_setup
     n = mg.fine.n_dofs
     its = 0
     for _ in range(args.warmup):
@@ -239,9 +241,12 @@ def run_reference(args, w):
         "value": value, "unit": "DoF/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_desc(w), "n_dofs_global": w.n_dofs(), "cells": list(w.cells),
-                   "rtol": args.rtol, "parallelism": "CPU oracle (numpy, host cores)",
-                   "sample_cells": list(ws.cells), "sample_n_dofs": n, "iterations": its},
+        "config": {"workload": workload_desc(w), "n_dofs_global": w.n_dofs(), "n_dofs_local": w.n_dofs(),
+                   "rtol": args.rtol, "iterations": its, "cells": list(w.cells),
+                   "l2": "n/a (CPU oracle)", "parallelism": "CPU oracle (numpy, host cores)",
+                   "setup_s": round(t_setup, 3), "residual_history": None, "err_vs_x7": None,
+                   "sample_cells": list(ws.cells), "sample_n_dofs": n,
+                   "step_ms": [round(t * 1e3, 4) for t in times]},
         "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": cpu_threads(), "kind": "oracle",
                          "sample": f"each step = one full oracle GMG-PCG solve of {what} ({n} DoFs, "
                                    f"{its} iterations, setup untimed); value = sample DoFs / mean step time"},
@@ -619,6 +624,7 @@ def run_ours(args, w):
                    "setup_s": round(t_setup, 3),
                    "residual_history": [float("%.4e" % h) for h in hist],
                    "err_vs_x7": err_x7,
+                   "sample_cells": list(cells), "sample_n_dofs": F.n_global,
                    "step_ms": [round(s, 4) for s in step_ms]},
         "roofline": smoother_roofline,
         "apply_roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",

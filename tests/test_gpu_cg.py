@@ -354,3 +354,26 @@ def test_profile_mode_2_times_the_finest_smoother_steps(monkeypatch):
     F.mg_smooth(F.n_levels - 1, b, x, False)
     assert F.fem_profile_read_bytes(reset=True)[1] == 0
     F.close()
+
+
+def test_conditional_graph_loop_equals_host_loop(monkeypatch):
+    # the single-graph PCG loop (conditional WHILE node, on-device stopping test) and the host
+    # loop run the same kernels: same iteration count, residual history and solution
+    import torch
+    fem = fem_mod()
+    res = {}
+    for cond in ("1", "0"):
+        monkeypatch.setenv("FEM_COND_GRAPH", cond)
+        F = fem.Fem((8, 8, 8), 3, fem.FEM_CG, deform_eps=0.05, bc=MIXED)
+        b = torch.zeros(F.n_local, dtype=torch.float64, device="cuda")
+        F.fem_rhs(b)
+        x = torch.zeros_like(b)
+        its, rr, ok = F.cg_solve(b, x, rtol=1e-10)
+        x.zero_()
+        its2, rr2, ok2 = F.cg_solve(b, x, rtol=1e-10)     # second call: the cached graph
+        assert ok and ok2 and its == its2
+        res[cond] = (its, F.cg_history(), x.cpu().numpy())
+        F.close()
+    assert res["1"][0] == res["0"][0]
+    assert np.allclose(res["1"][1], res["0"][1], rtol=1e-9, atol=0)
+    assert relmax(res["1"][2], res["0"][2]) <= 1e-11

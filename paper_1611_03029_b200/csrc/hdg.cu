@@ -1634,18 +1634,6 @@ double lagr1(const double* nodes, int n, int i, double z) {
     if (j != i) v *= (z - nodes[j]) / (nodes[i] - nodes[j]);
   return v;
 }
-double lagr1_d(const double* nodes, int n, int i, double z) {
-  double s = 0.0;
-  for (int m = 0; m < n; ++m) {
-    if (m == i) continue;
-    double t = 1.0 / (nodes[i] - nodes[m]);
-    for (int j = 0; j < n; ++j)
-      if (j != i && j != m) t *= (z - nodes[j]) / (nodes[i] - nodes[j]);
-    s += t;
-  }
-  return s;
-}
-
 void build_post_tab(int k, const double h[3], PostTab& T) {
   Tables1D tk, tp;
   build_tables(k, tk);

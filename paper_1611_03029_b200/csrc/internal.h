@@ -316,7 +316,8 @@ void launch_add(fem_ctx* h, double* y, const double* x, int64_t n);  // y += x
 // Cartesian CG single-rank levels, k = 2..4: atomic-free assembled stencil (kernels_stencil.cu)
 inline bool use_stencil2(const fem_ctx* h, const Level& L) {
   return h->method == FEM_CG && h->stencil2 && L.cartesian && !L.dist && !h->general_path &&
-         h->k >= 1 && h->k <= 4 && L.n_cells >= h->stencil2_min_cells;
+         h->k >= 1 && h->k <= 4 && L.n_cells >= h->stencil2_min_cells &&
+         (int64_t)L.nn[0] * L.nn[1] < (int64_t(1) << 31);   // 32-bit in-plane offsets
 }
 void launch_cg_stencil_apply(fem_ctx* h, const Level& L, const double* x, double* y, bool setc);
 void launch_cg_stencil_cheb(fem_ctx* h, const Level& L, const double* x, const double* xo, const double* b,

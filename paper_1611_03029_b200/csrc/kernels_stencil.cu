@@ -195,6 +195,12 @@ __constant__ RefTab<K> cRef = RefTab<K>();
 #ifndef FEM_ST_SUSPEND_NS
 #define FEM_ST_SUSPEND_NS 100000
 #endif
+#ifndef FEM_ST_EPI   // MODE 1 / 2 epilogue addressing (write_element)
+#define FEM_ST_EPI 0
+#endif
+#ifndef FEM_ST_WP   // MODE 0 store: 1 st.global.wb, 0 generic store
+#define FEM_ST_WP 1
+#endif
 #ifndef FEM_ST_CBANK
 #define FEM_ST_CBANK 0
 #endif
@@ -235,6 +241,16 @@ template <int W>
 __device__ __forceinline__ void st_cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(W) : "memory"); }
 
 enum { kBarX = 1, kBarFull = 2, kBarEmpty = 4 };
+
+// a plane's base pointer made opaque to the compiler, so that an address is formed as
+// plane base + 32-bit in-plane offset (one IMAD.WIDE / LEA pair) instead of the 64-bit
+// re-associated (plane offset + node offset) * 8 + array base (5 instructions per access;
+// NX * NY < 2^31 is checked by use_stencil2)
+template <typename T>
+__device__ __forceinline__ T* st_plane(T* p) {
+  asm("mov.b64 %0, %0;" : "+l"(p));
+  return p;
+}
 
 // banded 1-D row of slot node r from 2K+1 consecutive values v (v[0] = node K(e-1)):
 // r = 0 the vertex (elements e-1: left, e: right), r >= 1 element e only.  STIFF selects
@@ -316,7 +332,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   const int gx = X0 + c;
   const int f = f0 + s;
   const bool colin = c < C::TX && gx < a.NX;
-  double* const ybase = a.y + gx + (int64_t)a.NX * (Y0 + K * s);
+  const int rowo0 = gx + a.NX * (Y0 + K * s);   // in-plane offset of the thread's row 0 (row r: + NX r)
   uint32_t rvalid = 0, rcons = 0;              // per row r: inside the domain / constrained (x, y)
   {
     const bool xm = ((bm & 1) && gx == 0) || ((bm & 2) && gx == a.NX - 1);
@@ -327,14 +343,16 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
       if (xm || ((bm & 4) && gy == 0) || ((bm & 8) && gy == a.NY - 1)) rcons |= 1u << r;
     }
   }
-  auto epilogue = [&](int64_t off, double v, bool m) {   // off = offset from ybase
+  auto epilogue = [&](int pz, int r, double v, bool m) {   // output (row r, plane pz)
+    const int64_t pb = NXY * pz;
+    const int o = rowo0 + a.NX * r;
     if constexpr (MODE == 0) {   // constrained rows: 0 here, x_c by launch_set_constrained
-      ybase[off] = m ? 0.0 : v;
+      __stwb(st_plane(a.y + pb) + o, m ? 0.0 : v);
     } else {   // D^-1 = 0 on constrained rows
-      const int64_t idx = (ybase - a.y) + off;
-      const double xv = a.x[idx];
-      const double xov = a.xo ? a.xo[idx] : 0.0;
-      ybase[off] = fma(a.c2 * a.dinv[idx], a.b[idx] - v, fma(a.c1, xv - xov, xv));
+      const double xv = __ldg(st_plane(a.x + pb) + o);
+      const double xov = MODE == 1 ? __ldg(st_plane(a.xo + pb) + o) : 0.0;
+      __stwb(st_plane(a.y + pb) + o,
+             fma(a.c2 * __ldg(st_plane(a.dinv + pb) + o), __ldg(st_plane(a.b + pb) + o) - v, fma(a.c1, xv - xov, xv)));
     }
   };
   // tiles holding only the far boundary column / row of a Dirichlet side: every output
@@ -344,7 +362,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     for (int pz = K * ez0; pz < q1; ++pz)
 #pragma unroll
       for (int r = 0; r < K; ++r)
-        if ((rvalid >> r) & 1u) epilogue((int64_t)a.NX * r + NXY * pz, 0.0, true);
+        if ((rvalid >> r) & 1u) epilogue(pz, r, 0.0, true);
     return;
   }
   if (tid == 0) {
@@ -370,7 +388,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     if (i >= NP) return;
     const int gz = pz0 + i;
     const bool zm = ((bm & 16) && gz == 0) || ((bm & 32) && gz == a.NZ - 1);
-    const double* src = a.x + (int64_t)gz * NXY;
+    const double* src = st_plane(a.x + (int64_t)gz * NXY);
     double* dst = Xt + (i % NB) * LR * LP;
     const uint32_t ok = zm ? 0u : ld_ok;   // source sizes of this plane's copies: 8 or 0 bytes
 #pragma unroll
@@ -496,10 +514,14 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   };
   auto write_plane = [&](int pz, int q) {   // MODE 0: c_y out[.][q] -> global plane pz
     const bool zm = ((bm & 16) && pz == 0) || ((bm & 32) && pz == a.NZ - 1);
+    double* yp = st_plane(a.y + NXY * pz);
 #pragma unroll
     for (int r = 0; r < K; ++r)
-      if ((rvalid >> r) & 1u)
-        epilogue((int64_t)a.NX * r + NXY * pz, a.cy * out[r][q], zm || ((rcons >> r) & 1u));
+      if ((rvalid >> r) & 1u) {
+        const double v = zm || ((rcons >> r) & 1u) ? 0.0 : a.cy * out[r][q];
+        if (FEM_ST_WP) __stwb(yp + rowo0 + a.NX * r, v);
+        else yp[rowo0 + a.NX * r] = v;
+      }
   };
   // MODE 1: node classes of D^-1 (see api.cu): 0 first node, r inside an element, K interior
   // vertex, K+1 last node
@@ -511,32 +533,54 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   // MODE 1: the element's K output planes (plus the top plane at the domain end): all
   // operand loads of a pair of planes are issued before any store (a store may alias them,
   // so the compiler would otherwise serialise one DRAM round trip per output)
-  const int64_t yoff = ybase - a.y;
   auto write_element = [&](int ez, int nq) {
 #pragma unroll
     for (int q = 0; q < N; ++q) {
       if (q >= nq) break;
       const int pz = K * ez + q;
       const int clz = (K + 2) * (K + 2) * ncls(pz, a.NZ);
-      const int64_t po = yoff + NXY * pz;
+#if FEM_ST_EPI == 0   // 64-bit node offsets (round-2 form)
+      const int64_t po = rowo0 + NXY * pz;
       const double* xp = a.x + po;
       const double* bp = a.b + po;
-      const double* op = a.xo ? a.xo + po : nullptr;
+      const double* op = MODE == 1 ? a.xo + po : nullptr;
+      double* yp = a.y + po;
+      auto ld = [](const double* p) { return *p; };
+      auto st = [](double* p, double v) { *p = v; };
+      const int ro = 0;
+#else   // plane base + 32-bit in-plane offset
+      const int64_t pb = NXY * pz;
+      const double* xp = st_plane(a.x + pb);
+      const double* bp = st_plane(a.b + pb);
+      const double* op = MODE == 1 ? st_plane(a.xo + pb) : nullptr;
+      double* yp = st_plane(a.y + pb);
+#if FEM_ST_EPI == 1
+      auto ld = [](const double* p) { return __ldg(p); };
+      auto st = [](double* p, double v) { __stwb(p, v); };
+#elif FEM_ST_EPI == 3
+      auto ld = [](const double* p) { return *p; };
+      auto st = [](double* p, double v) { *p = v; };
+#else
+      auto ld = [](const double* p) { return __ldcg(p); };
+      auto st = [](double* p, double v) { __stcg(p, v); };
+#endif
+      const int ro = rowo0;
+#endif
       double xv[K], xov[K], bv2[K];
 #pragma unroll
       for (int r = 0; r < K; ++r) {
         const bool ok = (rvalid >> r) & 1u;
-        xv[r] = ok ? xp[a.NX * r] : 0.0;
-        xov[r] = ok && op ? op[a.NX * r] : 0.0;
-        bv2[r] = ok ? bp[a.NX * r] : 0.0;
+        const int o = ro + a.NX * r;
+        xv[r] = ok ? ld(xp + o) : 0.0;
+        xov[r] = MODE == 1 && ok ? ld(op + o) : 0.0;
+        bv2[r] = ok ? ld(bp + o) : 0.0;
       }
-      double* yp = a.y + po;
 #pragma unroll
       for (int r = 0; r < K; ++r) {
         if (!((rvalid >> r) & 1u)) continue;
-        const double dv = a.dcls ? __ldg(a.dcls + clxy[r] + clz) : a.dinv[po + a.NX * r];
+        const double dv = __ldg(a.dcls + clxy[r] + clz);
         const double v = a.cy * out[r][q];
-        yp[a.NX * r] = fma(a.c2 * dv, bv2[r] - v, fma(a.c1, xv[r] - xov[r], xv[r]));
+        st(yp + ro + a.NX * r, fma(a.c2 * dv, bv2[r] - v, fma(a.c1, xv[r] - xov[r], xv[r])));
       }
     }
   };
@@ -546,7 +590,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   // DRAM round trip, so the warp prefetches its 4 rows x (K planes) x the arrays into L2
   // FEM_ST_PF_AHEAD elements ahead (lanes split the 256-byte row ranges).
   auto prefetch_epilogue = [&](int ez) {
-    if constexpr (MODE == 1) {
+    if constexpr (MODE != 0) {
       if (ez < ez0) return;
       const int nq = K + (ez + 1 == a.nz ? 1 : 0);
       const int ncol = min(C::TX, a.NX - X0);
@@ -554,8 +598,8 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
         const int arr = t & 3, rq = t >> 2, r = rq % K, q = rq / K;
         const int gy = Y0 + K * s + r;
         if (gy >= a.NY) continue;
-        const double* base = arr == 0 ? (FEM_ST_PF_X ? a.x : nullptr) : arr == 1 ? a.xo : arr == 2 ? a.b
-                                                                                   : (a.dcls ? nullptr : a.dinv);
+        const double* base = arr == 0 ? (FEM_ST_PF_X ? a.x : nullptr) : arr == 1 ? (MODE == 1 ? a.xo : nullptr)
+                                                                        : arr == 2 ? a.b : nullptr;
         if (!base) continue;
 #if FEM_ST_PF_LINES
         {   // per 128-byte line
@@ -704,11 +748,17 @@ void launch_cg_stencil_cheb(fem_ctx* h, const Level& L, const double* x, const d
   a.dcls = L.dinv_cls;
   a.c1 = c1;
   a.c2 = c2;
-  switch (h->k) {
-    case 1: stencil_k<1, 1>(h, L, a); break;
-    case 2: stencil_k<2, 1>(h, L, a); break;
-    case 3: stencil_k<3, 1>(h, L, a); break;
-    case 4: stencil_k<4, 1>(h, L, a); break;
+  if (!a.dcls) throw Error{FEM_E_ARG, "stencil Chebyshev step: no D^-1 class table"};
+  // MODE 1: x_old read; MODE 2: first step of the recurrence, x_old = 0 (no stream)
+  switch (h->k * 4 + (xo ? 1 : 2)) {
+    case 5: stencil_k<1, 1>(h, L, a); break;
+    case 6: stencil_k<1, 2>(h, L, a); break;
+    case 9: stencil_k<2, 1>(h, L, a); break;
+    case 10: stencil_k<2, 2>(h, L, a); break;
+    case 13: stencil_k<3, 1>(h, L, a); break;
+    case 14: stencil_k<3, 2>(h, L, a); break;
+    case 17: stencil_k<4, 1>(h, L, a); break;
+    case 18: stencil_k<4, 2>(h, L, a); break;
     default: throw Error{FEM_E_ARG, "stencil kernel: k in 1..4"};
   }
 }

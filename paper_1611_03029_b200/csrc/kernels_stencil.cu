@@ -69,6 +69,9 @@ namespace fem {
 #ifndef FEM_ST_ROT
 #define FEM_ST_ROT 1
 #endif
+#ifndef FEM_ST_SYM   // exactly symmetric 1-D tables (RefTab)
+#define FEM_ST_SYM 1
+#endif
 template <int K, int MODE = 0>
 struct StCfg {
   static constexpr int N = K + 1;
@@ -112,7 +115,7 @@ constexpr void ct_legendre(int n, double x, double& p, double& dp) {
   p = n == 0 ? 1.0 : p1;
   dp = n == 0 ? 0.0 : n * (x * p1 - p0) / (x * x - 1.0);
 }
-template <int K>
+template <int K, bool SYM = false>
 struct RefTab {
   static constexpr int N = K + 1;
   double gll[N] = {}, qp[N] = {}, qw[N] = {};
@@ -165,14 +168,30 @@ struct RefTab {
         M[i][j] = m;
         S[i][j] = s;
       }
+    // SYM: exact symmetry M_ij = M_ji = M_{K-i,K-j} (S likewise) -- mathematically so (GLL
+    // nodes and Gauss points symmetric about 0), in floating point up to an ulp.  With one
+    // value per orbit the k = 4 matrices hold 9 distinct coefficients instead of 25, and the
+    // compiler reuses registers across the sweeps instead of re-materialising near-equal
+    // literals (2 IMAD.MOV / UMOV per use)
+    if (SYM) {
+      for (int i = 0; i < N; ++i)
+        for (int j = 0; j < N; ++j) {
+          int bi = i, bj = j;
+          const int ci[3] = {j, K - i, K - j}, cj[3] = {i, K - j, K - i};
+          for (int t = 0; t < 3; ++t)
+            if (ci[t] < bi || (ci[t] == bi && cj[t] < bj)) bi = ci[t], bj = cj[t];
+          M[i][j] = M[bi][bj];
+          S[i][j] = S[bi][bj];
+        }
+    }
     for (int j = 0; j <= 2 * K; ++j) {
       Mv[j] = (j <= K ? M[K][j] : 0.0) + (j >= K ? M[0][j - K] : 0.0);
       Sv[j] = (j <= K ? S[K][j] : 0.0) + (j >= K ? S[0][j - K] : 0.0);
     }
   }
 };
-template <int K>
-__device__ constexpr RefTab<K> kRef{};
+template <int K, bool SYM = false>
+__device__ constexpr RefTab<K, SYM> kRef{};
 // the same tables in the constant bank: DFMAs take them as uniform-register operands
 // loaded two doubles per LDCU.128 (compile-time literals cost two UMOVs per use)
 template <int K>
@@ -195,7 +214,10 @@ __constant__ RefTab<K> cRef = RefTab<K>();
 #ifndef FEM_ST_SUSPEND_NS
 #define FEM_ST_SUSPEND_NS 100000
 #endif
-#ifndef FEM_ST_EPI   // MODE 1 / 2 epilogue addressing (write_element)
+// MODE 1 / 2 epilogue addressing (write_element): 0 = 64-bit node offsets, 1 = plane base +
+// 32-bit offsets (C4 smoother step 1480 us vs 1596-1842 us with __ldg / ld.global / generic /
+// .cg loads: the form that helps the x~ copies and the MODE 0 stores does not help here)
+#ifndef FEM_ST_EPI
 #define FEM_ST_EPI 0
 #endif
 #ifndef FEM_ST_WP   // MODE 0 store: 1 st.global.wb, 0 generic store
@@ -205,9 +227,9 @@ __constant__ RefTab<K> cRef = RefTab<K>();
 #define FEM_ST_CBANK 0
 #endif
 #if FEM_ST_CBANK
-#define ST_TAB(K) cRef<K>
+#define ST_TAB(K) cRef<K>  // (SYMT unused)
 #else
-#define ST_TAB(K) kRef<K>
+#define ST_TAB(K) kRef<K, SYMT>
 #endif
 
 struct StArgs {
@@ -255,7 +277,7 @@ __device__ __forceinline__ T* st_plane(T* p) {
 // banded 1-D row of slot node r from 2K+1 consecutive values v (v[0] = node K(e-1)):
 // r = 0 the vertex (elements e-1: left, e: right), r >= 1 element e only.  STIFF selects
 // the reference stiffness S instead of the mass M.
-template <int K, bool STIFF>
+template <int K, bool STIFF, bool SYMT>
 __device__ __forceinline__ double band_row(const double* v, int r, bool both, bool left) {
   double s = 0.0;
   if (r == 0) {
@@ -308,6 +330,9 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
     cg_stencil2_kernel(StArgs a) {
   FEM_PDL_ENTRY();
   using C = StCfg<K, MODE>;
+  // exactly symmetric tables for the apply (C4 665 vs 683 us); the fused step measured slower
+  // with them (1530 vs 1482 us: register allocation), so it keeps the computed ones
+  constexpr bool SYMT = FEM_ST_SYM && MODE == 0;
   constexpr int N = K + 1, SX = C::SX, LR = C::LR, LC = C::LC, LP = C::LP, ABP = C::ABP, NB = C::NB;
   constexpr int NAB = C::NAB;
   extern __shared__ double smem[];
@@ -457,13 +482,13 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
       const double wk = w[K];
       w[K] = edge ? 0.5 * wk : wk;
       double* bo = ao + LR * ABP;
-      ao[0] = band_row<K, false>(w, 0, true, false);
-      bo[0] = ISO ? band_row<K, true>(w, 0, true, false) : rx * band_row<K, true>(w, 0, true, false);
+      ao[0] = band_row<K, false, SYMT>(w, 0, true, false);
+      bo[0] = ISO ? band_row<K, true, SYMT>(w, 0, true, false) : rx * band_row<K, true, SYMT>(w, 0, true, false);
       w[K] = wk;
 #pragma unroll
       for (int r = 1; r < K; ++r) {
-        ao[r] = band_row<K, false>(w, r, true, false);
-        bo[r] = ISO ? band_row<K, true>(w, r, true, false) : rx * band_row<K, true>(w, r, true, false);
+        ao[r] = band_row<K, false, SYMT>(w, r, true, false);
+        bo[r] = ISO ? band_row<K, true, SYMT>(w, r, true, false) : rx * band_row<K, true, SYMT>(w, r, true, false);
       }
     }
   };
@@ -554,16 +579,8 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
       const double* bp = st_plane(a.b + pb);
       const double* op = MODE == 1 ? st_plane(a.xo + pb) : nullptr;
       double* yp = st_plane(a.y + pb);
-#if FEM_ST_EPI == 1
       auto ld = [](const double* p) { return __ldg(p); };
       auto st = [](double* p, double v) { __stwb(p, v); };
-#elif FEM_ST_EPI == 3
-      auto ld = [](const double* p) { return *p; };
-      auto st = [](double* p, double v) { *p = v; };
-#else
-      auto ld = [](const double* p) { return __ldcg(p); };
-      auto st = [](double* p, double v) { __stcg(p, v); };
-#endif
       const int ro = rowo0;
 #endif
       double xv[K], xov[K], bv2[K];

@@ -69,8 +69,11 @@ namespace fem {
 #ifndef FEM_ST_ROT
 #define FEM_ST_ROT 1
 #endif
-#ifndef FEM_ST_SYM   // exactly symmetric 1-D tables (RefTab)
+#ifndef FEM_ST_SYM   // exactly symmetric 1-D tables (RefTab) in the apply
 #define FEM_ST_SYM 1
+#endif
+#ifndef FEM_ST_SYMALL   // ... and in the fused Chebyshev step
+#define FEM_ST_SYMALL 0
 #endif
 template <int K, int MODE = 0>
 struct StCfg {
@@ -214,11 +217,17 @@ __constant__ RefTab<K> cRef = RefTab<K>();
 #ifndef FEM_ST_SUSPEND_NS
 #define FEM_ST_SUSPEND_NS 100000
 #endif
-// MODE 1 / 2 epilogue addressing (write_element): 0 = 64-bit node offsets, 1 = plane base +
-// 32-bit offsets (C4 smoother step 1480 us vs 1596-1842 us with __ldg / ld.global / generic /
-// .cg loads: the form that helps the x~ copies and the MODE 0 stores does not help here)
-#ifndef FEM_ST_EPI
-#define FEM_ST_EPI 0
+// MODE 1 / 2 epilogue (write_element): 64-bit node offsets.  Plane base + 32-bit offsets, the
+// form that helps the x~ copies and the MODE 0 stores, measured 1596-1842 us per C4 smoother
+// step vs 1480 us (with __ldg / ld.global / generic / .cg loads alike).
+#ifndef FEM_ST_EPI_DV   // the rows' D^-1 loads issued with the x, x_old, b loads (1451 vs 1481 us)
+#define FEM_ST_EPI_DV 1
+#endif
+// (plane q+1's operand loads issued before plane q's stores, in registers: 92 B of spills,
+// 1558 vs 1445 us; the __restrict__ function form below: neutral, the compiler still keeps the
+// plane order)
+#ifndef FEM_ST_EPI_FN   // __restrict__-parameter function form
+#define FEM_ST_EPI_FN 0
 #endif
 #ifndef FEM_ST_WP   // MODE 0 store: 1 st.global.wb, 0 generic store
 #define FEM_ST_WP 1
@@ -325,6 +334,40 @@ __device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// MODE 1 / 2 epilogue of one z-element as a function with __restrict__ parameters: the
+// compiler may then issue a plane's operand loads ahead of the previous plane's stores
+template <int K, int MODE>
+__device__ __forceinline__ void st_write_element(const double* __restrict__ x, const double* __restrict__ xo,
+                                                 const double* __restrict__ b, const double* __restrict__ dcls,
+                                                 double* __restrict__ y, const double (&out)[K][K + 1], int rowo0,
+                                                 int64_t NXY, int NX, int NZ, uint32_t rvalid, const int (&clxy)[K],
+                                                 int ez, int nq, double c1, double c2, double cy) {
+#pragma unroll
+  for (int q = 0; q <= K; ++q) {
+    if (q >= nq) break;
+    const int pz = K * ez + q;
+    const int cz = pz == 0 ? 0 : pz == NZ - 1 ? K + 1 : (pz % K == 0 ? K : pz % K);
+    const int clz = (K + 2) * (K + 2) * cz;
+    const int64_t po = rowo0 + NXY * pz;
+    double xv[K], xov[K], bv[K], dv[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const bool ok = (rvalid >> r) & 1u;
+      const int64_t o = po + (int64_t)NX * r;
+      xv[r] = ok ? x[o] : 0.0;
+      xov[r] = MODE == 1 && ok ? xo[o] : 0.0;
+      bv[r] = ok ? b[o] : 0.0;
+      dv[r] = dcls[clxy[r] + clz];
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      if (!((rvalid >> r) & 1u)) continue;
+      const double v = cy * out[r][q];
+      y[po + (int64_t)NX * r] = fma(c2 * dv[r], bv[r] - v, fma(c1, xv[r] - xov[r], xv[r]));
+    }
+  }
+}
+
 template <int K, int MODE, bool ISO>
 __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXREG)
     cg_stencil2_kernel(StArgs a) {
@@ -332,7 +375,7 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   using C = StCfg<K, MODE>;
   // exactly symmetric tables for the apply (C4 665 vs 683 us); the fused step measured slower
   // with them (1530 vs 1482 us: register allocation), so it keeps the computed ones
-  constexpr bool SYMT = FEM_ST_SYM && MODE == 0;
+  constexpr bool SYMT = FEM_ST_SYM && (MODE == 0 || FEM_ST_SYMALL);
   constexpr int N = K + 1, SX = C::SX, LR = C::LR, LC = C::LC, LP = C::LP, ABP = C::ABP, NB = C::NB;
   constexpr int NAB = C::NAB;
   extern __shared__ double smem[];
@@ -559,47 +602,38 @@ __global__ void __launch_bounds__(StCfg<K>::THREADS) __maxnreg__(StCfg<K>::MAXRE
   // operand loads of a pair of planes are issued before any store (a store may alias them,
   // so the compiler would otherwise serialise one DRAM round trip per output)
   auto write_element = [&](int ez, int nq) {
+#if FEM_ST_EPI_FN
+    st_write_element<K, MODE>(a.x, a.xo, a.b, a.dcls, a.y, out, rowo0, NXY, a.NX, a.NZ, rvalid, clxy, ez, nq,
+                              a.c1, a.c2, a.cy);
+#else
 #pragma unroll
     for (int q = 0; q < N; ++q) {
       if (q >= nq) break;
       const int pz = K * ez + q;
       const int clz = (K + 2) * (K + 2) * ncls(pz, a.NZ);
-#if FEM_ST_EPI == 0   // 64-bit node offsets (round-2 form)
       const int64_t po = rowo0 + NXY * pz;
       const double* xp = a.x + po;
       const double* bp = a.b + po;
       const double* op = MODE == 1 ? a.xo + po : nullptr;
       double* yp = a.y + po;
-      auto ld = [](const double* p) { return *p; };
-      auto st = [](double* p, double v) { *p = v; };
-      const int ro = 0;
-#else   // plane base + 32-bit in-plane offset
-      const int64_t pb = NXY * pz;
-      const double* xp = st_plane(a.x + pb);
-      const double* bp = st_plane(a.b + pb);
-      const double* op = MODE == 1 ? st_plane(a.xo + pb) : nullptr;
-      double* yp = st_plane(a.y + pb);
-      auto ld = [](const double* p) { return __ldg(p); };
-      auto st = [](double* p, double v) { __stwb(p, v); };
-      const int ro = rowo0;
-#endif
-      double xv[K], xov[K], bv2[K];
+      double xv[K], xov[K], bv2[K], dv[K];
 #pragma unroll
       for (int r = 0; r < K; ++r) {
         const bool ok = (rvalid >> r) & 1u;
-        const int o = ro + a.NX * r;
-        xv[r] = ok ? ld(xp + o) : 0.0;
-        xov[r] = MODE == 1 && ok ? ld(op + o) : 0.0;
-        bv2[r] = ok ? ld(bp + o) : 0.0;
+        xv[r] = ok ? xp[a.NX * r] : 0.0;
+        xov[r] = MODE == 1 && ok ? op[a.NX * r] : 0.0;
+        bv2[r] = ok ? bp[a.NX * r] : 0.0;
+        if (FEM_ST_EPI_DV) dv[r] = __ldg(a.dcls + clxy[r] + clz);
       }
 #pragma unroll
       for (int r = 0; r < K; ++r) {
         if (!((rvalid >> r) & 1u)) continue;
-        const double dv = __ldg(a.dcls + clxy[r] + clz);
+        if (!FEM_ST_EPI_DV) dv[r] = __ldg(a.dcls + clxy[r] + clz);
         const double v = a.cy * out[r][q];
-        st(yp + ro + a.NX * r, fma(a.c2 * dv, bv2[r] - v, fma(a.c1, xv[r] - xov[r], xv[r])));
+        yp[a.NX * r] = fma(a.c2 * dv[r], bv2[r] - v, fma(a.c1, xv[r] - xov[r], xv[r]));
       }
     }
+#endif
   };
 
   // MODE 1: the epilogue reads x, x_old, b (D^-1 from the class table) of the element's

@@ -223,6 +223,8 @@ __constant__ RefTab<K> cRef = RefTab<K>();
 #ifndef FEM_ST_EPI_DV   // the rows' D^-1 loads issued with the x, x_old, b loads (1451 vs 1481 us)
 #define FEM_ST_EPI_DV 1
 #endif
+// (prefetch.global.L1 of the operands 1 / 2 / all planes ahead inside the epilogue: 1459 / 1473
+// / 1469 vs 1447 us)
 // (plane q+1's operand loads issued before plane q's stores, in registers: 92 B of spills,
 // 1558 vs 1445 us; the __restrict__ function form below: neutral, the compiler still keeps the
 // plane order)

@@ -1236,6 +1236,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_DG_CGEO_FLY")) h->dg_cgeo_fly = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_CG_GEO_FLY")) h->cg_geo_fly = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_ST_MIN_CELLS")) h->stencil2_min_cells = std::atoll(e);
+    if (const char* e = std::getenv("FEM_GT_MIN_CELLS")) h->grid_transfer_min_cells = std::atoll(e);
     if (const char* e = std::getenv("FEM_ST_EZ")) h->stencil_ez = std::atoi(e);
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)

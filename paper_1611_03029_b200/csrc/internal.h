@@ -239,6 +239,7 @@ struct fem_ctx {
   bool dg_fgeo_fly = false;            // FEM_DG_FGEO_FLY=1: deformed SIPG recomputes the face geometry (measured slower: C5 7.28 vs 5.35 ms)
   bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels (K1s, study)
   bool stencil2 = true;                // FEM_STENCIL2=0: warp-specialised assembled stencil (K1t) off
+  int64_t grid_transfer_min_cells = 4096;  // FEM_GT_MIN_CELLS: node-grid CG transfers (k <= 4) onto coarse levels with >= this many local cells
   int64_t stencil2_min_cells = 32768;  // FEM_ST_MIN_CELLS: K1t on single-rank Cartesian CG levels with >= this many cells
                                        // (C4 solve, 5 its: 4096 118.6 ms, 32768 116.9, 262144 116.4-119.2, 2097152 124.4: below
                                        // 32^3 cells the few z-marching blocks of K1t are latency-bound, 47 us at 16^3)

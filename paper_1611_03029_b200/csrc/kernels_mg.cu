@@ -477,6 +477,244 @@ __global__ void restrict_elem_kernel(TransferArgs a, Embed<K, DG> E, const doubl
   }
 }
 
+// Node-grid form (CG, k <= 4, large levels): the CG vector of a structured level is a 3-D
+// grid of nodes and P = P1 (x) P1 (x) P1 with the banded global 1-D embedding P1 (fine node
+// f = 2k c + r of coarse cell c takes E[r][i] from coarse node k c + i).  A block takes a
+// strip of kGridTXC coarse cells along x of one (cy, cz) and a thread owns one fine x-node
+// of the strip: the fine vector is read / written as rows of ~128 consecutive doubles
+// (the element form above moves 2k+1 = 9-double rows and spends most of its instructions
+// on the index arithmetic of the element gather: ncu r02k, 940M instructions per launch,
+// issue-bound at 73%).  The x sweep goes through shared memory (coarse strip), the y and z
+// sweeps stay in the thread's registers with compile-time E operands.  Ownership and
+// constraints are exactly those of the element form (half-open cells, last cell closed),
+// so the z-slab exchanges around the transfers are unchanged.
+constexpr int kGridThreads = 160;   // 2k TXC fine nodes (<= 128) + the closing node of the last strip
+#ifndef FEM_GT_MINB
+#define FEM_GT_MINB 4               // resident blocks per SM the register allocation aims at
+#endif
+#ifndef FEM_GT_RMINB
+#define FEM_GT_RMINB 4              // the same for the restriction
+#endif
+#ifndef FEM_GT_RPIPE
+#define FEM_GT_RPIPE 0              // restriction: software-pipelined plane loads
+#endif
+#ifndef FEM_GT_RGROUPS
+#define FEM_GT_RGROUPS 2            // restriction: threads per coarse node in the x sweep
+#endif
+#ifndef FEM_GT_RNOATOM
+#define FEM_GT_RNOATOM 0            // timing experiment: plain stores instead of the atomics
+#endif
+
+template <int K>
+struct GridTile {
+  static constexpr int TXC = 64 / K;          // coarse cells per strip
+  static constexpr int FX = 2 * K * TXC;      // fine nodes per strip (half-open)
+  static constexpr int CW = K * TXC + 1;      // coarse nodes per strip (closed)
+};
+
+// xf += P xc
+template <int K>
+__global__ void __launch_bounds__(kGridThreads, FEM_GT_MINB)
+prolongate_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restrict__ xc,
+                       double* __restrict__ xf) {
+  FEM_PDL_ENTRY();
+  constexpr int N = K + 1, M = 2 * K + 1, TXC = GridTile<K>::TXC, CW = GridTile<K>::CW;
+  __shared__ double s_c[N * N][CW + 1];
+  __shared__ double sE[M][N];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < M * N; i += kGridThreads) sE[i / N][i % N] = E.E[i / N][i % N];
+  const int cx0 = blockIdx.x * TXC, cy = blockIdx.y, cz = blockIdx.z;
+  const int ncx = min(TXC, a.nc0 - cx0);
+  const bool last_x = cx0 + ncx == a.nc0, last_y = cy == a.nc1 - 1, last_z = a.czc0 + cz == a.ncz - 1;
+  if (tid <= K * ncx) {   // coarse strip, constrained values read as 0
+    const int gx = K * cx0 + tid;
+    const bool con_x = ((a.bcmask & 1) && gx == 0) || ((a.bcmask & 2) && gx == a.nnc0 - 1);
+#pragma unroll
+    for (int jl = 0; jl < N * N; ++jl) {
+      const int gy = K * cy + jl % N, gz = K * cz + jl / N;
+      const bool con = con_x || cg_constrained(a.bcmask & ~3, gx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2);
+      const double v = __ldg(xc + cg_index(gx, gy, gz, a.nnc0, a.nnc1));
+      s_c[jl][tid] = con ? 0.0 : v;
+    }
+  }
+  __syncthreads();
+  const int nfx = 2 * K * ncx + (last_x ? 1 : 0);   // fine nodes this strip owns along x
+  if (tid >= nfx) return;
+  const int cl = min(tid / (2 * K), ncx - 1), r = tid - 2 * K * cl;
+  double e[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) e[i] = sE[r][i];
+  double u[N * N];   // x sweep: u[j + N l]
+#pragma unroll
+  for (int jl = 0; jl < N * N; ++jl) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) s = fma(e[i], s_c[jl][K * cl + i], s);
+    u[jl] = s;
+  }
+  const int gx = 2 * K * cx0 + tid;
+  if (((a.bcmask & 1) && gx == 0) || ((a.bcmask & 2) && gx == a.nnf0 - 1)) return;
+  const int64_t row = a.nnf0, plane = (int64_t)a.nnf0 * a.nnf1;
+  double* __restrict__ out = xf + cg_index(gx, 2 * K * cy, 2 * K * cz, a.nnf0, a.nnf1);
+  const int gz0 = 2 * K * (a.czc0 + cz);
+#pragma unroll
+  for (int s = 0; s < M; ++s) {
+    if (s == 2 * K && !last_y) break;
+    const int gy = 2 * K * cy + s;
+    if (((a.bcmask & 4) && gy == 0) || ((a.bcmask & 8) && gy == a.nnf1 - 1)) continue;
+    double v[N];   // y sweep for this fine row
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) t = fma(E.E[s][j], u[j + N * l], t);
+      v[l] = t;
+    }
+    double old[M];
+    bool wr[M];
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+      const int gz = gz0 + t;
+      wr[t] = !(t == 2 * K && !last_z) && !(((a.bcmask & 16) && gz == 0) || ((a.bcmask & 32) && gz == a.nnf2 - 1));
+      old[t] = wr[t] ? out[s * row + t * plane] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+      double w = old[t];
+#pragma unroll
+      for (int l = 0; l < N; ++l) w = fma(E.E[t][l], v[l], w);
+      if (wr[t]) out[s * row + t * plane] = w;
+    }
+  }
+}
+
+// xc += P^T (bf - axf)   [axf may be null]; xc zeroed by the caller (atomics, as the element form)
+template <int K, bool AX>
+__global__ void __launch_bounds__(kGridThreads, FEM_GT_RMINB)
+restrict_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restrict__ bf,
+                     const double* __restrict__ axf, double* __restrict__ xc) {
+  FEM_PDL_ENTRY();
+  constexpr int N = K + 1, M = 2 * K + 1, TXC = GridTile<K>::TXC, FX = GridTile<K>::FX;
+  constexpr int SW = FX + 2;   // fine positions 0..FX of the strip (+1 pad)
+  __shared__ double s_u[N * N][SW];
+  __shared__ double sE[M][N];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < M * N; i += kGridThreads) sE[i / N][i % N] = E.E[i / N][i % N];
+  const int cx0 = blockIdx.x * TXC, cy = blockIdx.y, cz = blockIdx.z;
+  const int ncx = min(TXC, a.nc0 - cx0);
+  const bool last_x = cx0 + ncx == a.nc0, last_y = cy == a.nc1 - 1, last_z = a.czc0 + cz == a.ncz - 1;
+  const int nfx = 2 * K * ncx + (last_x ? 1 : 0);
+  const int gx = 2 * K * cx0 + tid;
+  const bool act = tid < nfx && !(((a.bcmask & 1) && gx == 0) || ((a.bcmask & 2) && gx == a.nnf0 - 1));
+  double u[N * N];
+#pragma unroll
+  for (int jl = 0; jl < N * N; ++jl) u[jl] = 0.0;
+  if (act) {
+    const int64_t row = a.nnf0, plane = (int64_t)a.nnf0 * a.nnf1;
+    const int64_t base = cg_index(gx, 2 * K * cy, 2 * K * cz, a.nnf0, a.nnf1);
+    const double* __restrict__ pb = bf + base;
+    const double* __restrict__ pa = AX ? axf + base : nullptr;
+    const int gz0 = 2 * K * (a.czc0 + cz);
+    // fine plane t of the strip: used (owned and not constrained in z)?  its (masked) row values
+    auto plane_used = [&](int t) {
+      const int gz = gz0 + t;
+      return !(t == 2 * K && !last_z) && !(((a.bcmask & 16) && gz == 0) || ((a.bcmask & 32) && gz == a.nnf2 - 1));
+    };
+    auto load_plane = [&](int t, double (&val)[M]) {
+#pragma unroll
+      for (int s = 0; s < M; ++s) {
+        const int gy = 2 * K * cy + s;
+        const bool rd = !(s == 2 * K && !last_y) && !(((a.bcmask & 4) && gy == 0) || ((a.bcmask & 8) && gy == a.nnf1 - 1));
+        // no control flow around the loads (a branch per load keeps the compiler from batching
+        // them: ncu r02l, 60% of the stall samples on the first use of each value): the masked
+        // rows read the strip's first value instead
+        const int64_t off = rd ? s * row + t * plane : 0;
+        double v = __ldg(pb + off);
+        if constexpr (AX) v -= __ldg(pa + off);
+        val[s] = rd ? v : 0.0;
+      }
+    };
+    auto add_plane = [&](int t, const double (&val)[M]) {
+      double p[N];   // y sweep of this fine plane
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double q = 0.0;
+#pragma unroll
+        for (int s = 0; s < M; ++s) q = fma(E.E[s][j], val[s], q);
+        p[j] = q;
+      }
+#pragma unroll
+      for (int l = 0; l < N; ++l)
+#pragma unroll
+        for (int j = 0; j < N; ++j) u[j + N * l] = fma(E.E[t][l], p[j], u[j + N * l]);
+    };
+#if FEM_GT_RPIPE
+    // software pipeline: the loads of plane t+1 are issued before plane t is reduced
+    double cur[M], nxt[M];
+    if (plane_used(0)) load_plane(0, cur);
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+      if (t + 1 < M && plane_used(t + 1)) load_plane(t + 1, nxt);
+      if (plane_used(t)) add_plane(t, cur);
+#pragma unroll
+      for (int s = 0; s < M; ++s) cur[s] = nxt[s];
+    }
+#else
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+      if (!plane_used(t)) continue;
+      double val[M];
+      load_plane(t, val);
+      add_plane(t, val);
+    }
+#endif
+  }
+  if (tid <= FX) {
+#pragma unroll
+    for (int jl = 0; jl < N * N; ++jl) s_u[jl][tid] = u[jl];
+  }
+  __syncthreads();
+  // x sweep: coarse node I of the strip collects the fine positions 2I - (2k-1) .. 2I + (2k-1);
+  // the (j, l) pairs of a node are dealt to kGridRG threads
+  constexpr int CWmax = GridTile<K>::CW;
+  constexpr int RG = kGridThreads / CWmax < FEM_GT_RGROUPS ? kGridThreads / CWmax : FEM_GT_RGROUPS;
+  const int I = tid % CWmax, g = tid / CWmax;
+  if (g >= RG || I > K * ncx) return;
+  const int gcx = K * cx0 + I;
+  if (((a.bcmask & 1) && gcx == 0) || ((a.bcmask & 2) && gcx == a.nnc0 - 1)) return;
+  double wt[4 * K - 1];
+#pragma unroll
+  for (int d = 0; d < 4 * K - 1; ++d) {
+    const int f = 2 * I + d - (2 * K - 1);
+    double w = 0.0;
+    if (f >= 0 && f <= 2 * K * ncx) {
+      const int c = min(f / (2 * K), ncx - 1), i = I - K * c;
+      if (i >= 0 && i <= K) w = sE[f - 2 * K * c][i];
+    }
+    wt[d] = w;
+  }
+  const int f0 = 2 * I - (2 * K - 1);
+#pragma unroll
+  for (int jl0 = 0; jl0 < N * N; jl0 += RG) {
+    const int jl = jl0 + g;
+    if (jl >= N * N) break;
+    const int gy = K * cy + jl % N, gz = K * cz + jl / N;
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < 4 * K - 1; ++d) {
+      const int f = min(max(f0 + d, 0), FX);
+      s = fma(wt[d], s_u[jl][f], s);
+    }
+    if (!cg_constrained(a.bcmask & ~3, gcx, gy, K * a.czc0 + gz, a.nnc0, a.nnc1, a.nnc2)) {
+#if FEM_GT_RNOATOM
+      xc[cg_index(gcx, gy, gz, a.nnc0, a.nnc1)] = s;   // timing experiment only (wrong sums)
+#else
+      atomicAdd(xc + cg_index(gcx, gy, gz, a.nnc0, a.nnc1), s);
+#endif
+    }
+  }
+}
+
 // ---------------------------------------------------------------- vectors
 __global__ void cheb_step_kernel(double* __restrict__ xn, const double* __restrict__ x,
                                  const double* __restrict__ xo, const double* __restrict__ b,
@@ -701,6 +939,16 @@ Embed<K, DG> make_embed(const Tables1D& t) {
 template <int K, bool DG>
 void prolongate_kd(fem_ctx* h, const Level& c, const Level& f, const double* xc, double* xf) {
   constexpr int N = K + 1, M = Embed<K, DG>::M;
+  if constexpr (!DG && K <= 4) {
+    if (c.n_cells >= h->grid_transfer_min_cells) {
+      const dim3 grid((unsigned)((c.n[0] + GridTile<K>::TXC - 1) / GridTile<K>::TXC), (unsigned)c.n[1], (unsigned)c.n[2]);
+      launch_pdl(h, prolongate_grid_kernel<K>, grid, kGridThreads, 0, transfer_args(h, c, f),
+                 make_embed<K, DG>(h->tab), xc, xf);
+      count_launch();
+      check_launch("prolongate_grid_kernel");
+      return;
+    }
+  }
   if constexpr (!DG) {
     const size_t sm = sizeof(double) * (N * N * N + M * N * N + M * M * N);
     smem_attr(reinterpret_cast<const void*>(prolongate_elem_kernel<K, DG>), (size_t)((int)sm));
@@ -720,6 +968,20 @@ template <int K, bool DG>
 void restrict_kd(fem_ctx* h, const Level& c, const Level& f, const double* bf, const double* axf,
                  double* xc) {
   constexpr int N = K + 1, M = Embed<K, DG>::M;
+  if constexpr (!DG && K <= 4) {
+    if (c.n_cells >= h->grid_transfer_min_cells) {
+      const dim3 grid((unsigned)((c.n[0] + GridTile<K>::TXC - 1) / GridTile<K>::TXC), (unsigned)c.n[1], (unsigned)c.n[2]);
+      if (axf)
+        launch_pdl(h, restrict_grid_kernel<K, true>, grid, kGridThreads, 0, transfer_args(h, c, f),
+                   make_embed<K, DG>(h->tab), bf, axf, xc);
+      else
+        launch_pdl(h, restrict_grid_kernel<K, false>, grid, kGridThreads, 0, transfer_args(h, c, f),
+                   make_embed<K, DG>(h->tab), bf, axf, xc);
+      count_launch();
+      check_launch("restrict_grid_kernel");
+      return;
+    }
+  }
   if constexpr (!DG) {
     const size_t sm = sizeof(double) * (M * M * M + N * M * M);
     smem_attr(reinterpret_cast<const void*>(restrict_elem_kernel<K, DG>), (size_t)((int)sm));

@@ -377,3 +377,30 @@ def test_conditional_graph_loop_equals_host_loop(monkeypatch):
     assert res["1"][0] == res["0"][0]
     assert np.allclose(res["1"][1], res["0"][1], rtol=1e-9, atol=0)
     assert relmax(res["1"][2], res["0"][2]) <= 1e-11
+
+
+# node-grid CG transfers (kernels_mg.cu prolongate_grid_kernel / restrict_grid_kernel): forced onto
+# every level (FEM_GT_MIN_CELLS=1), several x strips with a ragged last strip (coarse n_x > 64/k),
+# unmasked inputs (constrained entries must be ignored on input and left alone on output), and
+# the element form (FEM_GT_MIN_CELLS huge) on the same inputs
+@pytest.mark.parametrize("k,cells,bc", [
+    (4, (40, 4, 2), MIXED), (4, (8, 6, 4), (DIRICHLET,) * 6), (3, (48, 2, 4), MIXED),
+    (2, (72, 4, 2), MIXED), (1, (136, 2, 2), (DIRICHLET,) * 6),
+    (4, (4, 2, 6), (NEUMANN, NEUMANN, DIRICHLET, NEUMANN, NEUMANN, NEUMANN)),
+])
+@pytest.mark.parametrize("min_cells", ["1", "1000000000"])
+def test_grid_and_element_transfers_match_oracle(k, cells, bc, min_cells, monkeypatch):
+    monkeypatch.setenv("FEM_GT_MIN_CELLS", min_cells)
+    F, m = make(cells, k, 0.0, bc)
+    mg = omg.Multigrid(m, CG)
+    for l in range(1, F.n_levels):
+        lev, cm = mg.levels[l], mg.levels[l - 1]
+        xc = fem_inputs.uniform_pm1(300 + l, cm.n_dofs)
+        xf = fem_inputs.uniform_pm1(400 + l, lev.n_dofs)
+        out = xf.copy()
+        F.mg_prolongate_add(l, xc, out)
+        assert relmax(out, xf + mg.prolongate(l, xc)) <= 1e-12, ("prolongate", l)
+        rc = np.full(cm.n_dofs, 7.0)          # the restriction overwrites its output
+        F.mg_restrict(l, xf, rc)
+        assert relmax(rc, mg.restrict(l, xf)) <= 1e-12, ("restrict", l)
+    F.close()

@@ -134,7 +134,10 @@ def test_apply_diagonal_rhs_match_single_rank_and_oracle(method, k, cells, eps, 
 
 
 @pytest.mark.parametrize("method,k,cells,eps,bc,P,mnl", CASES)
-def test_levels_and_transfers_match_single_rank(method, k, cells, eps, bc, P, mnl):
+def test_levels_and_transfers_match_single_rank(method, k, cells, eps, bc, P, mnl, monkeypatch):
+    # the single-rank reference uses the element-form CG transfers, the ranks the node-grid form
+    # (both forms against the oracle: test_gpu_cg.py)
+    monkeypatch.setenv("FEM_GT_MIN_CELLS", "1000000000")
     fem = fem_mod()
     kw = kw_of(method, k, cells, eps, bc, mnl)
     F1 = fem.Fem(**kw)
@@ -160,6 +163,7 @@ def test_levels_and_transfers_match_single_rank(method, k, cells, eps, bc, P, mn
             F1.mg_restrict(l, xf, rc)
             ref[("prol", l)], ref[("rest", l)] = pf, rc
     F1.close()
+    monkeypatch.setenv("FEM_GT_MIN_CELLS", "1")
 
     def body(F, r):
         got = {}

@@ -42,6 +42,16 @@ def run(w, solve=True):
         xs = torch.zeros_like(x)
         ms_s = timeit(lambda: F.mg_smooth(L, b, xs, False), reps=10)
         print(f"   smooth (5 steps from x != 0): {ms_s*1e3:.1f}us = {ms_s*1e3/5:.1f}us per step", flush=True)
+    if __import__("os").environ.get("PROBE_TRANSFER") == "1":   # finest-level transfers
+        L = F.n_levels - 1
+        nc = F.level_info(L - 1)[0]
+        xc = torch.from_numpy(fem_inputs.uniform_pm1(3, nc)).cuda()
+        rc = torch.zeros_like(xc)
+        xf = x.clone()
+        ms_p = timeit(lambda: F.mg_prolongate_add(L, xc, xf), reps=10)
+        ms_r = timeit(lambda: F.mg_restrict(L, x, rc), reps=10)
+        print(f"   transfers: prolongate_add {ms_p*1e3:.1f}us ({(16*n+8*nc)/ms_p/1e6:.0f} GB/s)  "
+              f"restrict (incl. zero) {ms_r*1e3:.1f}us ({(8*n+8*nc)/ms_r/1e6:.0f} GB/s)", flush=True)
     if solve:
         b = torch.zeros_like(x)
         F.fem_rhs(b) if w.rhs == "manufactured" else F.fem_apply(x, b)

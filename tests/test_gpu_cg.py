@@ -284,6 +284,49 @@ def test_c4_full_size_sampled_apply_and_exact_solution():
     assert ok and its <= 8
     err = (xs - xd)[~bm]
     assert (err.norm() / xd[~bm].norm()).item() < 1e-8
+    del xs, b, y
+    # finest-level transfers at full size, in the launch configuration of the bench (node-grid
+    # kernels): sampled fine / coarse nodes against P = P1 (x) P1 (x) P1 built from the oracle's
+    # 1-D embedding, constrained nodes ignored on input and untouched on output
+    L = F.n_levels - 1
+    ncd, ccells = F.level_info(L - 1)
+    P1 = otr._cg_1d(w.degree, ccells[0])            # [fine nodes, coarse nodes] per direction
+    NF, NC = P1.shape
+    assert NF ** 3 == n and NC ** 3 == ncd
+    rng = np.random.default_rng(1)
+
+    def interior(a):
+        g = np.zeros(a.shape, bool)
+        g[1:-1, 1:-1, 1:-1] = True
+        return np.where(g, a, 0.0)
+
+    xc = fem_inputs.uniform_pm1(11, ncd)
+    xcm, xfm = interior(xc.reshape(NC, NC, NC)), interior(x7.reshape(NF, NF, NF))
+    out = xd.clone()
+    F.mg_prolongate_add(L, dev(xc), out)
+    fs = np.vstack([rng.integers(0, NF, (300, 3)), [[0, 0, 0], [NF - 1, 5, 7], [1, 1, 1], [NF - 2, NF - 2, NF - 2],
+                                                    [128, 256, 8], [129, NF - 2, 1]]])
+    idx = fs[:, 0] + NF * (fs[:, 1] + NF * fs[:, 2])
+    got = host(out[torch.from_numpy(idx).cuda()])
+    for (fx, fy, fz), g, i in zip(fs, got, idx):
+        e = x7[i]
+        if 0 < fx < NF - 1 and 0 < fy < NF - 1 and 0 < fz < NF - 1:
+            ix, iy, iz = (np.nonzero(P1[f])[0] for f in (fx, fy, fz))
+            e += np.einsum("c,b,a,cba->", P1[fz, iz], P1[fy, iy], P1[fx, ix], xcm[np.ix_(iz, iy, ix)])
+        assert abs(g - e) <= 1e-12 * 4, (fx, fy, fz)
+    del out
+    rc = torch.full((ncd,), 3.0, dtype=torch.float64, device="cuda")
+    F.mg_restrict(L, xd, rc)
+    cs = np.vstack([rng.integers(0, NC, (300, 3)), [[0, 0, 0], [NC - 1, 3, 3], [1, 1, 1], [NC - 2, NC - 2, NC - 2],
+                                                    [64, 128, 4], [65, 1, NC - 2]]])
+    idx = cs[:, 0] + NC * (cs[:, 1] + NC * cs[:, 2])
+    got = host(rc[torch.from_numpy(idx).cuda()])
+    for (cx, cy, cz), g in zip(cs, got):
+        e = 0.0
+        if 0 < cx < NC - 1 and 0 < cy < NC - 1 and 0 < cz < NC - 1:
+            jx, jy, jz = (np.nonzero(P1[:, c])[0] for c in (cx, cy, cz))
+            e = np.einsum("c,b,a,cba->", P1[jz, cz], P1[jy, cy], P1[jx, cx], xfm[np.ix_(jz, jy, jx)])
+        assert abs(g - e) <= 1e-12 * 30, (cx, cy, cz)
 
 
 @pytest.mark.parametrize("k", [1, 2, 4, 6, 8])

@@ -561,6 +561,36 @@ def run_ours(args, w):
         F.fem_profile_read(reset=True)
         del xsm
 
+    # finest-level transfers (R8; node-grid kernels on C4): x_f += P x_c reads x_c, reads and writes
+    # x_f (16 B per fine + 8 B per coarse DoF); r_c = P^T (b - A x) reads two fine vectors, writes r_c
+    transfers = None
+    if world == 1 and w.method == fem_inputs.CG and F.n_levels > 1:
+        fine = F.n_levels - 1
+        ncd = F.level_info(fine - 1)[0]
+        xc = torch.from_numpy(fem_inputs.uniform_pm1(3, ncd)).cuda()
+        rc = torch.zeros_like(xc)
+        xf = b.clone()
+
+        def timed_us(fn, reps=10):
+            fn()
+            torch.cuda.synchronize()
+            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_.record(stream)
+            for _ in range(reps):
+                fn()
+            e_.record(stream)
+            torch.cuda.synchronize()
+            return s_.elapsed_time(e_) * 1e3 / reps
+
+        p_us = timed_us(lambda: F.mg_prolongate_add(fine, xc, xf))
+        r_us = timed_us(lambda: F.mg_restrict(fine, b, rc))
+        transfers = {"prolongate_add_us": p_us, "prolongate_algorithmic_bytes": 16 * n + 8 * ncd,
+                     "restrict_us": r_us, "restrict_algorithmic_bytes": 8 * n + 8 * ncd,
+                     "note": "finest level, standalone; the restriction here reads one fine vector (P^T b) and "
+                             "includes the zero fill of the coarse vector"}
+        F.fem_profile_read(reset=True)
+        del xc, rc, xf
+
     # end to end through the C ABI with host buffers (copies inside the timed region)
     bh = b.cpu().pin_memory()
     xh = torch.zeros(n, dtype=torch.float64).pin_memory()
@@ -596,6 +626,9 @@ def run_ours(args, w):
         "peak_source": hbm_src}
     if smoother:
         smoother["hbm_frac"] = smoother["achieved_gbs"] / hbm
+    if transfers:
+        transfers["prolongate_hbm_frac"] = transfers["prolongate_algorithmic_bytes"] / (transfers["prolongate_add_us"] * 1e-6) / 1e9 / hbm
+        transfers["restrict_hbm_frac"] = transfers["restrict_algorithmic_bytes"] / (transfers["restrict_us"] * 1e-6) / 1e9 / hbm
     bytes_per_launch = algorithmic_apply_bytes(w, n)
     avg_apply_s = apply_ms * 1e-3 / max(apply_launches, 1)
     achieved = bytes_per_launch / avg_apply_s / 1e9
@@ -638,6 +671,7 @@ def run_ours(args, w):
                   "hbm_frac": algorithmic_apply_bytes(w, F.n_global) / apply_s / 1e9 / hbm},
         "clocks": clk,
         "smoother": smoother,
+        "transfers": transfers,
         "e2e": {"value": e2e_value, "unit": "DoF/s", "h2d_bytes_per_step": 16 * n,
                 "d2h_bytes_per_step": 8 * n},
         "gpu_launches": launches,

@@ -488,7 +488,9 @@ __global__ void restrict_elem_kernel(TransferArgs a, Embed<K, DG> E, const doubl
 // sweeps stay in the thread's registers with compile-time E operands.  Ownership and
 // constraints are exactly those of the element form (half-open cells, last cell closed),
 // so the z-slab exchanges around the transfers are unchanged.
-constexpr int kGridThreads = 160;   // 2k TXC fine nodes (<= 128) + the closing node of the last strip
+#ifndef FEM_GT_SPAN
+#define FEM_GT_SPAN 64              // fine x-nodes per strip = 2 SPAN (k | SPAN) or the next lower multiple of 2k
+#endif
 #ifndef FEM_GT_MINB
 #define FEM_GT_MINB 4               // resident blocks per SM the register allocation aims at
 #endif
@@ -497,6 +499,9 @@ constexpr int kGridThreads = 160;   // 2k TXC fine nodes (<= 128) + the closing 
 #endif
 #ifndef FEM_GT_RPIPE
 #define FEM_GT_RPIPE 0              // restriction: software-pipelined plane loads
+#endif
+#ifndef FEM_GT_RPL
+#define FEM_GT_RPL 1                // restriction: fine planes loaded per batch
 #endif
 #ifndef FEM_GT_RGROUPS
 #define FEM_GT_RGROUPS 2            // restriction: threads per coarse node in the x sweep
@@ -507,14 +512,15 @@ constexpr int kGridThreads = 160;   // 2k TXC fine nodes (<= 128) + the closing 
 
 template <int K>
 struct GridTile {
-  static constexpr int TXC = 64 / K;          // coarse cells per strip
+  static constexpr int TXC = FEM_GT_SPAN / K; // coarse cells per strip
   static constexpr int FX = 2 * K * TXC;      // fine nodes per strip (half-open)
   static constexpr int CW = K * TXC + 1;      // coarse nodes per strip (closed)
+  static constexpr int THREADS = (FX + 1 + 31) / 32 * 32;   // FX fine nodes + the closing node of the last strip
 };
 
 // xf += P xc
 template <int K>
-__global__ void __launch_bounds__(kGridThreads, FEM_GT_MINB)
+__global__ void __launch_bounds__(GridTile<K>::THREADS, FEM_GT_MINB)
 prolongate_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restrict__ xc,
                        double* __restrict__ xf) {
   FEM_PDL_ENTRY();
@@ -522,7 +528,7 @@ prolongate_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restri
   __shared__ double s_c[N * N][CW + 1];
   __shared__ double sE[M][N];
   const int tid = threadIdx.x;
-  for (int i = tid; i < M * N; i += kGridThreads) sE[i / N][i % N] = E.E[i / N][i % N];
+  for (int i = tid; i < M * N; i += GridTile<K>::THREADS) sE[i / N][i % N] = E.E[i / N][i % N];
   const int cx0 = blockIdx.x * TXC, cy = blockIdx.y, cz = blockIdx.z;
   const int ncx = min(TXC, a.nc0 - cx0);
   const bool last_x = cx0 + ncx == a.nc0, last_y = cy == a.nc1 - 1, last_z = a.czc0 + cz == a.ncz - 1;
@@ -590,7 +596,7 @@ prolongate_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restri
 
 // xc += P^T (bf - axf)   [axf may be null]; xc zeroed by the caller (atomics, as the element form)
 template <int K, bool AX>
-__global__ void __launch_bounds__(kGridThreads, FEM_GT_RMINB)
+__global__ void __launch_bounds__(GridTile<K>::THREADS, FEM_GT_RMINB)
 restrict_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restrict__ bf,
                      const double* __restrict__ axf, double* __restrict__ xc) {
   FEM_PDL_ENTRY();
@@ -599,7 +605,7 @@ restrict_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restrict
   __shared__ double s_u[N * N][SW];
   __shared__ double sE[M][N];
   const int tid = threadIdx.x;
-  for (int i = tid; i < M * N; i += kGridThreads) sE[i / N][i % N] = E.E[i / N][i % N];
+  for (int i = tid; i < M * N; i += GridTile<K>::THREADS) sE[i / N][i % N] = E.E[i / N][i % N];
   const int cx0 = blockIdx.x * TXC, cy = blockIdx.y, cz = blockIdx.z;
   const int ncx = min(TXC, a.nc0 - cx0);
   const bool last_x = cx0 + ncx == a.nc0, last_y = cy == a.nc1 - 1, last_z = a.czc0 + cz == a.ncz - 1;
@@ -659,6 +665,17 @@ restrict_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restrict
 #pragma unroll
       for (int s = 0; s < M; ++s) cur[s] = nxt[s];
     }
+#elif FEM_GT_RPL == 2
+    // two planes' loads in flight before the first is reduced
+#pragma unroll
+    for (int t = 0; t < M; t += 2) {
+      double v0[M], v1[M];
+      const bool u0 = plane_used(t), u1 = t + 1 < M && plane_used(t + 1);
+      if (u0) load_plane(t, v0);
+      if (u1) load_plane(t + 1, v1);
+      if (u0) add_plane(t, v0);
+      if (u1) add_plane(t + 1, v1);
+    }
 #else
 #pragma unroll
     for (int t = 0; t < M; ++t) {
@@ -675,9 +692,9 @@ restrict_grid_kernel(TransferArgs a, Embed<K, false> E, const double* __restrict
   }
   __syncthreads();
   // x sweep: coarse node I of the strip collects the fine positions 2I - (2k-1) .. 2I + (2k-1);
-  // the (j, l) pairs of a node are dealt to kGridRG threads
+  // the (j, l) pairs of a node are dealt to RG threads
   constexpr int CWmax = GridTile<K>::CW;
-  constexpr int RG = kGridThreads / CWmax < FEM_GT_RGROUPS ? kGridThreads / CWmax : FEM_GT_RGROUPS;
+  constexpr int RG = GridTile<K>::THREADS / CWmax < FEM_GT_RGROUPS ? GridTile<K>::THREADS / CWmax : FEM_GT_RGROUPS;
   const int I = tid % CWmax, g = tid / CWmax;
   if (g >= RG || I > K * ncx) return;
   const int gcx = K * cx0 + I;
@@ -942,7 +959,7 @@ void prolongate_kd(fem_ctx* h, const Level& c, const Level& f, const double* xc,
   if constexpr (!DG && K <= 4) {
     if (c.n_cells >= h->grid_transfer_min_cells) {
       const dim3 grid((unsigned)((c.n[0] + GridTile<K>::TXC - 1) / GridTile<K>::TXC), (unsigned)c.n[1], (unsigned)c.n[2]);
-      launch_pdl(h, prolongate_grid_kernel<K>, grid, kGridThreads, 0, transfer_args(h, c, f),
+      launch_pdl(h, prolongate_grid_kernel<K>, grid, GridTile<K>::THREADS, 0, transfer_args(h, c, f),
                  make_embed<K, DG>(h->tab), xc, xf);
       count_launch();
       check_launch("prolongate_grid_kernel");
@@ -972,10 +989,10 @@ void restrict_kd(fem_ctx* h, const Level& c, const Level& f, const double* bf, c
     if (c.n_cells >= h->grid_transfer_min_cells) {
       const dim3 grid((unsigned)((c.n[0] + GridTile<K>::TXC - 1) / GridTile<K>::TXC), (unsigned)c.n[1], (unsigned)c.n[2]);
       if (axf)
-        launch_pdl(h, restrict_grid_kernel<K, true>, grid, kGridThreads, 0, transfer_args(h, c, f),
+        launch_pdl(h, restrict_grid_kernel<K, true>, grid, GridTile<K>::THREADS, 0, transfer_args(h, c, f),
                    make_embed<K, DG>(h->tab), bf, axf, xc);
       else
-        launch_pdl(h, restrict_grid_kernel<K, false>, grid, kGridThreads, 0, transfer_args(h, c, f),
+        launch_pdl(h, restrict_grid_kernel<K, false>, grid, GridTile<K>::THREADS, 0, transfer_args(h, c, f),
                    make_embed<K, DG>(h->tab), bf, axf, xc);
       count_launch();
       check_launch("restrict_grid_kernel");

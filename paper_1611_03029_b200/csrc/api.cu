@@ -1537,8 +1537,24 @@ int fem_rhs(fem_handle h, double* b, int64_t nb) {
 }
 
 
+namespace {
+int cg_solve_impl(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, double rtol,
+                  int32_t maxit, int32_t* iters, double* relres, bool zero_start);
+}
+
 int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, double rtol,
              int32_t maxit, int32_t* iters, double* relres) {
+  return cg_solve_impl(h, b, nb, x, nx, rtol, maxit, iters, relres, false);
+}
+
+int cg_solve_zero(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, double rtol,
+                  int32_t maxit, int32_t* iters, double* relres) {
+  return cg_solve_impl(h, b, nb, x, nx, rtol, maxit, iters, relres, true);
+}
+
+namespace {
+int cg_solve_impl(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, double rtol,
+                  int32_t maxit, int32_t* iters, double* relres, bool zero_start) {
   int result = FEM_OK;
   int rc = guarded([&] {
     check_handle(h);
@@ -1552,7 +1568,9 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     setup_coarse(h);
     const double* db = in_vec(h, b, nb, 0);
     bool st;
-    double* dx = out_vec(h, x, nx, 1, true, &st);
+    // zero_start: x is output only (a host x is not uploaded, a device x is cleared here)
+    double* dx = out_vec(h, x, nx, 1, !zero_start, &st);
+    if (zero_start) launch_zero(h, dx, n);
     if (!L.pcg_r) {
       L.pcg_r = valloc(L);
       L.pcg_p = valloc(L);
@@ -1564,10 +1582,10 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
     if (is_cg(h)) launch_set_constrained(h, L, db, dx);
     // r_0 = b - A x_0; a zero start (the usual call) skips the operator apply
     dot(h, L, db, db, 6);
-    dot(h, L, dx, dx, 7);
+    if (!zero_start) dot(h, L, dx, dx, 7);
     FEM_CUDA_TRY(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * 8, cudaMemcpyDeviceToHost, h->stream));
     FEM_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    if (h->hscal[7] == 0.0) {
+    if (zero_start || h->hscal[7] == 0.0) {
       launch_copy(h, r, db, n);
       h->hscal[2] = h->hscal[6];
     } else {
@@ -1675,6 +1693,7 @@ int cg_solve(fem_handle h, const double* b, int64_t nb, double* x, int64_t nx, d
   });
   return rc != FEM_OK ? rc : result;
 }
+}  // namespace
 
 int cg_history(fem_handle h, double* rel, int32_t cap, int32_t* n) {
   return guarded([&] {

@@ -74,6 +74,7 @@ def _load():
         "fem_diagonal": (C.c_int, [P, P, I64]),
         "mg_vcycle": (C.c_int, [P, P, I64, P, I64]),
         "cg_solve": (C.c_int, [P, P, I64, P, I64, D, I32, C.POINTER(I32), C.POINTER(D)]),
+        "cg_solve_zero": (C.c_int, [P, P, I64, P, I64, D, I32, C.POINTER(I32), C.POINTER(D)]),
         "fem_rhs": (C.c_int, [P, P, I64]),
         "cg_history": (C.c_int, [P, C.POINTER(D), I32, C.POINTER(I32)]),
         "fem_level_info": (C.c_int, [P, I32, C.POINTER(I64), C.POINTER(I32)]),
@@ -115,7 +116,7 @@ _lib = _load()
 # exported symbol list (tests check it against include/fem.h)
 SYMBOLS = ("fem_default_options", "fem_setup", "fem_partition", "fem_nccl_unique_id",
            "fem_local_group_create", "fem_local_group_destroy", "fem_info", "fem_apply", "fem_diagonal", "mg_vcycle",
-           "cg_solve", "cg_history", "fem_rhs", "fem_level_info", "fem_level_apply", "fem_level_diagonal",
+           "cg_solve", "cg_solve_zero", "cg_history", "fem_rhs", "fem_level_info", "fem_level_apply", "fem_level_diagonal",
            "fem_level_lambda", "fem_level_geometry", "mg_smooth", "mg_prolongate_add", "mg_restrict",
            "mg_coarse_solve", "fem_sync", "fem_kernel_launches", "fem_profile_read", "fem_profile_read_bytes", "fem_profile_mode",
            "fem_last_error",
@@ -301,6 +302,15 @@ class Fem:
         px, nx = _vec(x, True)
         its, rel = C.c_int32(), C.c_double()
         rc = _check(_lib.cg_solve(self.h, pb, nb, px, nx, rtol, maxit, C.byref(its), C.byref(rel)),
+                    (FEM_OK, FEM_NOT_CONVERGED))
+        return its.value, rel.value, rc == FEM_OK
+
+    def cg_solve_zero(self, b, x, rtol=1e-10, maxit=1000):
+        """cg_solve from x = 0; x is output only (a host x is not uploaded)."""
+        pb, nb = _vec(b)
+        px, nx = _vec(x, True)
+        its, rel = C.c_int32(), C.c_double()
+        rc = _check(_lib.cg_solve_zero(self.h, pb, nb, px, nx, rtol, maxit, C.byref(its), C.byref(rel)),
                     (FEM_OK, FEM_NOT_CONVERGED))
         return its.value, rel.value, rc == FEM_OK
 

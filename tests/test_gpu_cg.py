@@ -447,3 +447,22 @@ def test_grid_and_element_transfers_match_oracle(k, cells, bc, min_cells, monkey
         F.mg_restrict(l, xf, rc)
         assert relmax(rc, mg.restrict(l, xf)) <= 1e-12, ("restrict", l)
     F.close()
+
+
+def test_cg_solve_zero_ignores_x_on_entry_and_equals_cg_solve_from_zero():
+    F, m = make((8, 8, 8), 3, 0.05, MIXED)
+    n = m.cg_n_dofs()
+    b = torch.zeros(n, dtype=torch.float64, device="cuda")
+    F.fem_rhs(b)
+    x1 = torch.zeros_like(b)
+    its1, rr1, ok1 = F.cg_solve(b, x1, rtol=1e-10)
+    h1 = F.cg_history()
+    x2 = torch.full_like(b, float("nan"))            # contents on entry must not matter
+    its2, rr2, ok2 = F.cg_solve_zero(b, x2, rtol=1e-10)
+    assert ok1 and ok2 and its1 == its2
+    assert np.allclose(F.cg_history(), h1, rtol=1e-9, atol=0)
+    assert relmax(host(x2), host(x1)) <= 1e-12
+    xh = np.full(n, 1e300)                            # host vectors: x is not uploaded
+    its3, rr3, ok3 = F.cg_solve_zero(host(b), xh, rtol=1e-10)
+    assert ok3 and its3 == its1 and relmax(xh, host(x1)) <= 1e-12
+    F.close()

@@ -470,7 +470,10 @@ void chebyshev(fem_ctx* h, Level& L, const double* b, const double* x_in, double
   // step 1
   double* xn = (p == 1) ? x_out : next(x_in, nullptr);
   if (x_in == nullptr) {
-    launch_cheb_step(h, L, xn, nullptr, nullptr, b, nullptr, 0.0, 1.0 / theta, false);
+    if (st2 && L.dinv_cls && h->cheb_first_cls)
+      launch_cheb_first_cls(h, L, xn, b, 1.0 / theta);
+    else
+      launch_cheb_step(h, L, xn, nullptr, nullptr, b, nullptr, 0.0, 1.0 / theta, false);
   } else {
     step(x_in, nullptr, xn, 0.0, 1.0 / theta);
   }
@@ -1237,6 +1240,7 @@ int fem_setup(const fem_mesh* mesh, int32_t degree, int32_t method, const fem_op
     if (const char* e = std::getenv("FEM_CG_GEO_FLY")) h->cg_geo_fly = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_ST_MIN_CELLS")) h->stencil2_min_cells = std::atoll(e);
     if (const char* e = std::getenv("FEM_GT_MIN_CELLS")) h->grid_transfer_min_cells = std::atoll(e);
+    if (const char* e = std::getenv("FEM_CHEB_FIRST_CLS")) h->cheb_first_cls = std::atoi(e) != 0;
     if (const char* e = std::getenv("FEM_ST_EZ")) h->stencil_ez = std::atoi(e);
     build_tables(degree, h->tab);
     h->red = dalloc(16 * kRedBlocks + 16);   // partial sums + 16 reduction counters (zeroed)

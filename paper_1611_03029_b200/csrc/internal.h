@@ -239,6 +239,7 @@ struct fem_ctx {
   bool dg_fgeo_fly = false;            // FEM_DG_FGEO_FLY=1: deformed SIPG recomputes the face geometry (measured slower: C5 7.28 vs 5.35 ms)
   bool stencil = false;                // FEM_STENCIL=1: atomic-free global Kronecker stencil on Cartesian CG levels (K1s, study)
   bool stencil2 = true;                // FEM_STENCIL2=0: warp-specialised assembled stencil (K1t) off
+  bool cheb_first_cls = true;   // FEM_CHEB_FIRST_CLS: first Chebyshev step from x = 0 reads D^-1 from the class table (K1t levels)
   int64_t grid_transfer_min_cells = 4096;  // FEM_GT_MIN_CELLS: node-grid CG transfers (k <= 4) onto coarse levels with >= this many local cells
   int64_t stencil2_min_cells = 32768;  // FEM_ST_MIN_CELLS: K1t on single-rank Cartesian CG levels with >= this many cells
                                        // (C4 solve, 5 its: 4096 118.6 ms, 32768 116.9, 262144 116.4-119.2, 2097152 124.4: below
@@ -269,6 +270,8 @@ void launch_splitmix(fem_ctx* h, const Level& L, uint64_t seed, double* s);
 // Chebyshev three-term step:  xn = x + c1 (x - xo) + c2 Dinv (b - Ax); Ax <- 0.
 void launch_cheb_step(fem_ctx* h, const Level& L, double* xn, const double* x, const double* xo,
                       const double* b, double* ax, double c1, double c2, bool has_xo);
+// x_1 = c2 D^-1 b from the D^-1 class table (Cartesian CG levels with L.dinv_cls)
+void launch_cheb_first_cls(fem_ctx* h, const Level& L, double* xn, const double* b, double c2);
 // reductions into h->scal[slot] (device)
 void launch_dot(fem_ctx* h, const double* a, const double* b, int64_t n, int slot);
 // PCG pieces

@@ -748,6 +748,32 @@ __global__ void cheb_step_kernel(double* __restrict__ xn, const double* __restri
   }
 }
 
+// First Chebyshev step from x = 0 on a Cartesian CG level with a D^-1 class table (api.cu:
+// (k+2)^3 values, class per direction 0 first node, r inside an element, k interior vertex, k+1
+// last node): x_1 = c2 D^-1 b reads b and writes x_1 only (16 B per DoF; the D^-1 vector of the
+// generic kernel is a third stream: 505 -> 3xx us on the finest C4 level)
+template <int K>
+__global__ void cheb_first_cls_kernel(double* __restrict__ xn, const double* __restrict__ b,
+                                      const double* __restrict__ dcls, double c2, int NX, int NY, int NZ) {
+  FEM_PDL_ENTRY();
+  constexpr int ZPT = 8;   // z planes per thread: the (x, y) class and index arithmetic once per 8 nodes
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= NX * NY) return;
+  const int gy = p / NX, gx = p - gy * NX;
+  auto ncls = [](int g, int nn) { return g == 0 ? 0 : g == nn - 1 ? K + 1 : (g % K == 0 ? K : g % K); };
+  const double* __restrict__ dxy = dcls + ncls(gx, NX) + (K + 2) * ncls(gy, NY);
+  const int gz0 = blockIdx.y * ZPT;
+  const int64_t plane = (int64_t)NX * NY;
+  const double* __restrict__ pb = b + p + plane * gz0;
+  double* __restrict__ px = xn + p + plane * gz0;
+  double v[ZPT];
+#pragma unroll
+  for (int j = 0; j < ZPT; ++j) v[j] = gz0 + j < NZ ? pb[plane * j] : 0.0;
+#pragma unroll
+  for (int j = 0; j < ZPT; ++j)
+    if (gz0 + j < NZ) px[plane * j] = c2 * __ldg(dxy + (K + 2) * (K + 2) * ncls(gz0 + j, NZ)) * v[j];
+}
+
 __global__ void axpby_kernel(double* __restrict__ y, const double* __restrict__ x, double a, double b,
                              int64_t n) {
   FEM_PDL_ENTRY();
@@ -1090,6 +1116,21 @@ void launch_cheb_step(fem_ctx* h, const Level& L, double* xn, const double* x, c
   if (clear) L.t_zero = true;
   count_launch();
   check_launch("cheb_step_kernel");
+}
+
+void launch_cheb_first_cls(fem_ctx* h, const Level& L, double* xn, const double* b, double c2) {
+  const int NX = L.nn[0], NY = L.nn[1], NZ = L.nn[2];
+  const dim3 grid((unsigned)(((int64_t)NX * NY + 255) / 256), (unsigned)((NZ + 7) / 8));
+  const double* dcls = L.dinv_cls;
+  switch (h->k) {
+    case 1: launch_pdl(h, cheb_first_cls_kernel<1>, grid, 256, 0, xn, b, dcls, c2, NX, NY, NZ); break;
+    case 2: launch_pdl(h, cheb_first_cls_kernel<2>, grid, 256, 0, xn, b, dcls, c2, NX, NY, NZ); break;
+    case 3: launch_pdl(h, cheb_first_cls_kernel<3>, grid, 256, 0, xn, b, dcls, c2, NX, NY, NZ); break;
+    case 4: launch_pdl(h, cheb_first_cls_kernel<4>, grid, 256, 0, xn, b, dcls, c2, NX, NY, NZ); break;
+    default: throw Error{FEM_E_ARG, "class-table Chebyshev step: k in 1..4"};
+  }
+  count_launch();
+  check_launch("cheb_first_cls_kernel");
 }
 
 // reduction grid: deterministic for a given n (the finisher sums gridDim.x partials in order)

@@ -46,7 +46,9 @@
 namespace fem {
 
 // Pipeline depths per MODE (r02c A/B on C4, apply / smoother step): A/B planes in flight
-// (x-stage -> y-stage hand-off) 2 (3: 766 vs 754 us apply, 2044 vs 1706 us smoother);
+// (x-stage -> y-stage hand-off) 2 for the apply (3: 766 vs 754 us apply, 2044 vs 1706 us smoother in
+// r02c; re-measured at the end of round 2 on the final fused step: 3 is 1% faster there, 1443 -> 1428 us
+// per smoother step, and together with the symmetric tables 1443 -> 1412-1425 us: 3 for MODE 1 / 2);
 // x~ planes in flight 3 (4: 754 -> 748 us apply; smoother 1706 -> 1667 us with one element
 // of L2 prefetch; 2: 1863 us).  The LR * SX - THREADS extra x-stage items of a plane
 // rotate over the warps with the plane (FEM_ST_ROT; fixed on warps 0-1: 766 vs 754 us):
@@ -58,7 +60,7 @@ namespace fem {
 #define FEM_ST_NAB0 2
 #endif
 #ifndef FEM_ST_NAB1
-#define FEM_ST_NAB1 2
+#define FEM_ST_NAB1 3
 #endif
 #ifndef FEM_ST_NB0
 #define FEM_ST_NB0 3
@@ -72,8 +74,8 @@ namespace fem {
 #ifndef FEM_ST_SYM   // exactly symmetric 1-D tables (RefTab) in the apply
 #define FEM_ST_SYM 1
 #endif
-#ifndef FEM_ST_SYMALL   // ... and in the fused Chebyshev step
-#define FEM_ST_SYMALL 0
+#ifndef FEM_ST_SYMALL   // ... and in the fused Chebyshev step (slower there in r02k, 1% faster on the final kernel)
+#define FEM_ST_SYMALL 1
 #endif
 template <int K, int MODE = 0>
 struct StCfg {

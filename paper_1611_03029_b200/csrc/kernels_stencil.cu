@@ -48,7 +48,8 @@ namespace fem {
 // Pipeline depths per MODE (r02c A/B on C4, apply / smoother step): A/B planes in flight
 // (x-stage -> y-stage hand-off) 2 for the apply (3: 766 vs 754 us apply, 2044 vs 1706 us smoother in
 // r02c; re-measured at the end of round 2 on the final fused step: 3 is 1% faster there, 1443 -> 1428 us
-// per smoother step, and together with the symmetric tables 1443 -> 1412-1425 us: 3 for MODE 1 / 2);
+// per smoother step, and together with the symmetric tables 1443 -> 1412-1425 us: 3 for MODE 1 / 2; MODE 0 re-measured too:
+// 3 planes 664.5 -> 647.2 us per C4 apply, solve unchanged within noise: 3);
 // x~ planes in flight 3 (4: 754 -> 748 us apply; smoother 1706 -> 1667 us with one element
 // of L2 prefetch; 2: 1863 us).  The LR * SX - THREADS extra x-stage items of a plane
 // rotate over the warps with the plane (FEM_ST_ROT; fixed on warps 0-1: 766 vs 754 us):
@@ -57,7 +58,7 @@ namespace fem {
 // and writing one plane per following step (2023 us; with the operands loaded one step
 // early 2517 us, spills) -- extra shared memory costs this kernel more than the burst.
 #ifndef FEM_ST_NAB0
-#define FEM_ST_NAB0 2
+#define FEM_ST_NAB0 3
 #endif
 #ifndef FEM_ST_NAB1
 #define FEM_ST_NAB1 3
